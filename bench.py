@@ -1,0 +1,466 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 warp-primitive path (BASELINE.json metric:
+"Gelem/s + HBM GB/s (% of peak) per warp kernel at 1/2/4/8 B200 vs CPU ref").
+
+Headline workload (one JSON line, `value`): BASELINE config 2 — fp32
+warp-shuffle reduction over 2^30 elements, sharded across the N ranks
+(strong scaling), per-GPU partials combined by an NCCL all-gather and a
+fixed-order fold.  A step = one pass of the hot path over the whole 2^30
+input.  `per_kernel` adds the other BASELINE configs measured in the same run
+(C1 on rank 0 only; C3-C5 sharded like C2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun (N>1) every rank drives one GPU; times are CUDA-event times
+on each rank's stream, max over ranks.  `--impl reference` times the CPU
+restatement of the reference's collapsed loop nests (oracle/collapse_ref.c,
+the reference itself is pure Python and is not installed on the GPU box) on
+the host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Gelem/s + HBM GB/s (% of peak) per warp kernel at 1/2/4/8 B200 vs CPU ref"
+N_C1 = 1 << 20
+N_C2 = 1 << 30
+N_C3 = 1 << 28
+N_C4 = 1 << 28
+N_C5 = 1 << 32
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peak() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        v = float(json.loads(p.read_text())["hbm_gbs"])
+        return v, "measured (MEASURED_PEAKS.json hbm_gbs, torch copy read+write)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(name: str):
+    """dram bytes per launch of `name` from the committed ncu --set full
+    summary (profiles/ncu_traffic.json), or None."""
+    try:
+        d = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
+        return d.get(name)
+    except Exception:
+        return None
+
+
+# ---- clocks sampling (B200_PROFILING.md "clocks DURING the timed region") --
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.path = Path(f"/tmp/wf_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            for line in self.path.read_text().splitlines():
+                f = [x.strip() for x in line.split(",")]
+                if len(f) >= 9:
+                    rows.append(f)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---- distributed plumbing --------------------------------------------------
+def init_dist(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local) if args.impl == "ours" else None
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        dist.init_process_group(backend=backend,
+                                device_id=torch.device("cuda", local) if backend == "nccl" else None)
+    elif args.impl == "ours":
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier_sync(world):
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---- CPU baselines (oracle port of the collapsed loop nests) ---------------
+def cpu_baseline_c2(budget_s: float = 10.0, sample_n: int = 1 << 24) -> dict:
+    """The reference's per-warp-partials f32 reduction, collapsed into
+    block/warp/lane loop nests (oracle/collapse_ref.c), on all host threads;
+    repeated over a bounded sample until ~budget_s."""
+    import numpy as np
+    from oracle import cref, synthetic
+    cref.build()
+    workers = cref.workers_default()
+    x = synthetic.generate("f32_unit", sample_n, seed=1)
+    grid = 64 * workers
+    cref.reduce_f32(x, grid, 256, workers)  # warm
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        cref.reduce_f32(x, grid, 256, workers)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or reps >= 1000:
+            break
+    return {"value": round(sample_n * reps / el / 1e9, 6), "unit": "Gelem/s", "cores": workers,
+            "kind": "port",
+            "sample": f"{reps} x 2^{int(np.log2(sample_n))} fp32 (collapse_ref.c per-warp-partials "
+                      f"shfl_down reduction, grid {grid} x block 256, {workers} threads, "
+                      f"{el:.1f} s)"}
+
+
+def cpu_baseline_kernel(kind: str, budget_s: float) -> dict:
+    import numpy as np
+    from oracle import cref, synthetic
+    workers = cref.workers_default()
+    n = 1 << 24
+    if kind == "c1":
+        x = synthetic.generate("i32_full", N_C1, seed=0)
+        fn, n = (lambda: cref.reduce_i32(x, 8 * workers, 256, workers)), N_C1
+    elif kind == "c3":
+        x = synthetic.generate("i32_full", n, seed=0)
+        fn = lambda: cref.scan_i32(x, 256, workers)  # noqa: E731
+    elif kind == "c4":
+        x = synthetic.generate("i32_full", n, seed=0)
+        fn = lambda: cref.compact_gt0_i32(x, 256, workers)  # noqa: E731
+    else:
+        x = synthetic.generate("u8_uniform", n, seed=0)
+        fn = lambda: cref.hist256_u8(x, 64 * workers, 256, workers)  # noqa: E731
+    fn()
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        fn()
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or reps >= 2000:
+            break
+    return {"value": round(n * reps / el / 1e9, 6), "unit": "Gelem/s", "cores": workers,
+            "kind": "port", "sample": f"{reps} x {n} elements, {el:.1f} s"}
+
+
+# ---- GPU timing helpers -----------------------------------------------------
+def time_launches(fn, steps: int, warmup: int, flush=None):
+    """Per-launch CUDA-event times (ms) on the current stream."""
+    import torch
+    for _ in range(warmup):
+        if flush is not None:
+            flush()
+        fn()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    for s, e in evs:
+        if flush is not None:
+            flush()
+        s.record()
+        fn()
+        e.record()
+    torch.cuda.synchronize()
+    return [s.elapsed_time(e) for s, e in evs]
+
+
+def run_ours(args, rank, world, local) -> dict | None:
+    import torch
+    from paper_2112_10034_b200 import _lib, distributed as wd, ops
+
+    peak, peak_src = measured_peak()
+    dev = torch.device("cuda", local)
+    lo, hi = wd.shard_range(N_C2, rank, world)
+    n_local = hi - lo
+    x = ops.fill_synthetic("f32_unit", n_local, seed=1, base=lo, device=dev)
+    torch.cuda.synchronize()
+
+    # ---- headline: K2 step over the 2^30 job, device-resident inputs ------
+    kern = []
+    launches = 0
+
+    def step(record):
+        nonlocal launches
+        if record:
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            s.record()
+        part = ops.reduce_sum_f32(x, block=256)
+        launches += 1
+        if record:
+            e.record()
+            kern.append((s, e))
+        if world > 1:
+            ops.fold(wd.exchange(part).reshape(-1))
+            launches += 1
+        return part
+
+    for _ in range(args.warmup):
+        step(False)
+    launches = 0
+    barrier_sync(world)
+    with ClockSampler(local) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(args.steps):
+            step(True)
+        t1.record()
+        barrier_sync(world)
+    step_ms = t0.elapsed_time(t1) / args.steps
+    kern_ms = statistics.mean(s.elapsed_time(e) for s, e in kern)
+    step_ms_max = max_over_ranks(step_ms, world)
+    value = N_C2 / (step_ms_max * 1e-3) / 1e9
+    achieved = 4.0 * n_local / (kern_ms * 1e-3) / 1e9
+    gpu_launches = launches
+
+    # ---- e2e through the C-ABI host entry point ---------------------------
+    host = torch.empty(n_local, dtype=torch.float32, pin_memory=True)
+    host.copy_(x)
+    e2e_steps = max(1, min(args.steps, 3))
+    ops.reduce_sum_f32_host(host, device=dev)  # warm (staging + streams)
+    barrier_sync(world)
+    t = time.perf_counter()
+    for _ in range(e2e_steps):
+        v = ops.reduce_sum_f32_host(host, device=dev)
+        if world > 1:  # combine the per-rank partials: all-gather + fixed-order fold
+            part = torch.tensor([v], dtype=torch.float32, device=dev)
+            float(ops.fold(wd.exchange(part).reshape(-1)).item())
+    e2e_ms = (time.perf_counter() - t) * 1e3 / e2e_steps
+    e2e_ms_max = max_over_ranks(e2e_ms, world)
+    del host
+
+    # ---- per-kernel lines for the other BASELINE configs -------------------
+    per = {}
+    if not args.headline_only:
+        per = per_kernel(args, rank, world, local, dev, peak)
+    per["c2_reduce_f32"] = {"gelem_s": round(value, 3), "gbs": round(achieved, 1),
+                            "frac_of_peak": round(achieved / peak, 4),
+                            "kernel_us": round(kern_ms * 1e3, 2), "n": N_C2,
+                            "bytes_per_elem": 4}
+    del x
+    torch.cuda.empty_cache()
+
+    if rank != 0:
+        return None
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_c2(args.cpu_budget)
+        for k, key in (("c1", "c1_reduce_i32"), ("c3", "c3_scan_i32"), ("c4", "c4_compact_i32"),
+                       ("c5", "c5_hist_u8")):
+            if key in per:
+                per[key]["cpu_baseline"] = cpu_baseline_kernel(k, args.cpu_budget / 4)
+    traffic = ncu_traffic("reduce_sum_f32")
+    return {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": "Gelem/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(step_ms_max, 5),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (splitmix64 index hash, generated in HBM)",
+        "config": {
+            "workload": "C2: fp32 warp-shuffle reduction over 2^30 elements sharded across "
+                        f"{world} B200 (NCCL all-gather + fixed-order fold of partials)",
+            "n": N_C2, "block": 256, "parallelism": f"shard{world}",
+            "l2": "inputs larger than L2 (4 GiB vs 126 MB), no flush needed",
+        },
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "kernel": "reduce_sum_f32 (K2)", "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": 4 * n_local},
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(N_C2 / (e2e_ms_max * 1e-3) / 1e9, 4), "unit": "Gelem/s",
+                "h2d_bytes_per_step": 4 * n_local, "d2h_bytes_per_step": 4,
+                "path": "wf_reduce_sum_f32_host (pinned host -> chunked H2D overlapped with K2 "
+                        "-> D2H of the result)", "steps": e2e_steps},
+        "gpu_launches": gpu_launches,
+        "clocks": clk.summary(),
+        "per_kernel": per,
+    }
+
+
+def per_kernel(args, rank, world, local, dev, peak) -> dict:
+    import torch
+    from paper_2112_10034_b200 import distributed as wd, ops
+    res = {}
+    steps, warm = max(5, args.steps), max(3, args.warmup)
+
+    def stats(times_ms, n_elems, bytes_per_elem, n_total):
+        ms = statistics.mean(times_ms)
+        ms_max = max_over_ranks(ms, world)
+        gbs = bytes_per_elem * n_elems / (ms * 1e-3) / 1e9
+        return {"gelem_s": round(n_total / (ms_max * 1e-3) / 1e9, 3), "gbs": round(gbs, 1),
+                "frac_of_peak": round(gbs / peak, 4), "kernel_us": round(ms * 1e3, 2),
+                "n": n_total, "bytes_per_elem": bytes_per_elem}
+
+    # C1 (single GPU by definition): 2^20 int32, block 256, L2 flushed
+    if rank == 0:
+        x1 = ops.fill_synthetic("i32_full", N_C1, seed=0, device=dev)
+        flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        t = time_launches(lambda: ops.reduce_sum_i32(x1, block=256), steps, warm,
+                          flush=lambda: flush_buf.fill_(1))
+        res["c1_reduce_i32"] = stats(t, N_C1, 4, N_C1)
+        res["c1_reduce_i32"]["l2"] = "flushed (256 MiB write) before every launch"
+        del x1, flush_buf
+    # C3 scan
+    lo, hi = wd.shard_range(N_C3, rank, world)
+    x = ops.fill_synthetic("i32_full", hi - lo, seed=0, base=lo, device=dev)
+    y = torch.empty_like(x)
+    t = time_launches(lambda: wd.scan_inclusive_i32(x, y), steps, warm)
+    res["c3_scan_i32"] = stats(t, hi - lo, 8 if world == 1 else 12, N_C3)
+    # C4 compaction
+    out = torch.empty_like(x)
+    t = time_launches(lambda: wd.compact_gt0_i32(x, out), steps, warm)
+    res["c4_compact_i32"] = stats(t, hi - lo, 6, N_C4)
+    res["c4_compact_i32"]["bytes_per_elem_note"] = "4 B read + 4 B x selectivity (~0.5) written"
+    del x, y, out
+    torch.cuda.empty_cache()
+    # C5 histogram
+    lo, hi = wd.shard_range(N_C5, rank, world)
+    u = ops.fill_synthetic("u8_uniform", hi - lo, seed=0, base=lo, device=dev)
+    t = time_launches(lambda: wd.histogram256_u8(u), steps, warm)
+    res["c5_hist_u8"] = stats(t, hi - lo, 1, N_C5)
+    del u
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_reference(args, rank, world) -> dict | None:
+    """CPU arm: the collapsed-loop restatement of the reference on the host
+    cores (rank 0 only); each step a bounded sample of the C2 workload."""
+    if rank != 0:
+        return None
+    import numpy as np
+    from oracle import cref, synthetic
+    cref.build()
+    workers = cref.workers_default()
+    sample_n = 1 << 24
+    x = synthetic.generate("f32_unit", sample_n, seed=1)
+    grid = 64 * workers
+    for _ in range(args.warmup):
+        cref.reduce_f32(x, grid, 256, workers)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        cref.reduce_f32(x, grid, 256, workers)
+        times.append(time.perf_counter() - t)
+    ms = statistics.mean(times) * 1e3
+    value = sample_n / (ms * 1e-3) / 1e9
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "Gelem/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "C2: fp32 warp-shuffle reduction over 2^30 elements "
+                               "(CPU: bounded 2^24-element sample per step)",
+                   "n": N_C2, "block": 256, "parallelism": f"cpu{workers}"},
+        "cpu_baseline": {"value": round(value, 6), "unit": "Gelem/s", "cores": workers,
+                         "kind": "port",
+                         "sample": f"2^24 fp32 per step through oracle/collapse_ref.c "
+                                   f"(per-warp-partials shfl_down kernel collapsed into "
+                                   f"block/warp/lane loops, grid {grid} x 256, {workers} threads)"},
+        "e2e": {"value": round(value, 6), "unit": "Gelem/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--headline-only", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup raised to 3 (timing rules)")
+        args.warmup = 3
+    if args.impl == "reference":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        line = run_reference(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    rank, world, local = init_dist(args)
+    line = run_ours(args, rank, world, local)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

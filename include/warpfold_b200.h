@@ -1,0 +1,190 @@
+/*
+ * warpfold_b200.h — C ABI of the B200-native warp-primitive path.
+ *
+ * This is the drop-in boundary for the data-parallel path that the warpfold
+ * CPU reference (arXiv 2112.10034, "COX" hierarchical collapsing) emulates.
+ * In the reference that path is
+ *
+ *     launch(hybrid_transform(kernel, cfg), cfg, memory, args)
+ *         runtime/launch.py:90          (block scheduling over a fork pool)
+ *         passes/pipeline.py:103-179    (collapse warps/blocks into loop nests)
+ *         passes/warp_lower.py:17-88    (lane-array emulation of shfl / vote)
+ *         interp/mpmd.py:237-255        (per-block interpreter, the CPU hot loop)
+ *
+ * Here every one of those layers is replaced by a hand-written sm_100a kernel
+ * reached through the plain-C entry points below.  Conventions:
+ *
+ *   - Pointers are device pointers unless the name says `host_`.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *   - The library never allocates or frees caller buffers.  Scratch state
+ *     (tile descriptors, block partials, tickets) lives in a caller-provided
+ *     workspace of wf_workspace_bytes() bytes that must be zero-filled once
+ *     (wf_workspace_init) and may then be reused by any number of calls of
+ *     the same op on the same stream.  Kernels leave it ready for reuse.
+ *   - Every call is stream-ordered and asynchronous; results are valid once
+ *     the stream is synchronised (the Python `launch` does that, preserving
+ *     the reference's join semantics, runtime/launch.py:1-8).
+ *   - Return value: 0 = OK, > 0 = cudaError_t, < 0 = WF_ERR_* below.
+ *     wf_last_error() returns a thread-local message for the last failure.
+ *     The Python wrapper maps WF_ERR_CONFIG -> ConfigError, WF_ERR_ARG ->
+ *     LaunchError, WF_ERR_UNSUPPORTED -> UnsupportedFeatureError and CUDA
+ *     errors -> ExecutionError (reference errors.py:22-47).
+ *
+ * Integer arithmetic wraps modulo 2^32 exactly like the reference's i32
+ * (numerics.py:20-22); f32 is IEEE single precision with a fixed,
+ * run-to-run reproducible association order.
+ */
+#ifndef WARPFOLD_B200_H
+#define WARPFOLD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WF_ABI_VERSION 1
+
+/* error codes (negative); positive values are cudaError_t */
+#define WF_OK 0
+#define WF_ERR_CONFIG (-1)      /* bad block/grid/width (config.py:26-41)      */
+#define WF_ERR_ARG (-2)         /* bad pointer/size/alignment (launch.py:28-46) */
+#define WF_ERR_COMM (-3)        /* reserved for the cross-GPU exchange          */
+#define WF_ERR_UNSUPPORTED (-4) /* op/variant not provided (errors.py:18-19)    */
+#define WF_ERR_WORKSPACE (-5)   /* workspace missing or too small               */
+#define WF_ERR_EXEC (-6)        /* device-side fault flagged by a kernel        */
+
+/* op ids for wf_workspace_bytes */
+#define WF_OP_REDUCE_SUM_I32 1
+#define WF_OP_REDUCE_SUM_F32 2
+#define WF_OP_SCAN_INCLUSIVE_I32 3
+#define WF_OP_COMPACT_GT0_I32 4
+#define WF_OP_HISTOGRAM256_U8 5
+#define WF_OP_WARP_COLLECTIVE 6
+
+/* warp collective kinds for wf_warp_collective (Appendix B of SURVEY.md) */
+#define WF_COLL_SHFL_DOWN 0 /* passes/warp_lower.py:36-45 shuffle_down      */
+#define WF_COLL_SHFL_UP 1   /* extension: CUDA __shfl_up_sync              */
+#define WF_COLL_SHFL_XOR 2  /* extension: CUDA __shfl_xor_sync             */
+#define WF_COLL_SHFL_IDX 3  /* extension: CUDA __shfl_sync                 */
+#define WF_COLL_VOTE_ALL 4  /* passes/warp_lower.py:17-33 reduce_vote all  */
+#define WF_COLL_VOTE_ANY 5  /* passes/warp_lower.py:17-33 reduce_vote any  */
+#define WF_COLL_BALLOT 6    /* extension: CUDA __ballot_sync               */
+#define WF_COLL_REDUCE_ADD 7 /* extension: CUDA __reduce_add_sync (REDUX)  */
+
+/* synthetic input generators for wf_fill_synthetic:
+ * h = splitmix64(seed ^ (index_base + i)) */
+#define WF_GEN_I32_FULL 0   /* (int32)(h >> 32)                             */
+#define WF_GEN_I32_SMALL 1  /* (int32)((h >> 32) % 21) - 10  (corpus.py:320)*/
+#define WF_GEN_F32_UNIT 2   /* (float)(h >> 40) * 2^-24 - 0.5 (exact)      */
+#define WF_GEN_U8_UNIFORM 3 /* h & 0xff                                     */
+#define WF_GEN_U8_CONST 4   /* param & 0xff                                 */
+#define WF_GEN_U8_GEOM 5    /* min(clz64(h), 255): geometric, skewed        */
+#define WF_GEN_I32_SELECT 6 /* > 0 with probability param/1000              */
+
+typedef void *wf_stream_t;
+
+/* ---- housekeeping ------------------------------------------------------ */
+const char *wf_version(void);
+int wf_abi_version(void);
+const char *wf_last_error(void);
+int wf_device_sm_count(int device);
+size_t wf_workspace_bytes(int op, uint64_t n, int block);
+int wf_workspace_init(void *ws, size_t ws_bytes, wf_stream_t stream);
+void wf_shutdown(void);
+
+/* ---- K1/K2: shuffle reductions ----------------------------------------
+ * Replaces the reference's per-warp-partials shfl_down reduction executed by
+ * launch() (runtime/launch.py:90 -> interp/mpmd.py:237) plus its host fold.
+ * out[0] = sum(in[0..n)); i32 wraps mod 2^32.  grid = 0 picks the persistent
+ * grid (SM count x resident blocks); block in {128, 256, 512, 1024}.
+ * f32: fixed order (per-thread chains, butterfly warp tree, block tree,
+ * fixed-order fold of block partials) => bitwise reproducible for a given
+ * (n, block, grid, device). */
+int wf_reduce_sum_i32(const int32_t *in, uint64_t n, int32_t *out, int block,
+                      int grid, void *ws, size_t ws_bytes, wf_stream_t stream);
+int wf_reduce_sum_f32(const float *in, uint64_t n, float *out, int block,
+                      int grid, void *ws, size_t ws_bytes, wf_stream_t stream);
+
+/* Fixed-order folds of `count` device values (cross-GPU partial combine,
+ * SURVEY.md §8e).  out[0] = vals[0] + vals[1] + ... + vals[count-1] in that
+ * association order for f32; wrapping for i32. */
+int wf_fold_f32(const float *vals, uint32_t count, float *out,
+                wf_stream_t stream);
+int wf_fold_i32(const int32_t *vals, uint32_t count, int32_t *out,
+                wf_stream_t stream);
+int wf_fold_u64(const uint64_t *vals, uint32_t count, uint64_t *out,
+                wf_stream_t stream);
+
+/* ---- K3: shfl_scan inclusive prefix sum --------------------------------
+ * out[i] = carry + in[0] + ... + in[i] (wrapping), single pass with
+ * decoupled look-back.  d_carry_in: device int32 (NULL = 0), used by the
+ * cross-GPU reduce-then-scan.  in/out may alias exactly (in-place). */
+int wf_scan_inclusive_i32(const int32_t *in, int32_t *out, uint64_t n,
+                          const int32_t *d_carry_in, void *ws, size_t ws_bytes,
+                          wf_stream_t stream);
+
+/* ---- K4: warp-aggregated stream compaction -----------------------------
+ * out[0..m) = in[i] for in[i] > 0 in index order; *d_count = m (uint64).
+ * n < 2^32 per call.  out must hold n elements. */
+int wf_compact_gt0_i32(const int32_t *in, uint64_t n, int32_t *out,
+                       uint64_t *d_count, void *ws, size_t ws_bytes,
+                       wf_stream_t stream);
+
+/* ---- K5: smem-privatised 256-bin histogram -----------------------------
+ * bins[b] = #{i : in[i] == b} as uint64 (overwrites bins). */
+int wf_histogram256_u8(const uint8_t *in, uint64_t n, uint64_t *bins, int grid,
+                       void *ws, size_t ws_bytes, wf_stream_t stream);
+
+/* ---- P: warp collectives with reference semantics ----------------------
+ * Runs n_threads logical threads as blocks of `block` threads (the last warp
+ * of a block is partial when block % 32 != 0; n_threads % block == 0).
+ * Lanes are grouped into segments of `width` lanes (1,2,4,8,16,32: the
+ * reference's warp_size, config.py:17-23).  Thread i, if its lane is in
+ * `mask`, computes the collective over its segment's participating lanes
+ * (mask & present lanes) and writes out[i]; other threads leave out[i].
+ * `a` is the value/predicate operand, `b` the per-lane offset/lane-mask/
+ * source-lane operand (NULL = use `operand` for every lane).
+ * Semantics (reference passes/warp_lower.py:17-45, interp/oracle.py:147-161):
+ *   SHFL_DOWN  src = l + off, own value unless 0 <= src < width and src
+ *              participates (reference clamp, any int offset)
+ *   SHFL_UP    src = l - off, same clamp
+ *   SHFL_XOR   src = l ^ off, same clamp
+ *   SHFL_IDX   src = off mod width (CUDA rule), own value if src absent
+ *   VOTE_ALL/VOTE_ANY  0/1 over participating lanes
+ *   BALLOT     bit j set iff participating lane j of the segment has a != 0
+ *   REDUCE_ADD wrapping sum over participating lanes */
+int wf_warp_collective(int kind, const int32_t *a, const int32_t *b,
+                       int32_t operand, int32_t *out, uint64_t n_threads,
+                       int block, int width, uint32_t mask,
+                       wf_stream_t stream);
+
+/* ---- synthetic inputs (identical to oracle/synthetic.py) --------------- */
+int wf_fill_synthetic(int gen, void *out, uint64_t n, uint64_t seed,
+                      uint64_t index_base, uint32_t param, wf_stream_t stream);
+
+/* ---- host-buffer entry points (end-to-end path) ------------------------
+ * Same result contract as the device entry points, but `host_in` is host
+ * memory (pinned for full PCIe speed).  The input is streamed through a
+ * caller-provided device staging buffer in double-buffered chunks, each
+ * chunk's copy overlapping the previous chunk's kernel; the scalar result is
+ * copied back into *host_out.  Synchronous (returns after the result is in
+ * host memory).  staging_bytes >= 2 MiB. */
+int wf_reduce_sum_f32_host(const float *host_in, uint64_t n, float *host_out,
+                           void *staging, size_t staging_bytes, void *ws,
+                           size_t ws_bytes, wf_stream_t stream);
+int wf_reduce_sum_i32_host(const int32_t *host_in, uint64_t n,
+                           int32_t *host_out, void *staging,
+                           size_t staging_bytes, void *ws, size_t ws_bytes,
+                           wf_stream_t stream);
+int wf_histogram256_u8_host(const uint8_t *host_in, uint64_t n,
+                            uint64_t *host_bins, void *staging,
+                            size_t staging_bytes, void *ws, size_t ws_bytes,
+                            wf_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WARPFOLD_B200_H */

@@ -1,0 +1,380 @@
+// wf_abi.cu — the extern "C" boundary declared in include/warpfold_b200.h.
+//
+// Argument validation mirrors the reference's launch-time checks
+// (runtime/launch.py:28-46 bind_args, config.py:26-41 validate) so the
+// Python wrapper can raise the same exception classes; nothing here falls
+// back to the CPU.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "wf_device.cuh"
+#include "wf_internal.h"
+#include "../../include/warpfold_b200.h"
+
+namespace wf {
+
+static thread_local std::string g_last_error;
+
+static int fail(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+static int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+static int cuda_status(cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return WF_OK;
+  cudaGetLastError();  // clear the sticky-free error state
+  return fail(int(e), "%s: %s", what, cudaGetErrorString(e));
+}
+
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+int sm_count(int device) {
+  static int cache[64] = {};
+  if (device < 0 || device >= 64) return 148;
+  if (cache[device] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0) {
+      cudaGetLastError();
+      v = 148;
+    }
+    cache[device] = v;
+  }
+  return cache[device];
+}
+
+static bool valid_reduce_block(int b) { return b == 128 || b == 256 || b == 512 || b == 1024; }
+
+static size_t ws_need(int op, uint64_t n) {
+  switch (op) {
+    case WF_OP_REDUCE_SUM_I32:
+    case WF_OP_REDUCE_SUM_F32:
+      return kWsHeader + size_t(kMaxReduceGrid) * 8;
+    case WF_OP_SCAN_INCLUSIVE_I32:
+    case WF_OP_COMPACT_GT0_I32: {
+      const uint64_t tiles = (n + kScanTile - 1) / kScanTile;
+      return kWsHeader + size_t(tiles < 1 ? 1 : tiles) * 8;
+    }
+    case WF_OP_HISTOGRAM256_U8:
+      return kWsHeader + 256 * 8;
+    case WF_OP_WARP_COLLECTIVE:
+      return 0;
+    default:
+      return 0;
+  }
+}
+
+static int check_ws(int op, uint64_t n, void *ws, size_t ws_bytes) {
+  const size_t need = ws_need(op, n);
+  if (need == 0) return WF_OK;
+  if (ws == nullptr) return fail(WF_ERR_WORKSPACE, "workspace is NULL (need %zu bytes)", need);
+  if (ws_bytes < need)
+    return fail(WF_ERR_WORKSPACE, "workspace of %zu bytes is too small (need %zu)", ws_bytes, need);
+  if (reinterpret_cast<uintptr_t>(ws) & 255u)
+    return fail(WF_ERR_WORKSPACE, "workspace must be 256-byte aligned");
+  return WF_OK;
+}
+
+// ---- streams for the host-buffer (e2e) entry points ---------------------
+struct CopyStreams {
+  cudaStream_t copy[2] = {nullptr, nullptr};
+  cudaEvent_t copied[2] = {nullptr, nullptr};
+  cudaEvent_t consumed[2] = {nullptr, nullptr};
+};
+static std::mutex g_streams_mu;
+static CopyStreams g_streams[64];
+
+static int get_copy_streams(CopyStreams *&cs) {
+  const int dev = current_device();
+  if (dev < 0 || dev >= 64) return fail(WF_ERR_CONFIG, "device %d out of range", dev);
+  std::lock_guard<std::mutex> lk(g_streams_mu);
+  CopyStreams &c = g_streams[dev];
+  if (c.copy[0] == nullptr) {
+    for (int k = 0; k < 2; ++k) {
+      cudaError_t e = cudaStreamCreateWithFlags(&c.copy[k], cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.copied[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.consumed[k], cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_status(e, "creating copy streams");
+    }
+  }
+  cs = &c;
+  return WF_OK;
+}
+
+// Streams `n` elements of `elem` bytes from host memory through two staging
+// halves.  `consume(dev_ptr, count, chunk_index)` enqueues the chunk's kernel
+// on `stream`.  Copy of chunk c+1 overlaps the kernel of chunk c.
+template <class F>
+static int stream_chunks(const void *host_in, uint64_t n, size_t elem, void *staging,
+                         size_t staging_bytes, cudaStream_t stream, F consume) {
+  CopyStreams *cs = nullptr;
+  int rc = get_copy_streams(cs);
+  if (rc) return rc;
+  const size_t half = (staging_bytes / 2) & ~size_t(255);
+  const uint64_t per_chunk = half / elem;
+  const uint64_t nchunks = (n + per_chunk - 1) / per_chunk;
+  for (uint64_t c = 0; c < nchunks; ++c) {
+    const int k = int(c & 1);
+    const uint64_t first = c * per_chunk;
+    const uint64_t cnt = (n - first) < per_chunk ? (n - first) : per_chunk;
+    char *dst = static_cast<char *>(staging) + size_t(k) * half;
+    cudaError_t e = cudaSuccess;
+    if (c >= 2) e = cudaStreamWaitEvent(cs->copy[k], cs->consumed[k], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(dst, static_cast<const char *>(host_in) + first * elem, cnt * elem,
+                          cudaMemcpyHostToDevice, cs->copy[k]);
+    if (e == cudaSuccess) e = cudaEventRecord(cs->copied[k], cs->copy[k]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, cs->copied[k], 0);
+    if (e != cudaSuccess) return cuda_status(e, "staging copy");
+    e = consume(dst, cnt, c);
+    if (e == cudaSuccess) e = cudaEventRecord(cs->consumed[k], stream);
+    if (e != cudaSuccess) return cuda_status(e, "chunk kernel");
+  }
+  return WF_OK;
+}
+
+}  // namespace wf
+
+using namespace wf;
+
+extern "C" {
+
+const char *wf_version(void) { return "warpfold_b200 0.1.0 (sm_100a)"; }
+int wf_abi_version(void) { return WF_ABI_VERSION; }
+const char *wf_last_error(void) { return g_last_error.c_str(); }
+
+int wf_device_sm_count(int device) { return sm_count(device); }
+
+size_t wf_workspace_bytes(int op, uint64_t n, int block) {
+  (void)block;
+  return ws_need(op, n);
+}
+
+int wf_workspace_init(void *ws, size_t ws_bytes, wf_stream_t stream) {
+  if (ws == nullptr || ws_bytes == 0) return WF_OK;
+  return cuda_status(cudaMemsetAsync(ws, 0, ws_bytes, static_cast<cudaStream_t>(stream)),
+                     "workspace init");
+}
+
+void wf_shutdown(void) {
+  std::lock_guard<std::mutex> lk(g_streams_mu);
+  for (auto &c : g_streams) {
+    for (int k = 0; k < 2; ++k) {
+      if (c.copy[k]) cudaStreamDestroy(c.copy[k]);
+      if (c.copied[k]) cudaEventDestroy(c.copied[k]);
+      if (c.consumed[k]) cudaEventDestroy(c.consumed[k]);
+      c.copy[k] = nullptr;
+      c.copied[k] = c.consumed[k] = nullptr;
+    }
+  }
+}
+
+static int reduce_common(int op, const void *in, uint64_t n, void *out, int block, int grid,
+                         void *ws, size_t ws_bytes) {
+  if (!valid_reduce_block(block))
+    return fail(WF_ERR_CONFIG, "block size must be one of 128/256/512/1024, got %d", block);
+  if (grid < 0 || grid > int(kMaxReduceGrid))
+    return fail(WF_ERR_CONFIG, "grid size must be in [0, %u], got %d", kMaxReduceGrid, grid);
+  if (out == nullptr) return fail(WF_ERR_ARG, "output pointer is NULL");
+  if (n > 0 && in == nullptr) return fail(WF_ERR_ARG, "input pointer is NULL");
+  if (reinterpret_cast<uintptr_t>(in) & 3u) return fail(WF_ERR_ARG, "input must be 4-byte aligned");
+  return check_ws(op, n, ws, ws_bytes);
+}
+
+int wf_reduce_sum_i32(const int32_t *in, uint64_t n, int32_t *out, int block, int grid,
+                      void *ws, size_t ws_bytes, wf_stream_t stream) {
+  int rc = reduce_common(WF_OP_REDUCE_SUM_I32, in, n, out, block, grid, ws, ws_bytes);
+  if (rc) return rc;
+  if (grid == 0) grid = auto_reduce_grid(false, block, n);
+  return cuda_status(launch_reduce_i32(in, n, out, block, grid, ws, static_cast<cudaStream_t>(stream)),
+                     "reduce_sum_i32");
+}
+
+int wf_reduce_sum_f32(const float *in, uint64_t n, float *out, int block, int grid, void *ws,
+                      size_t ws_bytes, wf_stream_t stream) {
+  int rc = reduce_common(WF_OP_REDUCE_SUM_F32, in, n, out, block, grid, ws, ws_bytes);
+  if (rc) return rc;
+  if (grid == 0) grid = auto_reduce_grid(true, block, n);
+  return cuda_status(launch_reduce_f32(in, n, out, block, grid, ws, static_cast<cudaStream_t>(stream)),
+                     "reduce_sum_f32");
+}
+
+int wf_fold_f32(const float *vals, uint32_t count, float *out, wf_stream_t stream) {
+  if (out == nullptr || (count && vals == nullptr)) return fail(WF_ERR_ARG, "NULL pointer");
+  return cuda_status(launch_fold_f32(vals, count, out, static_cast<cudaStream_t>(stream)), "fold_f32");
+}
+
+int wf_fold_i32(const int32_t *vals, uint32_t count, int32_t *out, wf_stream_t stream) {
+  if (out == nullptr || (count && vals == nullptr)) return fail(WF_ERR_ARG, "NULL pointer");
+  return cuda_status(launch_fold_i32(vals, count, out, static_cast<cudaStream_t>(stream)), "fold_i32");
+}
+
+int wf_fold_u64(const uint64_t *vals, uint32_t count, uint64_t *out, wf_stream_t stream) {
+  if (out == nullptr || (count && vals == nullptr)) return fail(WF_ERR_ARG, "NULL pointer");
+  return cuda_status(launch_fold_u64(vals, count, out, static_cast<cudaStream_t>(stream)), "fold_u64");
+}
+
+int wf_scan_inclusive_i32(const int32_t *in, int32_t *out, uint64_t n, const int32_t *d_carry_in,
+                          void *ws, size_t ws_bytes, wf_stream_t stream) {
+  if (n > 0 && (in == nullptr || out == nullptr)) return fail(WF_ERR_ARG, "NULL buffer pointer");
+  if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 3u)
+    return fail(WF_ERR_ARG, "buffers must be 4-byte aligned");
+  if (n > (uint64_t(0xffffffffu) * kScanTile))
+    return fail(WF_ERR_ARG, "n=%llu exceeds the tile-id range", (unsigned long long)n);
+  int rc = check_ws(WF_OP_SCAN_INCLUSIVE_I32, n, ws, ws_bytes);
+  if (rc) return rc;
+  return cuda_status(launch_scan_i32(in, out, n, d_carry_in, ws, static_cast<cudaStream_t>(stream)),
+                     "scan_inclusive_i32");
+}
+
+int wf_compact_gt0_i32(const int32_t *in, uint64_t n, int32_t *out, uint64_t *d_count, void *ws,
+                       size_t ws_bytes, wf_stream_t stream) {
+  if (d_count == nullptr) return fail(WF_ERR_ARG, "count pointer is NULL");
+  if (n > 0 && (in == nullptr || out == nullptr)) return fail(WF_ERR_ARG, "NULL buffer pointer");
+  if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 3u)
+    return fail(WF_ERR_ARG, "buffers must be 4-byte aligned");
+  if (n > 0xffffffffull)
+    return fail(WF_ERR_ARG, "compaction takes n < 2^32 per call, got %llu", (unsigned long long)n);
+  int rc = check_ws(WF_OP_COMPACT_GT0_I32, n, ws, ws_bytes);
+  if (rc) return rc;
+  return cuda_status(
+      launch_compact_gt0_i32(in, n, out, d_count, ws, static_cast<cudaStream_t>(stream)),
+      "compact_gt0_i32");
+}
+
+int wf_histogram256_u8(const uint8_t *in, uint64_t n, uint64_t *bins, int grid, void *ws,
+                       size_t ws_bytes, wf_stream_t stream) {
+  if (bins == nullptr) return fail(WF_ERR_ARG, "bins pointer is NULL");
+  if (n > 0 && in == nullptr) return fail(WF_ERR_ARG, "input pointer is NULL");
+  if (grid < 0) return fail(WF_ERR_CONFIG, "grid size must be >= 0, got %d", grid);
+  int rc = check_ws(WF_OP_HISTOGRAM256_U8, n, ws, ws_bytes);
+  if (rc) return rc;
+  if (grid == 0) grid = auto_hist_grid(n);
+  return cuda_status(
+      launch_hist256(in, n, bins, false, grid, ws, static_cast<cudaStream_t>(stream)),
+      "histogram256_u8");
+}
+
+int wf_warp_collective(int kind, const int32_t *a, const int32_t *b, int32_t operand, int32_t *out,
+                       uint64_t n_threads, int block, int width, uint32_t mask,
+                       wf_stream_t stream) {
+  if (kind < WF_COLL_SHFL_DOWN || kind > WF_COLL_REDUCE_ADD)
+    return fail(WF_ERR_UNSUPPORTED, "unknown warp collective kind %d", kind);
+  if (block < 1 || block > 1024) return fail(WF_ERR_CONFIG, "block size must be in [1, 1024], got %d", block);
+  if (width < 1 || width > 32 || (width & (width - 1)))
+    return fail(WF_ERR_CONFIG, "warp width must be a power of two in [1, 32], got %d", width);
+  if (n_threads % uint64_t(block))
+    return fail(WF_ERR_CONFIG, "n_threads (%llu) must be a multiple of the block size (%d)",
+                (unsigned long long)n_threads, block);
+  if (n_threads / uint64_t(block) > 0x7fffffffull) return fail(WF_ERR_CONFIG, "grid too large");
+  if (n_threads && (a == nullptr || out == nullptr)) return fail(WF_ERR_ARG, "NULL buffer pointer");
+  return cuda_status(launch_warp_collective(kind, a, b, operand, out, n_threads, block, width, mask,
+                                            static_cast<cudaStream_t>(stream)),
+                     "warp_collective");
+}
+
+int wf_fill_synthetic(int gen, void *out, uint64_t n, uint64_t seed, uint64_t index_base,
+                      uint32_t param, wf_stream_t stream) {
+  if (gen < WF_GEN_I32_FULL || gen > WF_GEN_I32_SELECT)
+    return fail(WF_ERR_UNSUPPORTED, "unknown generator %d", gen);
+  if (n && out == nullptr) return fail(WF_ERR_ARG, "output pointer is NULL");
+  return cuda_status(
+      launch_fill_synthetic(gen, out, n, seed, index_base, param, static_cast<cudaStream_t>(stream)),
+      "fill_synthetic");
+}
+
+}  // extern "C"
+
+// ---- host-buffer entry points --------------------------------------------
+namespace wf {
+template <class T, class Launch, class Fold>
+static int reduce_host(int op, const T *host_in, uint64_t n, T *host_out, void *staging,
+                       size_t staging_bytes, void *ws, size_t ws_bytes, wf_stream_t stream,
+                       Launch launch_one, Fold fold) {
+  if (host_out == nullptr) return fail(WF_ERR_ARG, "host output pointer is NULL");
+  if (n && host_in == nullptr) return fail(WF_ERR_ARG, "host input pointer is NULL");
+  if (staging == nullptr || staging_bytes < (size_t(2) << 20))
+    return fail(WF_ERR_ARG, "staging buffer must be at least 2 MiB");
+  // chunk partials live in the tail of the staging buffer
+  const size_t slots = 4096;
+  const size_t body = (staging_bytes - slots * sizeof(T)) & ~size_t(511);
+  T *partials = reinterpret_cast<T *>(static_cast<char *>(staging) + body);
+  const uint64_t per_chunk = (body / 2 & ~size_t(255)) / sizeof(T);
+  if ((n + per_chunk - 1) / per_chunk > slots)
+    return fail(WF_ERR_ARG, "staging buffer too small for n=%llu", (unsigned long long)n);
+  int rc = check_ws(op, n, ws, ws_bytes);
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint64_t nchunks = 0;
+  rc = stream_chunks(host_in, n, sizeof(T), staging, body, s,
+                     [&](void *dev, uint64_t cnt, uint64_t c) {
+                       nchunks = c + 1;
+                       return launch_one(static_cast<const T *>(dev), cnt, partials + c, s);
+                     });
+  if (rc) return rc;
+  cudaError_t e = fold(partials, uint32_t(nchunks), partials + slots - 1, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(host_out, partials + slots - 1, sizeof(T), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return cuda_status(e, "host reduction");
+}
+}  // namespace wf
+
+extern "C" {
+
+int wf_reduce_sum_f32_host(const float *host_in, uint64_t n, float *host_out, void *staging,
+                           size_t staging_bytes, void *ws, size_t ws_bytes, wf_stream_t stream) {
+  return reduce_host<float>(
+      WF_OP_REDUCE_SUM_F32, host_in, n, host_out, staging, staging_bytes, ws, ws_bytes, stream,
+      [&](const float *d, uint64_t cnt, float *o, cudaStream_t s) {
+        return launch_reduce_f32(d, cnt, o, 256, auto_reduce_grid(true, 256, cnt), ws, s);
+      },
+      [](const float *v, uint32_t c, float *o, cudaStream_t s) { return launch_fold_f32(v, c, o, s); });
+}
+
+int wf_reduce_sum_i32_host(const int32_t *host_in, uint64_t n, int32_t *host_out, void *staging,
+                           size_t staging_bytes, void *ws, size_t ws_bytes, wf_stream_t stream) {
+  return reduce_host<int32_t>(
+      WF_OP_REDUCE_SUM_I32, host_in, n, host_out, staging, staging_bytes, ws, ws_bytes, stream,
+      [&](const int32_t *d, uint64_t cnt, int32_t *o, cudaStream_t s) {
+        return launch_reduce_i32(d, cnt, o, 256, auto_reduce_grid(false, 256, cnt), ws, s);
+      },
+      [](const int32_t *v, uint32_t c, int32_t *o, cudaStream_t s) { return launch_fold_i32(v, c, o, s); });
+}
+
+int wf_histogram256_u8_host(const uint8_t *host_in, uint64_t n, uint64_t *host_bins, void *staging,
+                            size_t staging_bytes, void *ws, size_t ws_bytes, wf_stream_t stream) {
+  if (host_bins == nullptr) return fail(WF_ERR_ARG, "host bins pointer is NULL");
+  if (n && host_in == nullptr) return fail(WF_ERR_ARG, "host input pointer is NULL");
+  if (staging == nullptr || staging_bytes < (size_t(2) << 20))
+    return fail(WF_ERR_ARG, "staging buffer must be at least 2 MiB");
+  int rc = check_ws(WF_OP_HISTOGRAM256_U8, n, ws, ws_bytes);
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t body = (staging_bytes - 4096) & ~size_t(511);
+  uint64_t *dbins = reinterpret_cast<uint64_t *>(static_cast<char *>(staging) + body);
+  cudaError_t e = cudaMemsetAsync(dbins, 0, 256 * sizeof(uint64_t), s);
+  if (e != cudaSuccess) return cuda_status(e, "bins init");
+  rc = stream_chunks(host_in, n, 1, staging, body, s, [&](void *dev, uint64_t cnt, uint64_t) {
+    return launch_hist256(static_cast<const uint8_t *>(dev), cnt, dbins, true, auto_hist_grid(cnt),
+                          ws, s);
+  });
+  if (rc) return rc;
+  e = cudaMemcpyAsync(host_bins, dbins, 256 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return cuda_status(e, "host histogram");
+}
+
+}  // extern "C"

@@ -1,0 +1,143 @@
+// wf_hist.cu — K5 histogram256_u8: shared-memory-privatised 256-bin byte
+// histogram.
+//
+// Reference analog: none expressible (no u8 type, no atomics in the DSL,
+// dsl/parser.py:83-88, dsl/lexer.py:18-25); under hierarchical collapsing a
+// block's smem histogram becomes plain increments inside the block loop
+// (one CPU thread runs the whole block).  On B200 the block's 1024 threads
+// share ONE lane-banked sub-histogram in shared memory:
+//
+//     counter(bin b, lane l) at word b*32 + l        (256 x 32 x u32 = 32 KiB)
+//
+// Every lane of a warp updates its own bank, so one ATOMS.ADD warp
+// instruction is bank-conflict-free whatever the data (uniform, all-equal,
+// skewed); lanes of different warps that hit the same (bin, lane) word are
+// serialised by the shared-memory atomic unit.  Input streams in as 16-byte
+// vectors over a persistent grid.  At the end each block folds its 32 lane
+// columns per bin (rotated reads, conflict-free) and adds them into 256
+// uint64 accumulators in the workspace; the last block (atomic ticket) moves
+// them to `bins` and re-zeroes the accumulators.
+//
+// Roofline: HBM, 1 B/elem read.
+#include "wf_device.cuh"
+#include "wf_internal.h"
+
+namespace wf {
+namespace {
+
+constexpr int BLOCK = kHistBlock;
+constexpr int UNROLL = 2;
+
+__device__ __forceinline__ void count_word(uint32_t *col, uint32_t w) {
+  atomicAdd(col + ((w & 0xffu) << 5), 1u);
+  atomicAdd(col + (((w >> 8) & 0xffu) << 5), 1u);
+  atomicAdd(col + (((w >> 16) & 0xffu) << 5), 1u);
+  atomicAdd(col + ((w >> 24) << 5), 1u);
+}
+
+__global__ void __launch_bounds__(BLOCK, 2)
+    hist256_kernel(const uint8_t *__restrict__ in, uint64_t n,
+                   unsigned long long *__restrict__ bins, bool accumulate,
+                   unsigned long long *__restrict__ accum,
+                   uint32_t *__restrict__ ticket) {
+  extern __shared__ uint32_t sh[];  // [256][32]
+  for (uint32_t i = threadIdx.x; i < 256 * 32; i += BLOCK) sh[i] = 0u;
+  __syncthreads();
+
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t *col = sh + lane;
+  const uint64_t gtid = uint64_t(blockIdx.x) * BLOCK + threadIdx.x;
+  const uint64_t nthreads = uint64_t(gridDim.x) * BLOCK;
+
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(in);
+  uint64_t head = (16u - (addr & 15u)) & 15u;
+  if (head > n) head = n;
+  const uint64_t nvec = (n - head) / 16;
+  const uint64_t tail0 = head + nvec * 16;
+  const uint4 *vin = reinterpret_cast<const uint4 *>(in + head);
+
+  uint64_t i = gtid;
+  for (; i + uint64_t(UNROLL - 1) * nthreads < nvec; i += UNROLL * nthreads) {
+    uint4 q[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) q[u] = ldg_stream(vin + i + u * nthreads);
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      count_word(col, q[u].x);
+      count_word(col, q[u].y);
+      count_word(col, q[u].z);
+      count_word(col, q[u].w);
+    }
+  }
+  for (; i < nvec; i += nthreads) {
+    const uint4 q = ldg_stream(vin + i);
+    count_word(col, q.x);
+    count_word(col, q.y);
+    count_word(col, q.z);
+    count_word(col, q.w);
+  }
+  if (gtid < head) atomicAdd(col + (uint32_t(in[gtid]) << 5), 1u);
+  if (tail0 + gtid < n) atomicAdd(col + (uint32_t(in[tail0 + gtid]) << 5), 1u);
+  __syncthreads();
+
+  // fold the 32 lane columns of each bin; rotation keeps the reads of a warp
+  // on 32 distinct banks
+  if (threadIdx.x < 256) {
+    const uint32_t b = threadIdx.x;
+    uint32_t s = 0;
+#pragma unroll 8
+    for (uint32_t l = 0; l < 32; ++l) s += sh[b * 32 + ((l + b) & 31u)];
+    if (s) atomicAdd(accum + b, (unsigned long long)s);
+  }
+  __shared__ bool am_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    am_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  if (threadIdx.x < 256) {
+    const unsigned long long v = atomicExch(accum + threadIdx.x, 0ull);
+    bins[threadIdx.x] = accumulate ? bins[threadIdx.x] + v : v;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
+}  // namespace
+
+int auto_hist_grid(uint64_t n) {
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    cudaFuncSetAttribute(hist256_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kHistSmem));
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, hist256_kernel, BLOCK, kHistSmem);
+    per_sm = b > 0 ? b : 1;
+  }
+  const uint64_t full = uint64_t(per_sm) * uint64_t(sm_count(current_device()));
+  const uint64_t per_block = uint64_t(BLOCK) * 16 * UNROLL * 4;
+  uint64_t need = (n + per_block - 1) / per_block;
+  if (need < 1) need = 1;
+  return int(need < full ? need : full);
+}
+
+cudaError_t launch_hist256(const uint8_t *in, uint64_t n, uint64_t *bins,
+                           bool accumulate, int grid, void *ws,
+                           cudaStream_t s) {
+  auto *ticket = reinterpret_cast<uint32_t *>(ws);
+  auto *accum = reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + kWsHeader);
+  static uint64_t configured = 0;  // one bit per device
+  const int dev = current_device();
+  if (dev < 64 && !(configured >> dev & 1)) {
+    cudaFuncSetAttribute(hist256_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kHistSmem));
+    configured |= 1ull << dev;
+  }
+  hist256_kernel<<<grid, BLOCK, kHistSmem, s>>>(
+      in, n, reinterpret_cast<unsigned long long *>(bins), accumulate, accum, ticket);
+  return cudaGetLastError();
+}
+
+}  // namespace wf

@@ -1,0 +1,61 @@
+// wf_internal.h — host-side launchers shared between the kernel translation
+// units and the C ABI (wf_abi.cu).  Not part of the public interface.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace wf {
+
+// Workspace layout: a 256-byte header followed by op-specific arrays.
+constexpr size_t kWsHeader = 256;
+constexpr uint32_t kMaxReduceGrid = 8192;   // partial slots for reductions
+constexpr int kScanBlock = 256;             // threads per scan/compact tile
+constexpr int kScanVec = 4;                 // int4 loads per thread per tile
+constexpr uint64_t kScanTile = uint64_t(kScanBlock) * kScanVec * 4;  // 4096
+constexpr int kHistBlock = 1024;
+constexpr size_t kHistSmem = 256 * 32 * sizeof(uint32_t);  // 32 KiB
+
+int sm_count(int device);
+int current_device();
+
+// reductions (wf_reduce.cu)
+cudaError_t launch_reduce_i32(const int32_t *in, uint64_t n, int32_t *out,
+                              int block, int grid, void *ws,
+                              cudaStream_t s);
+cudaError_t launch_reduce_f32(const float *in, uint64_t n, float *out,
+                              int block, int grid, void *ws, cudaStream_t s);
+int auto_reduce_grid(bool is_f32, int block, uint64_t n);
+cudaError_t launch_fold_f32(const float *v, uint32_t count, float *out,
+                            cudaStream_t s);
+cudaError_t launch_fold_i32(const int32_t *v, uint32_t count, int32_t *out,
+                            cudaStream_t s);
+cudaError_t launch_fold_u64(const uint64_t *v, uint32_t count, uint64_t *out,
+                            cudaStream_t s);
+
+// scan / compaction (wf_scan.cu)
+cudaError_t launch_scan_i32(const int32_t *in, int32_t *out, uint64_t n,
+                            const int32_t *carry, void *ws, cudaStream_t s);
+cudaError_t launch_compact_gt0_i32(const int32_t *in, uint64_t n,
+                                   int32_t *out, uint64_t *count, void *ws,
+                                   cudaStream_t s);
+
+// histogram (wf_hist.cu)
+cudaError_t launch_hist256(const uint8_t *in, uint64_t n, uint64_t *bins,
+                           bool accumulate, int grid, void *ws,
+                           cudaStream_t s);
+int auto_hist_grid(uint64_t n);
+
+// warp collectives (wf_warp.cu)
+cudaError_t launch_warp_collective(int kind, const int32_t *a,
+                                   const int32_t *b, int32_t operand,
+                                   int32_t *out, uint64_t n_threads, int block,
+                                   int width, uint32_t mask, cudaStream_t s);
+
+// synthetic inputs (wf_gen.cu)
+cudaError_t launch_fill_synthetic(int gen, void *out, uint64_t n,
+                                  uint64_t seed, uint64_t base, uint32_t param,
+                                  cudaStream_t s);
+
+}  // namespace wf

@@ -1,0 +1,273 @@
+// wf_reduce.cu — K1 reduce_sum_i32 and K2 reduce_sum_f32.
+//
+// Reference analog: the per-warp-partials shuffle reduction of SURVEY.md §8c
+// (grid-stride per-thread sum -> five shfl_down rounds -> out[warp]) that the
+// reference executes through launch() (runtime/launch.py:90) and the
+// collapsed lane loops of passes/warp_lower.py:64-73, followed by a host
+// wrap-fold.  Here the whole thing is ONE persistent-grid launch:
+//
+//   1. every thread streams 16-byte vectors (UNROLL loads in flight) into
+//      4*UNROLL independent accumulator chains;
+//   2. the chains fold in a fixed pairwise order, then the warp folds with
+//      REDUX.SUM (i32) or a SHFL.BFLY butterfly (f32; REDUX has no f32 add);
+//   3. warp sums fold through shared memory inside the block;
+//   4. block partials go to the workspace; the last block to finish (atomic
+//      ticket) folds them in block-index order and resets the ticket.
+//
+// The element->thread assignment depends only on (n, block, grid), so the f32
+// result is bitwise reproducible run to run.  Roofline: HBM read, 4 B/elem.
+#include "wf_device.cuh"
+#include "wf_internal.h"
+
+namespace wf {
+namespace {
+
+struct SumI32 {
+  using elem_t = int32_t;
+  using acc_t = uint32_t;
+  __device__ static acc_t zero() { return 0u; }
+  __device__ static acc_t add(acc_t a, acc_t b) { return a + b; }
+  __device__ static acc_t from_bits(uint32_t b) { return b; }
+  __device__ static acc_t load(const elem_t *p) { return uint32_t(*p); }
+  __device__ static acc_t warp_sum(acc_t v) {
+    return __reduce_add_sync(kFull, v);  // REDUX.SUM
+  }
+  __device__ static elem_t to_elem(acc_t v) { return int32_t(v); }
+};
+
+struct SumF32 {
+  using elem_t = float;
+  using acc_t = float;
+  __device__ static acc_t zero() { return 0.0f; }
+  __device__ static acc_t add(acc_t a, acc_t b) { return __fadd_rn(a, b); }
+  __device__ static acc_t from_bits(uint32_t b) { return __uint_as_float(b); }
+  __device__ static acc_t load(const elem_t *p) { return *p; }
+  __device__ static acc_t warp_sum(acc_t v) {
+    // butterfly: every lane ends with identical bits (fp add commutes)
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) v = __fadd_rn(v, __shfl_xor_sync(kFull, v, m));
+    return v;
+  }
+  __device__ static elem_t to_elem(acc_t v) { return v; }
+};
+
+template <class Op, int BLOCK>
+__device__ __forceinline__ typename Op::acc_t block_sum(typename Op::acc_t v) {
+  using acc_t = typename Op::acc_t;
+  constexpr int NW = BLOCK / 32;
+  __shared__ acc_t warp_sums[NW];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = Op::warp_sum(v);
+  if (lane == 0) warp_sums[warp] = v;
+  __syncthreads();
+  acc_t r = Op::zero();
+  if (warp == 0) {
+    r = Op::warp_sum(lane < NW ? warp_sums[lane] : Op::zero());
+  }
+  __syncthreads();  // warp_sums reusable by a second call
+  return r;         // valid in warp 0
+}
+
+template <class Op, int BLOCK, int UNROLL>
+__global__ void __launch_bounds__(BLOCK)
+    reduce_kernel(const typename Op::elem_t *__restrict__ in, uint64_t n,
+                  typename Op::elem_t *__restrict__ out,
+                  typename Op::acc_t *__restrict__ partials,
+                  uint32_t *__restrict__ ticket) {
+  using acc_t = typename Op::acc_t;
+  using elem_t = typename Op::elem_t;
+  const uint64_t gtid = uint64_t(blockIdx.x) * BLOCK + threadIdx.x;
+  const uint64_t nthreads = uint64_t(gridDim.x) * BLOCK;
+
+  // head (scalar until 16 B alignment) | body (16 B vectors) | tail (scalar)
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(in);
+  uint64_t head = ((16u - (addr & 15u)) & 15u) / sizeof(elem_t);
+  if (head > n) head = n;
+  const uint64_t nvec = (n - head) / 4;
+  const uint64_t tail0 = head + nvec * 4;
+  const uint4 *vin = reinterpret_cast<const uint4 *>(in + head);
+
+  acc_t acc[UNROLL][4];
+#pragma unroll
+  for (int u = 0; u < UNROLL; ++u)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[u][k] = Op::zero();
+
+  uint64_t i = gtid;
+  for (; i + uint64_t(UNROLL - 1) * nthreads < nvec; i += UNROLL * nthreads) {
+    uint4 q[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) q[u] = ldg_stream(vin + i + u * nthreads);
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      acc[u][0] = Op::add(acc[u][0], Op::from_bits(q[u].x));
+      acc[u][1] = Op::add(acc[u][1], Op::from_bits(q[u].y));
+      acc[u][2] = Op::add(acc[u][2], Op::from_bits(q[u].z));
+      acc[u][3] = Op::add(acc[u][3], Op::from_bits(q[u].w));
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < UNROLL; ++u) {  // remainder: < UNROLL vectors left
+    if (i < nvec) {
+      const uint4 q = ldg_stream(vin + i);
+      acc[u][0] = Op::add(acc[u][0], Op::from_bits(q.x));
+      acc[u][1] = Op::add(acc[u][1], Op::from_bits(q.y));
+      acc[u][2] = Op::add(acc[u][2], Op::from_bits(q.z));
+      acc[u][3] = Op::add(acc[u][3], Op::from_bits(q.w));
+      i += nthreads;
+    }
+  }
+  if (gtid < head) acc[0][0] = Op::add(acc[0][0], Op::load(in + gtid));
+  if (tail0 + gtid < n) acc[0][1] = Op::add(acc[0][1], Op::load(in + tail0 + gtid));
+
+  // fixed pairwise fold of the 4*UNROLL chains
+#pragma unroll
+  for (int u = 0; u < UNROLL; ++u) {
+    acc[u][0] = Op::add(Op::add(acc[u][0], acc[u][1]), Op::add(acc[u][2], acc[u][3]));
+  }
+#pragma unroll
+  for (int s = 1; s < UNROLL; s <<= 1)
+#pragma unroll
+    for (int u = 0; u + s < UNROLL; u += 2 * s) acc[u][0] = Op::add(acc[u][0], acc[u + s][0]);
+
+  const acc_t bsum = block_sum<Op, BLOCK>(acc[0][0]);
+
+  __shared__ bool am_last;
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = bsum;
+    __threadfence();
+    am_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  // fixed-order fold of the block partials (thread t: t, t+BLOCK, ...)
+  acc_t f = Op::zero();
+  for (uint32_t j = threadIdx.x; j < gridDim.x; j += BLOCK) {
+    f = Op::add(f, __ldcg(partials + j));
+  }
+  f = block_sum<Op, BLOCK>(f);
+  if (threadIdx.x == 0) {
+    out[0] = Op::to_elem(f);
+    *ticket = 0u;
+  }
+}
+
+// Single-block fold with a fixed association (thread-strided chains, then the
+// block tree), so a cross-GPU combine over ranks is deterministic and every
+// rank computes identical bits.
+template <class Op>
+__global__ void __launch_bounds__(256)
+    fold_kernel(const typename Op::elem_t *__restrict__ v, uint32_t count,
+                typename Op::elem_t *__restrict__ out) {
+  using acc_t = typename Op::acc_t;
+  acc_t f = Op::zero();
+  for (uint32_t j = threadIdx.x; j < count; j += 256) f = Op::add(f, Op::load(v + j));
+  f = block_sum<Op, 256>(f);
+  if (threadIdx.x == 0) out[0] = Op::to_elem(f);
+}
+
+__global__ void __launch_bounds__(256)
+    fold_u64_kernel(const uint64_t *__restrict__ v, uint32_t count,
+                    uint64_t *__restrict__ out) {
+  __shared__ unsigned long long s;
+  if (threadIdx.x == 0) s = 0;
+  __syncthreads();
+  unsigned long long f = 0;
+  for (uint32_t j = threadIdx.x; j < count; j += 256) f += v[j];
+  atomicAdd(&s, f);
+  __syncthreads();
+  if (threadIdx.x == 0) out[0] = s;
+}
+
+constexpr int kUnroll = 4;
+
+template <class Op, int BLOCK>
+cudaError_t launch_block(const typename Op::elem_t *in, uint64_t n,
+                         typename Op::elem_t *out, int grid, void *ws,
+                         cudaStream_t s) {
+  auto *ticket = reinterpret_cast<uint32_t *>(ws);
+  auto *partials = reinterpret_cast<typename Op::acc_t *>(
+      static_cast<char *>(ws) + kWsHeader);
+  reduce_kernel<Op, BLOCK, kUnroll>
+      <<<grid, BLOCK, 0, s>>>(in, n, out, partials, ticket);
+  return cudaGetLastError();
+}
+
+template <class Op>
+cudaError_t launch_reduce(const typename Op::elem_t *in, uint64_t n,
+                          typename Op::elem_t *out, int block, int grid,
+                          void *ws, cudaStream_t s) {
+  switch (block) {
+    case 128: return launch_block<Op, 128>(in, n, out, grid, ws, s);
+    case 256: return launch_block<Op, 256>(in, n, out, grid, ws, s);
+    case 512: return launch_block<Op, 512>(in, n, out, grid, ws, s);
+    case 1024: return launch_block<Op, 1024>(in, n, out, grid, ws, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <class Op, int BLOCK>
+int occupancy_blocks() {
+  int b = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &b, reduce_kernel<Op, BLOCK, kUnroll>, BLOCK, 0);
+  return b > 0 ? b : 1;
+}
+
+template <class Op>
+int resident_blocks(int block) {
+  switch (block) {
+    case 128: return occupancy_blocks<Op, 128>();
+    case 256: return occupancy_blocks<Op, 256>();
+    case 512: return occupancy_blocks<Op, 512>();
+    default: return occupancy_blocks<Op, 1024>();
+  }
+}
+
+}  // namespace
+
+int auto_reduce_grid(bool is_f32, int block, uint64_t n) {
+  static int cache[2][11] = {};
+  const int lg = block == 128 ? 7 : block == 256 ? 8 : block == 512 ? 9 : 10;
+  int &per_sm = cache[is_f32][lg];
+  if (per_sm == 0) per_sm = is_f32 ? resident_blocks<SumF32>(block)
+                                   : resident_blocks<SumI32>(block);
+  uint64_t full = uint64_t(per_sm) * uint64_t(sm_count(current_device()));
+  if (full > kMaxReduceGrid) full = kMaxReduceGrid;
+  // enough blocks that each thread issues at least one UNROLL batch
+  const uint64_t per_block = uint64_t(block) * kUnroll * 4;
+  uint64_t need = (n + per_block - 1) / per_block;
+  if (need < 1) need = 1;
+  return int(need < full ? need : full);
+}
+
+cudaError_t launch_reduce_i32(const int32_t *in, uint64_t n, int32_t *out,
+                              int block, int grid, void *ws, cudaStream_t s) {
+  return launch_reduce<SumI32>(in, n, out, block, grid, ws, s);
+}
+
+cudaError_t launch_reduce_f32(const float *in, uint64_t n, float *out,
+                              int block, int grid, void *ws, cudaStream_t s) {
+  return launch_reduce<SumF32>(in, n, out, block, grid, ws, s);
+}
+
+cudaError_t launch_fold_f32(const float *v, uint32_t count, float *out,
+                            cudaStream_t s) {
+  fold_kernel<SumF32><<<1, 256, 0, s>>>(v, count, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fold_i32(const int32_t *v, uint32_t count, int32_t *out,
+                            cudaStream_t s) {
+  fold_kernel<SumI32><<<1, 256, 0, s>>>(v, count, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fold_u64(const uint64_t *v, uint32_t count, uint64_t *out,
+                            cudaStream_t s) {
+  fold_u64_kernel<<<1, 256, 0, s>>>(v, count, out);
+  return cudaGetLastError();
+}
+
+}  // namespace wf

@@ -1,0 +1,209 @@
+"""Generate golden vectors by running the warpfold reference itself.
+
+Run in the container that has the read-only reference mounted:
+
+    PYTHONPATH=/root/reference/pkg/src PYTHONDONTWRITEBYTECODE=1 \
+        python tests/golden/make_golden.py
+
+Writes small fixtures next to this script.  The GPU box never reads the
+reference: tests load only these committed files.  Every vector comes from
+the reference's own code paths:
+  - warp_semantics.json: passes/warp_lower.py shuffle_down / reduce_vote
+  - oracle_kat.npz: interp/oracle.py run_oracle on the kernels of the
+    reference's tests/test_oracle.py:41-89 known-answer tests
+  - c1c2_pin.npz: the SURVEY.md §8c per-warp-partials shfl_down reduction
+    (i32 and f32) through BOTH run_oracle and launch(hybrid_transform(...))
+  - c3_pin.npz: warp inclusive prefix scan (lane-reversed shfl_down, the only
+    formulation the reference DSL can express) through run_oracle and launch
+  - corpus.npz: all 17 corpus kernels (corpus.py) through run_oracle
+"""
+
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parents[1]))  # repo root, for oracle.synthetic
+
+from warpfold import DeviceMemory, LaunchConfig, hybrid_transform, parse_module, run_oracle  # noqa: E402
+from warpfold import corpus  # noqa: E402
+from warpfold.passes.warp_lower import reduce_vote, shuffle_down  # noqa: E402
+from warpfold.runtime.launch import bind_args, launch  # noqa: E402
+
+from oracle import synthetic  # noqa: E402
+
+C1_I32 = """
+__global__ void wsum(global i32* a, global i32* out, i32 n) {
+    i32 tx = threadIdx.x;
+    i32 sum = 0;
+    for (i32 i = tx + blockIdx.x * blockDim.x; i < n; i = i + blockDim.x * gridDim.x) {
+        sum = sum + a[i];
+    }
+    for (i32 off = 16; off > 0; off = off / 2) {
+        sum = sum + shfl_down(sum, off);
+    }
+    if (tx % 32 == 0) {
+        out[blockIdx.x * (blockDim.x / 32) + tx / 32] = sum;
+    }
+}
+"""
+C1_F32 = C1_I32.replace("global i32* a, global i32* out", "global f32* a, global f32* out") \
+               .replace("i32 sum = 0;", "f32 sum = 0.0;")
+
+C3_WARP_PREFIX = """
+__global__ void warp_prefix(global i32* a, global i32* out) {
+    i32 tid = threadIdx.x + blockIdx.x * blockDim.x;
+    i32 lane = threadIdx.x % 32;
+    i32 base = tid - lane;
+    i32 v = a[base + 31 - lane];
+    for (i32 off = 1; off < 32; off = off * 2) {
+        i32 t = shfl_down(v, off);
+        if (lane + off < 32) {
+            v = v + t;
+        }
+    }
+    out[base + 31 - lane] = v;
+}
+"""
+
+
+def _run(engine: str, source: str, grid: int, block: int, buffers, scalars=(), warp=32):
+    kernel = parse_module(source).kernel()
+    cfg = LaunchConfig(grid_size=grid, block_size=block, warp_size=warp, workers=1)
+    mem = DeviceMemory()
+    args = []
+    for kind, init in buffers:
+        buf = mem.alloc(4 * len(init))
+        mem.view(buf, kind)[:] = init
+        args.append(buf)
+    args.extend(scalars)
+    if engine == "oracle":
+        run_oracle(kernel, cfg, bind_args(kernel.params, mem, args))
+    else:
+        cfg.workers = 8
+        launch(hybrid_transform(kernel, cfg), cfg, mem, args)
+    return [mem.view(b, kind).copy() for (kind, _), b in zip(buffers, args)]
+
+
+def warp_semantics() -> dict:
+    lanes = list(range(100, 132))
+    table = [[int(shuffle_down(lanes, lane, off, 32)) for off in range(-40, 40)]
+             for lane in range(32)]
+    votes = {}
+    for width in (4, 8):
+        rows = []
+        for m in range(1 << width):
+            bits = [(m >> k) & 1 for k in range(width)]
+            rows.append([m, reduce_vote(bits, "all"), reduce_vote(bits, "any")])
+        votes[str(width)] = rows
+    return {"source": "warpfold passes/warp_lower.py:17-45",
+            "shfl_down": {"buffer": lanes, "offsets": list(range(-40, 40)), "table": table},
+            "reduce_vote": votes}
+
+
+def oracle_kat() -> dict:
+    reduce_src = """
+__global__ void reduce_warp(global i32* a, global i32* out) {
+    i32 tid = threadIdx.x + blockIdx.x * blockDim.x;
+    i32 val = a[tid];
+    if (threadIdx.x < 32) {
+        for (i32 offset = 16; offset > 0; offset = offset / 2) {
+            val = val + shfl_down(val, offset);
+        }
+    }
+    if (threadIdx.x == 0) { out[blockIdx.x] = val; }
+    a[tid] = val;
+}
+"""
+    out = {}
+    a, o = _run("oracle", reduce_src, 1, 64, [("i32", np.ones(64)), ("i32", np.zeros(1))])
+    out["kat_ones_a"], out["kat_ones_out"] = a, o
+    data = np.arange(128) % 7 - 3
+    a, o = _run("oracle", reduce_src, 2, 64, [("i32", data), ("i32", np.zeros(2))])
+    out["kat_general_in"], out["kat_general_a"], out["kat_general_out"] = data.astype(np.int32), a, o
+    vall = "__global__ void v(global i32* a, global i32* out) { out[threadIdx.x] = vote_all(a[threadIdx.x] > 0); }"
+    _, o = _run("oracle", vall, 1, 32, [("i32", np.ones(32)), ("i32", np.zeros(32))])
+    out["kat_vote_all_out"] = o
+    vany = "__global__ void v(global i32* a, global i32* out) { out[threadIdx.x] = vote_any(a[threadIdx.x] == 9); }"
+    d = np.zeros(64)
+    d[37] = 9
+    _, o = _run("oracle", vany, 1, 64, [("i32", d), ("i32", np.zeros(64))])
+    out["kat_vote_any_in"], out["kat_vote_any_out"] = d.astype(np.int32), o
+    shfl = "__global__ void s(global i32* a, global i32* out) { out[threadIdx.x] = shfl_down(a[threadIdx.x], 1); }"
+    _, o = _run("oracle", shfl, 1, 32, [("i32", np.arange(32)), ("i32", np.zeros(32))])
+    out["kat_shfl_out"] = o
+    return out
+
+
+def c1c2_pin() -> dict:
+    out = {}
+    n, grid, block = 1 << 14, 8, 256
+    for gen in ("i32_full", "i32_small"):
+        a = synthetic.generate(gen, n, seed=7)
+        _, p1 = _run("oracle", C1_I32, grid, block, [("i32", a), ("i32", np.zeros(grid * 8))], [n])
+        _, p2 = _run("launch", C1_I32, grid, block, [("i32", a), ("i32", np.zeros(grid * 8))], [n])
+        assert np.array_equal(p1, p2)
+        out[f"{gen}_partials"] = p1
+    f = synthetic.generate("f32_unit", n, seed=7)
+    _, p1 = _run("oracle", C1_F32, grid, block, [("f32", f), ("f32", np.zeros(grid * 8))], [n])
+    _, p2 = _run("launch", C1_F32, grid, block, [("f32", f), ("f32", np.zeros(grid * 8))], [n])
+    assert np.array_equal(p1.view(np.int32), p2.view(np.int32))
+    out["f32_unit_partials"] = p1
+    out["meta"] = np.array([n, grid, block, 7], dtype=np.int64)
+    return out
+
+
+def c3_pin() -> dict:
+    n, grid, block = 1 << 12, 16, 256
+    a = synthetic.generate("i32_full", n, seed=3)
+    _, o1 = _run("oracle", C3_WARP_PREFIX, grid, block, [("i32", a), ("i32", np.zeros(n))])
+    _, o2 = _run("launch", C3_WARP_PREFIX, grid, block, [("i32", a), ("i32", np.zeros(n))])
+    assert np.array_equal(o1, o2)
+    return {"warp_prefix_out": o1, "meta": np.array([n, grid, block, 3], dtype=np.int64)}
+
+
+def corpus_golden() -> tuple[dict, dict]:
+    arrays, manifest = {}, {}
+    for k in corpus.ALL:
+        for grid, block, warp in ((2, 64, 32), (3, 32, 32)):
+            mem, args = k.build(grid, block, 0)
+            kernel = k.kernel()
+            ids = [a for p, a in zip(kernel.params, args) if p.is_buffer]
+            kinds = [p.kind for p in kernel.params if p.is_buffer]
+            tag = f"{k.name}__g{grid}b{block}w{warp}"
+            for i, (bid, kind) in enumerate(zip(ids, kinds)):
+                arrays[f"{tag}__in{i}"] = mem.view(bid, kind).copy()
+            cfg = LaunchConfig(grid_size=grid, block_size=block, warp_size=warp, workers=1)
+            run_oracle(kernel, cfg, bind_args(kernel.params, mem, args))
+            for i, (bid, kind) in enumerate(zip(ids, kinds)):
+                arrays[f"{tag}__out{i}"] = mem.view(bid, kind).copy()
+            manifest[tag] = {"kernel": k.name, "grid": grid, "block": block, "warp": warp,
+                             "kinds": kinds,
+                             "args": [("buf", kernel.params.index(p)) if p.is_buffer
+                                      else ("scalar", a if not isinstance(a, np.floating)
+                                            else float(a))
+                                      for p, a in zip(kernel.params, args)],
+                             "source": k.source}
+    return arrays, manifest
+
+
+def main() -> None:
+    (HERE / "warp_semantics.json").write_text(json.dumps(warp_semantics(), indent=1))
+    np.savez_compressed(HERE / "oracle_kat.npz", **oracle_kat())
+    np.savez_compressed(HERE / "c1c2_pin.npz", **c1c2_pin())
+    np.savez_compressed(HERE / "c3_pin.npz", **c3_pin())
+    arrays, manifest = corpus_golden()
+    np.savez_compressed(HERE / "corpus.npz", **arrays)
+    (HERE / "corpus_manifest.json").write_text(json.dumps(manifest, indent=1))
+    (HERE / "C1_I32.spk").write_text(C1_I32)
+    (HERE / "C1_F32.spk").write_text(C1_F32)
+    (HERE / "C3_WARP_PREFIX.spk").write_text(C3_WARP_PREFIX)
+    print("golden vectors written to", HERE)
+
+
+if __name__ == "__main__":
+    main()

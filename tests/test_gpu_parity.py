@@ -1,0 +1,398 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the oracle and
+the reference's golden vectors.  Bit-exact for integer work; fp32 within the
+a-priori bound stated in oracle/numpy_oracle.f32_tolerance."""
+
+import json
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from oracle import numpy_oracle as no, semantics, synthetic  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ops():
+    from paper_2112_10034_b200 import build
+    build.build_library()
+    from paper_2112_10034_b200 import ops as _ops
+    torch.cuda.init()
+    return _ops
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+SIZES = [0, 1, 3, 4, 5, 31, 1000, 4095, 4096, 4097, 65536 + 7, (1 << 20) + 3]
+
+
+# ---- synthetic generator -----------------------------------------------------
+
+@pytest.mark.parametrize("gen", synthetic.GENS)
+def test_generator_bit_exact(ops, gen):
+    for n, base in ((1, 0), (1027, 0), (100003, 12345678901)):
+        g = host(ops.fill_synthetic(gen, n, seed=0xABCDEF, base=base, param=437))
+        want = synthetic.generate(gen, n, seed=0xABCDEF, base=base, param=437)
+        assert np.array_equal(g.view(np.uint8), want.view(np.uint8)), (gen, n)
+
+
+# ---- K1 ----------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", SIZES)
+def test_reduce_i32_sizes(ops, n):
+    a = synthetic.generate("i32_full", n, seed=n)
+    got = host(ops.reduce_sum_i32(dev(a)))[0]
+    assert got == no.reduce_sum_i32(a)
+
+
+@pytest.mark.parametrize("block", [128, 256, 512, 1024])
+@pytest.mark.parametrize("grid", [0, 1, 7, 148])
+def test_reduce_i32_blocks_grids(ops, block, grid):
+    a = synthetic.generate("i32_small", 300001, seed=block + grid)
+    assert host(ops.reduce_sum_i32(dev(a), block=block, grid=grid))[0] == no.reduce_sum_i32(a)
+
+
+def test_reduce_i32_misaligned_views(ops):
+    a = synthetic.generate("i32_full", 100000, seed=9)
+    d = dev(a)
+    for off in (1, 2, 3, 5):
+        assert host(ops.reduce_sum_i32(d[off:]))[0] == no.reduce_sum_i32(a[off:])
+
+
+def test_reduce_i32_matches_reference_c1_pin(ops, golden):
+    g = np.load(golden / "c1c2_pin.npz")
+    n, grid, block, seed = (int(v) for v in g["meta"])
+    for gen in ("i32_full", "i32_small"):
+        a = ops.fill_synthetic(gen, n, seed=seed)
+        want = no.reduce_sum_i32(g[f"{gen}_partials"])  # reference partials, wrap-folded
+        assert host(ops.reduce_sum_i32(a, block=256))[0] == want
+
+
+def test_reduce_i32_c1_config(ops):
+    """BASELINE config 1: 2^20 int32, block 256."""
+    n = 1 << 20
+    a = ops.fill_synthetic("i32_full", n, seed=0)
+    want = no.reduce_sum_i32(synthetic.generate("i32_full", n, seed=0))
+    for _ in range(3):  # workspace reuse across launches
+        assert host(ops.reduce_sum_i32(a, block=256))[0] == want
+
+
+# ---- K2 ----------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", SIZES)
+def test_reduce_f32_within_bound(ops, n):
+    a = synthetic.generate("f32_unit", n, seed=n)
+    got = float(host(ops.reduce_sum_f32(dev(a)))[0])
+    tol = no.f32_tolerance(max(n, 1), no.abs_sum(a), chain=max(1, n // 1000))
+    assert abs(got - no.reduce_sum_f32_exact(a)) <= tol + 1e-30
+
+
+def test_reduce_f32_reproducible_and_pinned(ops, golden):
+    g = np.load(golden / "c1c2_pin.npz")
+    n, grid, block, seed = (int(v) for v in g["meta"])
+    x = ops.fill_synthetic("f32_unit", n, seed=seed)
+    r1 = host(ops.reduce_sum_f32(x)).view(np.int32)[0]
+    r2 = host(ops.reduce_sum_f32(x)).view(np.int32)[0]
+    assert r1 == r2  # bitwise reproducible
+    ref_total = np.float32(0)
+    for p in g["f32_unit_partials"]:  # the reference's own result
+        ref_total = np.float32(ref_total + p)
+    a = synthetic.generate("f32_unit", n, seed=seed)
+    tol = no.f32_tolerance(n, no.abs_sum(a), chain=n // (grid * block))
+    assert abs(float(np.int32(r1).view(np.float32)) - float(ref_total)) <= 2 * tol
+
+
+@pytest.mark.slow
+def test_reduce_f32_full_config(ops):
+    """BASELINE config 2 on one GPU: 2^30 fp32."""
+    n = 1 << 30
+    x = ops.fill_synthetic("f32_unit", n, seed=1)
+    got = float(host(ops.reduce_sum_f32(x))[0])
+    exact = float(torch.sum(x, dtype=torch.float64))
+    absx = float(torch.sum(x.abs(), dtype=torch.float64))
+    # per-thread chains: n / (148 SMs * resident threads * 16 chains) elements
+    chain = n // (148 * 1024 * 16) + 16
+    assert abs(got - exact) <= no.f32_tolerance(n, absx, chain=chain)
+    assert abs(got - exact) <= no.f32_tolerance(n, absx)  # SURVEY §8c contract
+    assert float(host(ops.reduce_sum_f32(x))[0]) == got
+    del x
+
+
+# ---- K3 ----------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", SIZES)
+def test_scan_sizes(ops, n):
+    a = synthetic.generate("i32_full", n, seed=n + 1)
+    assert np.array_equal(host(ops.scan_inclusive_i32(dev(a))), no.scan_inclusive_i32(a))
+
+
+def test_scan_carry_inplace_misaligned(ops):
+    a = synthetic.generate("i32_full", 50000, seed=4)
+    carry = torch.tensor([123456789], dtype=torch.int32, device="cuda")
+    got = host(ops.scan_inclusive_i32(dev(a), carry=carry))
+    assert np.array_equal(got, no.scan_inclusive_i32(a, carry=123456789))
+    d = dev(a)
+    ops.scan_inclusive_i32(d, out=d)
+    assert np.array_equal(host(d), no.scan_inclusive_i32(a))
+    d = dev(a)
+    out = torch.empty(50001, dtype=torch.int32, device="cuda")
+    got = host(ops.scan_inclusive_i32(d[1:], out=out[:50000]))
+    assert np.array_equal(got, no.scan_inclusive_i32(a[1:]))
+
+
+def test_scan_repeated_launches(ops):
+    # epoch/ticket reuse: many launches on one workspace, varying sizes
+    for i, n in enumerate([4096 * 3, 10, 4096 * 17 + 5, 1 << 16, 7]):
+        a = synthetic.generate("i32_small", n, seed=i)
+        assert np.array_equal(host(ops.scan_inclusive_i32(dev(a))), no.scan_inclusive_i32(a))
+
+
+def test_scan_matches_reference_warp_prefix(ops, golden):
+    g = np.load(golden / "c3_pin.npz")
+    n, grid, block, seed = (int(v) for v in g["meta"])
+    a = synthetic.generate("i32_full", n, seed=seed)
+    got = host(ops.scan_inclusive_i32(dev(a)))
+    # global scan minus the carry of each 32-element warp segment == the
+    # reference's warp prefix
+    seg_start = np.concatenate([[0], got[31::32][:-1]]).astype(np.int64)
+    local = (got.reshape(-1, 32).astype(np.int64) - seg_start[:, None]) & 0xFFFFFFFF
+    assert np.array_equal(local.astype(np.uint32).view(np.int32).reshape(-1), g["warp_prefix_out"])
+
+
+@pytest.mark.slow
+def test_scan_full_config_properties(ops):
+    """BASELINE config 3 on one GPU: 2^28 int32."""
+    n = 1 << 28
+    x = ops.fill_synthetic("i32_full", n, seed=2)
+    y = ops.scan_inclusive_i32(x)
+    torch.cuda.synchronize()
+    # checksum: last element == wrapping total (K1), first == x[0]
+    total = host(ops.reduce_sum_i32(x))[0]
+    assert host(y[-1:])[0] == total and host(y[:1])[0] == host(x[:1])[0]
+    # linearity: y[i] - y[i-1] == x[i] (mod 2^32) everywhere
+    d = (y[1:].to(torch.int64) - y[:-1].to(torch.int64) - x[1:].to(torch.int64)) % (1 << 32)
+    assert int(d.count_nonzero()) == 0
+    # sampled slices vs numpy with the right carry
+    xs = synthetic.generate("i32_full", 1 << 20, seed=2, base=(1 << 27))
+    carry = int(host(y[(1 << 27) - 1:(1 << 27)])[0])
+    want = no.scan_inclusive_i32(xs, carry=carry)
+    assert np.array_equal(host(y[1 << 27:(1 << 27) + (1 << 20)]), want)
+
+
+# ---- K4 ----------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", SIZES)
+def test_compact_sizes(ops, n):
+    a = synthetic.generate("i32_full", n, seed=n + 2)
+    out, cnt = ops.compact_gt0_i32(dev(a))
+    m = int(host(cnt)[0])
+    want = no.compact_gt0_i32(a)
+    assert m == len(want)
+    assert np.array_equal(host(out)[:m], want)
+
+
+@pytest.mark.parametrize("permille", [0, 10, 500, 1000])
+def test_compact_selectivity(ops, permille):
+    n = 300007
+    x = ops.fill_synthetic("i32_select", n, seed=11, param=permille)
+    out, cnt = ops.compact_gt0_i32(x)
+    a = synthetic.generate("i32_select", n, seed=11, param=permille)
+    want = no.compact_gt0_i32(a)
+    assert int(host(cnt)[0]) == len(want)
+    assert np.array_equal(host(out)[:len(want)], want)
+
+
+@pytest.mark.slow
+def test_compact_full_config(ops):
+    """BASELINE config 4: 2^28 int32, ordered output."""
+    n = 1 << 28
+    x = ops.fill_synthetic("i32_full", n, seed=3)
+    out, cnt = ops.compact_gt0_i32(x)
+    want = torch.masked_select(x, x > 0)
+    m = int(host(cnt)[0])
+    assert m == want.numel()
+    assert torch.equal(out[:m], want)
+
+
+# ---- K5 ----------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", SIZES + [(1 << 22) + 13])
+def test_hist_sizes(ops, n):
+    a = synthetic.generate("u8_uniform", n, seed=n)
+    got = host(ops.histogram256_u8(dev(a))).view(np.uint64)
+    assert np.array_equal(got, no.histogram256_u8(a))
+
+
+@pytest.mark.parametrize("gen,param", [("u8_const", 0), ("u8_const", 255), ("u8_geom", 0)])
+def test_hist_skewed(ops, gen, param):
+    n = 5_000_011
+    x = ops.fill_synthetic(gen, n, seed=5, param=param)
+    want = no.histogram256_u8(synthetic.generate(gen, n, seed=5, param=param))
+    assert np.array_equal(host(ops.histogram256_u8(x)).view(np.uint64), want)
+
+
+def test_hist_misaligned_and_grids(ops):
+    a = synthetic.generate("u8_uniform", 1 << 20, seed=6)
+    d = dev(a)
+    for off in (1, 7, 15):
+        got = host(ops.histogram256_u8(d[off:])).view(np.uint64)
+        assert np.array_equal(got, no.histogram256_u8(a[off:]))
+    for grid in (1, 3, 296):
+        got = host(ops.histogram256_u8(d, grid=grid)).view(np.uint64)
+        assert np.array_equal(got, no.histogram256_u8(a))
+
+
+@pytest.mark.slow
+def test_hist_full_config(ops):
+    """BASELINE config 5 on one GPU: 2^32 uint8 (4 GiB)."""
+    n = 1 << 32
+    x = ops.fill_synthetic("u8_uniform", n, seed=4)
+    bins = host(ops.histogram256_u8(x)).view(np.uint64)
+    assert int(bins.sum()) == n
+    # linearity: the histogram of the whole == sum of histograms of 8 slices
+    parts = np.zeros(256, dtype=np.uint64)
+    step = n // 8
+    for k in range(8):
+        parts += host(ops.histogram256_u8(x[k * step:(k + 1) * step])).view(np.uint64)
+    assert np.array_equal(parts, bins)
+    # one slice against torch's own bincount
+    tb = torch.bincount(x[:1 << 28].to(torch.int32), minlength=256).cpu().numpy()
+    got = host(ops.histogram256_u8(x[:1 << 28])).view(np.uint64)
+    assert np.array_equal(got, tb.astype(np.uint64))
+    del x
+
+
+# ---- P: warp collectives -----------------------------------------------------
+
+def test_shfl_down_golden_table(ops, golden):
+    t = json.loads((golden / "warp_semantics.json").read_text())["shfl_down"]
+    buf = np.array(t["buffer"], dtype=np.int32)
+    for j, off in enumerate(t["offsets"]):
+        got = host(ops.warp_collective("shfl_down", dev(buf), operand=off, block=32))
+        assert got.tolist() == [t["table"][lane][j] for lane in range(32)], off
+
+
+def test_oracle_kats_on_gpu(ops, golden):
+    kat = np.load(golden / "oracle_kat.npz")
+    got = host(ops.warp_collective("shfl_down", dev(np.arange(32, dtype=np.int32)), operand=1))
+    assert np.array_equal(got, kat["kat_shfl_out"])
+    pred = (kat["kat_vote_any_in"] == 9).astype(np.int32)
+    got = host(ops.warp_collective("vote_any", dev(pred), block=64))
+    assert np.array_equal(got, kat["kat_vote_any_out"])
+    got = host(ops.warp_collective("vote_all", dev(np.ones(32, dtype=np.int32))))
+    assert np.array_equal(got, kat["kat_vote_all_out"])
+
+
+KINDS = ["shfl_down", "shfl_up", "shfl_xor", "shfl_idx", "vote_all", "vote_any", "ballot",
+         "reduce_add"]
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("block,width,mask", [
+    (32, 32, 0xFFFFFFFF), (64, 32, 0xFFFFFFFF), (256, 32, 0xFFFFFFFF),
+    (48, 32, 0xFFFFFFFF), (100, 32, 0xFFFFFFFF),          # partial warps
+    (64, 32, 0x0F0F00FF), (96, 32, 0xAAAAAAAA),            # non-full masks
+    (64, 4, 0xFFFFFFFF), (64, 8, 0x00FFFF00), (40, 16, 0xFFFFFFFF), (32, 1, 0xFFFFFFFF),
+])
+def test_collectives_vs_semantics(ops, kind, block, width, mask):
+    rng = np.random.default_rng(block * 131 + width)
+    n = block * 3
+    a = rng.integers(-3, 4, n).astype(np.int32)
+    a[rng.random(n) < 0.3] = 0
+    b = rng.integers(-40, 40, n).astype(np.int32)
+    init = np.full(n, -777, dtype=np.int32)
+    got = host(ops.warp_collective(kind, dev(a), dev(b), block=block, width=width, mask=mask,
+                                   out=dev(init)))
+    want = semantics.collective(kind, a, b, 0, block, width, mask, out_init=init)
+    assert np.array_equal(got, want)
+
+
+# ---- launch() drop-in API ----------------------------------------------------
+
+def test_launch_named_programs(ops):
+    from paper_2112_10034_b200 import DeviceMemory, LaunchConfig, launch, PROGRAMS
+    mem = DeviceMemory()
+    n = 10007
+    a = synthetic.generate("i32_full", n, seed=1)
+    ab = mem.alloc(4 * n)
+    mem.write(ab, a, "i32")
+    ob = mem.alloc(4)
+    launch(PROGRAMS["reduce_sum_i32"], LaunchConfig(grid_size=1, block_size=256), mem, [ab, ob, n])
+    assert mem.host_view(ob, "i32")[0] == no.reduce_sum_i32(a)
+    sb = mem.alloc(4 * n)
+    launch(PROGRAMS["scan_inclusive_i32"], LaunchConfig(block_size=256), mem, [ab, sb, n])
+    assert np.array_equal(mem.host_view(sb, "i32"), no.scan_inclusive_i32(a))
+    cb, kb = mem.alloc(4 * n), mem.alloc(8)
+    launch(PROGRAMS["compact_gt0_i32"], LaunchConfig(), mem, [ab, cb, kb, n])
+    m = int(mem.host_view(kb, "u64")[0])
+    assert np.array_equal(mem.host_view(cb, "i32")[:m], no.compact_gt0_i32(a))
+    u = synthetic.generate("u8_uniform", n, seed=2)
+    ub, hb = mem.alloc(n), mem.alloc(256 * 8)
+    mem.copy_in(ub, u.tobytes())
+    launch(PROGRAMS["histogram256_u8"], LaunchConfig(), mem, [ub, hb, n])
+    assert np.array_equal(mem.host_view(hb, "u64"), no.histogram256_u8(u))
+
+
+def test_launch_errors_follow_reference(ops):
+    from paper_2112_10034_b200 import (DeviceMemory, ExecutionError, LaunchConfig, LaunchError,
+                                       launch, PROGRAMS)
+    mem = DeviceMemory()
+    ab, ob = mem.alloc(40), mem.alloc(4)
+    with pytest.raises(LaunchError, match="kernel takes 3 arguments, got 2"):
+        launch(PROGRAMS["reduce_sum_i32"], LaunchConfig(), mem, [ab, ob])
+    with pytest.raises(ExecutionError, match=r"out-of-bounds read a\[10\], length 10"):
+        launch(PROGRAMS["reduce_sum_i32"], LaunchConfig(), mem, [ab, ob, 11])
+    launch(PROGRAMS["reduce_sum_i32"], LaunchConfig(grid_size=0), mem, [ab, ob, 11])  # no-op
+
+
+def test_launch_warp_program_partial_warps(ops):
+    from paper_2112_10034_b200 import DeviceMemory, LaunchConfig, launch, warp_program
+    mem = DeviceMemory()
+    grid, block = 3, 48
+    n = grid * block
+    a = np.arange(n, dtype=np.int32)
+    off = np.full(n, 2, dtype=np.int32)
+    ab, bb, ob = mem.alloc(4 * n), mem.alloc(4 * n), mem.alloc(4 * n)
+    mem.write(ab, a, "i32")
+    mem.write(bb, off, "i32")
+    launch(warp_program("shfl_down"), LaunchConfig(grid_size=grid, block_size=block), mem,
+           [ab, bb, ob])
+    want = semantics.collective("shfl_down", a, off, 0, block, 32, 0xFFFFFFFF)
+    assert np.array_equal(mem.host_view(ob, "i32"), want)
+
+
+def test_device_memory_roundtrip(ops):
+    from paper_2112_10034_b200 import DeviceMemory, LaunchError
+    mem = DeviceMemory()
+    b = mem.alloc(16)
+    mem.copy_in(b, bytes(range(16)))
+    assert mem.copy_out(b, 4, offset=2) == bytes([2, 3, 4, 5])
+    c = mem.clone()
+    assert c.equal_bytes(mem)
+    with pytest.raises(LaunchError, match="exceeds buffer"):
+        mem.copy_in(b, bytes(17))
+    mem.free(b)
+    with pytest.raises(LaunchError, match="unknown buffer"):
+        mem.raw(b)
+
+
+# ---- host-buffer (end-to-end) entry points -----------------------------------
+
+def test_host_entry_points(ops):
+    n = (64 << 20) + 5  # several staging chunks
+    f = synthetic.generate("f32_unit", n, seed=8)
+    got = ops.reduce_sum_f32_host(torch.from_numpy(f).pin_memory())
+    assert abs(got - no.reduce_sum_f32_exact(f)) <= no.f32_tolerance(n, no.abs_sum(f))
+    a = synthetic.generate("i32_full", n, seed=8)
+    assert ops.reduce_sum_i32_host(a) == no.reduce_sum_i32(a)
+    u = synthetic.generate("u8_uniform", 3 * (128 << 20) + 11, seed=8)
+    assert np.array_equal(ops.histogram256_u8_host(u), no.histogram256_u8(u))
