@@ -19,10 +19,10 @@ __version__ = "0.1.0"
 
 _LAZY = {
     "DeviceMemory": ("memory", "DeviceMemory"),
-    "launch": ("launch", "launch"),
-    "bind_args": ("launch", "bind_args"),
-    "PROGRAMS": ("launch", "PROGRAMS"),
-    "warp_program": ("launch", "warp_program"),
+    "launch": ("runtime", "launch"),
+    "bind_args": ("runtime", "bind_args"),
+    "PROGRAMS": ("runtime", "PROGRAMS"),
+    "warp_program": ("runtime", "warp_program"),
     "ops": ("ops", None),
     "distributed": ("distributed", None),
     "dsl": ("dsl", None),

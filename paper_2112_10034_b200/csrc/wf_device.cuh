@@ -142,4 +142,133 @@ __device__ __forceinline__ uint32_t lookback_exclusive(const uint64_t *desc,
   }
 }
 
+
+// Wide look-back: lane l inspects the K predecessors tile-1-K*l-k (k = 0..K-1),
+// so one round trip to L2 covers 32*K tiles.  The prefix frontier therefore
+// advances up to 32*K tiles per round trip instead of 32, which is what keeps
+// a single-pass scan at HBM speed when hundreds of tiles are in flight.
+template <int K>
+__device__ __forceinline__ uint32_t lookback_exclusive_wide(const uint64_t *desc,
+                                                            uint32_t tile, uint32_t epoch) {
+  const uint32_t lane = lane_id();
+  uint32_t excl = 0;
+  int64_t hi = int64_t(tile) - 1;
+  while (true) {
+    uint32_t st[K], val[K];
+    while (true) {
+      bool valid = true;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int64_t p = hi - int64_t(lane) * K - k;
+        if (p >= 0) {
+          const uint64_t d = ld_relaxed_gpu(desc + p);
+          st[k] = uint32_t(d >> 34) == epoch ? uint32_t(d >> 32) & 3u : kStInvalid;
+          val[k] = uint32_t(d);
+        } else {
+          st[k] = kStPrefix;
+          val[k] = 0;
+        }
+        valid &= st[k] != kStInvalid;
+      }
+      if (__all_sync(kFull, valid)) break;
+      __nanosleep(64);
+    }
+    int kp = K;  // nearest PREFIX inside this lane's run
+#pragma unroll
+    for (int k = K - 1; k >= 0; --k)
+      if (st[k] == kStPrefix) kp = k;
+    uint32_t run = 0, upto = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      run += val[k];
+      if (k <= kp) upto += val[k];
+    }
+    const uint32_t lanes = __ballot_sync(kFull, kp < K);
+    if (lanes) {
+      const uint32_t first = __ffs(lanes) - 1;
+      excl += __reduce_add_sync(kFull, lane < first ? run : (lane == first ? upto : 0u));
+      return excl;
+    }
+    excl += __reduce_add_sync(kFull, run);
+    hi -= 32 * K;
+  }
+}
+
+}  // namespace wf
+
+// ---- TMA bulk copies + mbarriers (sm_90+/sm_100a async proxy) ------------
+namespace wf {
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+// make barrier initialisation visible to the async proxy (TMA unit)
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// 1-D bulk copy global -> shared, completion reported on `bar` (UBLKCP)
+__device__ __forceinline__ void tma_load_1d(void *dst_smem, const void *src, uint32_t bytes,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// 1-D bulk copy shared -> global, tracked by bulk groups
+__device__ __forceinline__ void tma_store_1d(void *dst, const void *src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src_smem)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// wait until every committed bulk store has finished READING shared memory
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// wait until every committed bulk store has fully completed
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// generic-proxy smem writes -> visible to the async proxy (before a TMA store)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 }  // namespace wf

@@ -22,6 +22,8 @@
 #include "wf_device.cuh"
 #include "wf_internal.h"
 
+#include <cstdlib>
+
 namespace wf {
 namespace {
 
@@ -66,7 +68,7 @@ __device__ __forceinline__ uint32_t tile_prefix(uint64_t *__restrict__ desc,
       if (threadIdx.x == 0) st_relaxed_gpu(desc, pack_desc(epoch, kStPrefix, excl + aggregate));
     } else {
       if (threadIdx.x == 0) st_relaxed_gpu(desc + tile, pack_desc(epoch, kStAggregate, aggregate));
-      excl = lookback_exclusive(desc, tile, epoch);
+      excl = lookback_exclusive_wide<8>(desc, tile, epoch);
       if (threadIdx.x == 0) st_relaxed_gpu(desc + tile, pack_desc(epoch, kStPrefix, excl + aggregate));
     }
     if (threadIdx.x == 0) s_prefix = excl;
@@ -214,6 +216,242 @@ __global__ void __launch_bounds__(BLOCK)
   if (tile == ntiles - 1 && threadIdx.x == 0) *count = uint64_t(prefix) + agg;
 }
 
+
+// ---------------------------------------------------------------------------
+// Persistent, TMA-pipelined variant (16-byte aligned buffers).
+//
+// grid = SMs x resident CTAs.  Each CTA draws tile ids from the ticket
+// counter and keeps a ring of PSTAGES shared-memory stages: the 1-D bulk copy
+// (cp.async.bulk -> UBLKCP) of tile t+1 is in flight while tile t is scanned
+// and looks back, so HBM latency overlaps the look-back latency.  Scan results
+// are written back into the stage and leave through a bulk store
+// (cp.async.bulk.global.shared); compaction writes its (unaligned) output with
+// coalesced stores from the stage.
+//
+// Ticket protocol: every CTA draws until it receives an id >= ntiles (exactly
+// one over-draw per CTA), so the CTA whose draw returns ntiles + grid - 1 is
+// the last drawer: it resets the counter and bumps the epoch.  Every CTA read
+// the epoch before its first draw, hence before the bump.
+constexpr int PBLOCK = 256;
+constexpr int PNW = PBLOCK / 32;
+constexpr int PVEC = 8;                          // 128-item chunks per warp
+constexpr uint32_t PTILE = uint32_t(PBLOCK) * PVEC * 4;   // 8192 items, 32 KiB
+constexpr int PSTAGES = 2;
+constexpr uint32_t kNoTile = 0xffffffffu;
+
+struct PersistShared {
+  uint64_t full[PSTAGES];
+  uint32_t tile[PSTAGES];
+  uint32_t epoch;
+  uint32_t prefix;
+  uint32_t wtot[PNW];
+};
+
+__device__ __forceinline__ uint32_t draw_ticket(TileHeader *hdr, uint32_t ntiles,
+                                                uint32_t epoch, bool &drained) {
+  const uint32_t t = atomicAdd(&hdr->ticket, 1u);
+  if (t >= ntiles) {
+    drained = true;
+    if (t == ntiles + gridDim.x - 1) {  // last of all draws
+      atomicExch(&hdr->ticket, 0u);
+      atomicExch(&hdr->epoch, (epoch + 1) & kEpochMask);
+    }
+    return kNoTile;
+  }
+  return t;
+}
+
+template <bool COMPACT>
+__global__ void __launch_bounds__(PBLOCK)
+    tile_persistent_kernel(const int32_t *__restrict__ in, int32_t *__restrict__ out,
+                           uint64_t n, uint32_t ntiles,
+                           const int32_t *__restrict__ carry_in,
+                           uint64_t *__restrict__ count, uint64_t *__restrict__ desc,
+                           TileHeader *__restrict__ hdr) {
+  extern __shared__ __align__(128) uint8_t dyn_smem[];
+  __shared__ PersistShared sh;
+  int32_t *stage0 = reinterpret_cast<int32_t *>(dyn_smem);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  bool drained = false;  // meaningful in thread 0 only
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < PSTAGES; ++s) mbar_init(&sh.full[s], 1);
+    fence_barrier_init();
+    sh.epoch = ld_volatile_u32(&hdr->epoch) & kEpochMask;
+    __threadfence();
+    for (int s = 0; s < PSTAGES; ++s) {
+      const uint32_t t = drained ? kNoTile : draw_ticket(hdr, ntiles, sh.epoch, drained);
+      sh.tile[s] = t;
+      if (t != kNoTile && uint64_t(t + 1) * PTILE <= n) {
+        mbar_arrive_expect_tx(&sh.full[s], PTILE * 4);
+        tma_load_1d(stage0 + s * PTILE, in + uint64_t(t) * PTILE, PTILE * 4, &sh.full[s]);
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t epoch = sh.epoch;
+  uint32_t phase = 0;  // bit s = parity of stage s
+
+  for (uint32_t it = 0;; ++it) {
+    const int s = int(it % PSTAGES);
+    const uint32_t tile = sh.tile[s];
+    if (tile == kNoTile) break;
+    int32_t *buf = stage0 + s * PTILE;
+    const uint64_t base = uint64_t(tile) * PTILE;
+    const bool full = base + PTILE <= n;
+    if (full) {
+      mbar_wait(&sh.full[s], (phase >> s) & 1u);
+      phase ^= 1u << s;
+    } else {  // ragged last tile: guarded cooperative loads
+      for (uint32_t i = threadIdx.x; i < PTILE; i += PBLOCK)
+        buf[i] = base + i < n ? in[base + i] : 0;
+      __syncthreads();
+    }
+
+    uint32_t x[PVEC][4];
+    const uint32_t off0 = warp * (PVEC * 128) + lane * 4;
+#pragma unroll
+    for (int j = 0; j < PVEC; ++j) {
+      const uint4 q = *reinterpret_cast<const uint4 *>(buf + off0 + j * 128);
+      x[j][0] = q.x; x[j][1] = q.y; x[j][2] = q.z; x[j][3] = q.w;
+    }
+
+    uint32_t carry = 0;
+    uint32_t pos[PVEC];
+    if (!COMPACT) {
+#pragma unroll
+      for (int j = 0; j < PVEC; ++j) {
+        x[j][1] += x[j][0];
+        x[j][2] += x[j][1];
+        x[j][3] += x[j][2];
+        const uint32_t t = x[j][3];
+        uint32_t v = t;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, v, d);
+          if (lane >= uint32_t(d)) v += y;
+        }
+        const uint32_t add = carry + v - t;
+        carry += __shfl_sync(kFull, v, 31);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[j][k] += add;
+      }
+    } else {
+      const uint32_t lt = lanemask_lt();
+#pragma unroll
+      for (int j = 0; j < PVEC; ++j) {
+        uint32_t excl = 0, tot = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const bool f = int32_t(x[j][k]) > 0;  // padding of a ragged tile is 0
+          const uint32_t b = __ballot_sync(kFull, f);
+          excl += __popc(b & lt);
+          tot += __popc(b);
+          if (!f) x[j][k] = 0u;
+        }
+        pos[j] = carry + excl;
+        carry += tot;
+      }
+    }
+    if (lane == 0) sh.wtot[warp] = carry;
+    __syncthreads();  // also: every thread has its items in registers
+    uint32_t wexcl = 0, agg = 0;
+#pragma unroll
+    for (int w = 0; w < PNW; ++w) {
+      const uint32_t v = sh.wtot[w];
+      wexcl += uint32_t(w) < warp ? v : 0u;
+      agg += v;
+    }
+    if (COMPACT) {  // in-place tile-local compaction (items are in registers)
+#pragma unroll
+      for (int j = 0; j < PVEC; ++j) {
+        uint32_t p = wexcl + pos[j];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (x[j][k] != 0u) buf[p++] = int32_t(x[j][k]);
+      }
+    }
+    // decoupled look-back (warp 0)
+    if (warp == 0) {
+      uint32_t excl;
+      if (tile == 0) {
+        excl = (!COMPACT && carry_in != nullptr) ? uint32_t(*carry_in) : 0u;
+        if (lane == 0) st_relaxed_gpu(desc, pack_desc(epoch, kStPrefix, excl + agg));
+      } else {
+        if (lane == 0) st_relaxed_gpu(desc + tile, pack_desc(epoch, kStAggregate, agg));
+        excl = lookback_exclusive_wide<8>(desc, tile, epoch);
+        if (lane == 0) st_relaxed_gpu(desc + tile, pack_desc(epoch, kStPrefix, excl + agg));
+      }
+      if (lane == 0) sh.prefix = excl;
+    }
+    __syncthreads();
+    const uint32_t prefix = sh.prefix;
+
+    if (!COMPACT) {
+      const uint32_t add = prefix + wexcl;
+#pragma unroll
+      for (int j = 0; j < PVEC; ++j) {
+        uint4 q;
+        q.x = x[j][0] + add; q.y = x[j][1] + add; q.z = x[j][2] + add; q.w = x[j][3] + add;
+        *reinterpret_cast<uint4 *>(buf + off0 + j * 128) = q;
+      }
+      if (full) {
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          tma_store_1d(out + base, buf, PTILE * 4);
+          bulk_commit();
+        }
+      } else {
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < PTILE && base + i < n; i += PBLOCK) out[base + i] = buf[i];
+      }
+    } else {
+      int32_t *dst = out + prefix;
+      for (uint32_t i = threadIdx.x; i < agg; i += PBLOCK) dst[i] = buf[i];
+      if (tile == ntiles - 1 && threadIdx.x == 0) *count = uint64_t(prefix) + agg;
+    }
+    __syncthreads();  // stage s fully consumed by the threads
+    if (threadIdx.x == 0) {  // refill stage s with the next tile
+      const uint32_t t = drained ? kNoTile : draw_ticket(hdr, ntiles, epoch, drained);
+      sh.tile[s] = t;
+      if (!COMPACT && t != kNoTile) bulk_wait_read_all();  // bulk store has left stage s
+      if (t != kNoTile && uint64_t(t + 1) * PTILE <= n) {
+        mbar_arrive_expect_tx(&sh.full[s], PTILE * 4);
+        tma_load_1d(buf, in + uint64_t(t) * PTILE, PTILE * 4, &sh.full[s]);
+      }
+    }
+    __syncthreads();
+  }
+  if (!COMPACT && threadIdx.x == 0) bulk_wait_all();
+}
+
+constexpr size_t kPersistSmem = size_t(PSTAGES) * PTILE * 4;
+
+template <bool COMPACT>
+int persistent_grid(uint32_t ntiles) {
+  static int per_sm[2] = {0, 0};
+  int &b = per_sm[COMPACT];
+  if (b == 0) {
+    cudaFuncSetAttribute(tile_persistent_kernel<COMPACT>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPersistSmem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tile_persistent_kernel<COMPACT>, PBLOCK,
+                                                  kPersistSmem);
+    if (b < 1) b = 1;
+  }
+  const uint32_t full = uint32_t(b) * uint32_t(sm_count(current_device()));
+  return int(ntiles < full ? ntiles : full);
+}
+
+bool persistent_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("WF_SCAN_PERSISTENT");
+    v = (e == nullptr || e[0] != '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 }  // namespace
 
 cudaError_t launch_scan_i32(const int32_t *in, int32_t *out, uint64_t n,
@@ -223,6 +461,13 @@ cudaError_t launch_scan_i32(const int32_t *in, int32_t *out, uint64_t n,
   auto *hdr = reinterpret_cast<TileHeader *>(ws);
   auto *desc = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + kWsHeader);
   const bool aligned = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u) == 0;
+  if (aligned && persistent_enabled()) {
+    const uint64_t pt = (n + PTILE - 1) / PTILE;
+    const int grid = persistent_grid<false>(uint32_t(pt));
+    tile_persistent_kernel<false><<<grid, PBLOCK, kPersistSmem, s>>>(
+        in, out, n, uint32_t(pt), carry, nullptr, desc, hdr);
+    return cudaGetLastError();
+  }
   scan_i32_kernel<<<uint32_t(ntiles), BLOCK, 0, s>>>(in, out, n, uint32_t(ntiles), aligned,
                                                       carry, desc, hdr);
   return cudaGetLastError();
@@ -235,6 +480,13 @@ cudaError_t launch_compact_gt0_i32(const int32_t *in, uint64_t n, int32_t *out,
   auto *hdr = reinterpret_cast<TileHeader *>(ws);
   auto *desc = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + kWsHeader);
   const bool aligned = (reinterpret_cast<uintptr_t>(in) & 15u) == 0;
+  if (aligned && persistent_enabled()) {
+    const uint64_t pt = (n + PTILE - 1) / PTILE;
+    const int grid = persistent_grid<true>(uint32_t(pt));
+    tile_persistent_kernel<true><<<grid, PBLOCK, kPersistSmem, s>>>(
+        in, out, n, uint32_t(pt), nullptr, count, desc, hdr);
+    return cudaGetLastError();
+  }
   compact_gt0_kernel<<<uint32_t(ntiles), BLOCK, 0, s>>>(in, n, uint32_t(ntiles), aligned, out,
                                                          count, desc, hdr);
   return cudaGetLastError();

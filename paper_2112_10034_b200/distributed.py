@@ -57,9 +57,10 @@ def exchange(local: torch.Tensor, group=None) -> torch.Tensor:
     rank, world = _world(group)
     if world == 1:
         return local.reshape(1, *local.shape)
-    out = torch.empty((world, *local.shape), dtype=local.dtype, device=local.device)
-    dist.all_gather_into_tensor(out, local.contiguous(), group=group)
-    return out
+    flat = local.contiguous().reshape(-1)
+    out = torch.empty(world * flat.numel(), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, flat, group=group)
+    return out.reshape(world, *local.shape)
 
 
 def reduce_sum_f32(x_local: torch.Tensor, group=None, block: int = 256) -> torch.Tensor:

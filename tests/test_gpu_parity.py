@@ -145,7 +145,7 @@ def test_scan_carry_inplace_misaligned(ops):
     assert np.array_equal(host(d), no.scan_inclusive_i32(a))
     d = dev(a)
     out = torch.empty(50001, dtype=torch.int32, device="cuda")
-    got = host(ops.scan_inclusive_i32(d[1:], out=out[:50000]))
+    got = host(ops.scan_inclusive_i32(d[1:], out=out[2:50001]))  # both misaligned
     assert np.array_equal(got, no.scan_inclusive_i32(a[1:]))
 
 

@@ -67,7 +67,7 @@ class _FakeMem:
 
 
 def test_bind_args_messages():
-    from paper_2112_10034_b200.launch import Param, bind_args
+    from paper_2112_10034_b200.runtime import Param, bind_args
     params = [Param("a", "i32", True), Param("n", "i32", False), Param("s", "f32", False)]
     with pytest.raises(errors.LaunchError, match="kernel takes 3 arguments, got 2"):
         bind_args(params, _FakeMem(), [1, 2])
@@ -82,7 +82,7 @@ def test_bind_args_messages():
 
 
 def test_program_registry_signatures():
-    from paper_2112_10034_b200.launch import PROGRAMS, warp_program
+    from paper_2112_10034_b200.runtime import PROGRAMS, warp_program
     assert set(PROGRAMS) == {"reduce_sum_i32", "reduce_sum_f32", "scan_inclusive_i32",
                              "compact_gt0_i32", "histogram256_u8"}
     assert [p.name for p in PROGRAMS["compact_gt0_i32"].params] == ["a", "out", "count", "n"]
