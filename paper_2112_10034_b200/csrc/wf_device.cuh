@@ -77,6 +77,10 @@ __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 // launches read as "not yet published" and the descriptor array never needs
 // clearing between launches.
 enum : uint32_t { kStInvalid = 0, kStAggregate = 1, kStPrefix = 2 };
+#ifndef WF_DSTRIDE
+#define WF_DSTRIDE 16  // descriptor stride in 8-byte words (16 = one per 128-byte line)
+#endif
+constexpr int kDescStride = WF_DSTRIDE;
 constexpr uint32_t kEpochMask = (1u << 30) - 1;
 
 __device__ __forceinline__ uint64_t pack_desc(uint32_t epoch, uint32_t st,
@@ -105,48 +109,12 @@ __device__ __forceinline__ void take_ticket(TileHeader *hdr, uint32_t ntiles,
   }
 }
 
-// Warp-parallel decoupled look-back (called by all 32 lanes of one warp).
-// Returns the exclusive prefix (wrapping uint32 sum) of all tiles < `tile`.
-// Each lane inspects one predecessor; the window slides back 32 tiles at a
-// time until a tile with an inclusive prefix is found.
-__device__ __forceinline__ uint32_t lookback_exclusive(const uint64_t *desc,
-                                                       uint32_t tile,
-                                                       uint32_t epoch) {
-  const uint32_t lane = lane_id();
-  uint32_t excl = 0;
-  int64_t pred_base = int64_t(tile) - 1;
-  while (true) {
-    const int64_t p = pred_base - int64_t(lane);
-    uint32_t st, val;
-    while (true) {
-      if (p >= 0) {
-        const uint64_t d = ld_relaxed_gpu(desc + p);
-        const bool live = uint32_t(d >> 34) == epoch;
-        st = live ? uint32_t(d >> 32) & 3u : kStInvalid;
-        val = uint32_t(d);
-      } else {
-        st = kStPrefix;  // virtual tile before tile 0 contributes nothing
-        val = 0;
-      }
-      if (__all_sync(kFull, st != kStInvalid)) break;
-      __nanosleep(32);
-    }
-    const uint32_t prefix_lanes = __ballot_sync(kFull, st == kStPrefix);
-    if (prefix_lanes) {
-      const uint32_t first = __ffs(prefix_lanes) - 1;  // nearest prefix tile
-      excl += __reduce_add_sync(kFull, lane <= first ? val : 0u);
-      return excl;
-    }
-    excl += __reduce_add_sync(kFull, val);
-    pred_base -= 32;
-  }
-}
-
-
 // Wide look-back: lane l inspects the K predecessors tile-1-K*l-k (k = 0..K-1),
-// so one round trip to L2 covers 32*K tiles.  The prefix frontier therefore
-// advances up to 32*K tiles per round trip instead of 32, which is what keeps
-// a single-pass scan at HBM speed when hundreds of tiles are in flight.
+// so one round trip to L2 covers 32*K tiles and the prefix frontier advances
+// up to 32*K tiles per round trip instead of 32.  Descriptors already seen
+// valid are kept (an aggregate never changes), only not-yet-published ones
+// are re-polled, and the window resolves as soon as every tile nearer than
+// the nearest inclusive prefix is valid — so polling traffic stays small.
 template <int K>
 __device__ __forceinline__ uint32_t lookback_exclusive_wide(const uint64_t *desc,
                                                             uint32_t tile, uint32_t epoch) {
@@ -155,40 +123,52 @@ __device__ __forceinline__ uint32_t lookback_exclusive_wide(const uint64_t *desc
   int64_t hi = int64_t(tile) - 1;
   while (true) {
     uint32_t st[K], val[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) st[k] = kStInvalid;
+    uint32_t backoff = 16;
     while (true) {
-      bool valid = true;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        const int64_t p = hi - int64_t(lane) * K - k;
-        if (p >= 0) {
-          const uint64_t d = ld_relaxed_gpu(desc + p);
-          st[k] = uint32_t(d >> 34) == epoch ? uint32_t(d >> 32) & 3u : kStInvalid;
-          val[k] = uint32_t(d);
-        } else {
-          st[k] = kStPrefix;
-          val[k] = 0;
+        if (st[k] == kStInvalid) {
+          const int64_t p = hi - int64_t(lane) * K - k;
+          if (p >= 0) {
+            const uint64_t d = ld_relaxed_gpu(desc + p * kDescStride);
+            st[k] = uint32_t(d >> 34) == epoch ? uint32_t(d >> 32) & 3u : kStInvalid;
+            val[k] = uint32_t(d);
+          } else {
+            st[k] = kStPrefix;
+            val[k] = 0;
+          }
         }
-        valid &= st[k] != kStInvalid;
       }
-      if (__all_sync(kFull, valid)) break;
-      __nanosleep(64);
-    }
-    int kp = K;  // nearest PREFIX inside this lane's run
+      int kp = K, ki = K;  // nearest prefix / nearest invalid in this lane's run
 #pragma unroll
-    for (int k = K - 1; k >= 0; --k)
-      if (st[k] == kStPrefix) kp = k;
-    uint32_t run = 0, upto = 0;
+      for (int k = K - 1; k >= 0; --k) {
+        if (st[k] == kStPrefix) kp = k;
+        if (st[k] == kStInvalid) ki = k;
+      }
+      const uint32_t lp = __ballot_sync(kFull, kp < K);
+      const uint32_t li = __ballot_sync(kFull, ki < K);
+      const uint32_t pos_p = lp ? (__ffs(lp) - 1) * K + __shfl_sync(kFull, kp, __ffs(lp) - 1) : ~0u;
+      const uint32_t pos_i = li ? (__ffs(li) - 1) * K + __shfl_sync(kFull, ki, __ffs(li) - 1) : ~0u;
+      if (lp && pos_p < pos_i) {  // resolved: everything nearer than the prefix is valid
+        uint32_t c = 0;
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      run += val[k];
-      if (k <= kp) upto += val[k];
+        for (int k = 0; k < K; ++k)
+          if (lane * K + k <= pos_p) c += val[k];
+        excl += __reduce_add_sync(kFull, c);
+        return excl;
+      }
+      if (!li) break;  // all aggregates, no prefix: slide the window
+#ifndef WF_BACKOFF_MAX
+#define WF_BACKOFF_MAX 256
+#endif
+      if (WF_BACKOFF_MAX > 0) __nanosleep(backoff);
+      backoff = backoff < WF_BACKOFF_MAX ? backoff * 2 : WF_BACKOFF_MAX;
     }
-    const uint32_t lanes = __ballot_sync(kFull, kp < K);
-    if (lanes) {
-      const uint32_t first = __ffs(lanes) - 1;
-      excl += __reduce_add_sync(kFull, lane < first ? run : (lane == first ? upto : 0u));
-      return excl;
-    }
+    uint32_t run = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) run += val[k];
     excl += __reduce_add_sync(kFull, run);
     hi -= 32 * K;
   }

@@ -1,17 +1,31 @@
 // wf_scan.cu — K3 scan_inclusive_i32 and K4 compact_gt0_i32.
 //
-// Both are single-pass tile kernels with decoupled look-back:
-//   tile = 256 threads x 16 items = 4096 int32 (16 KiB).  Warp w of the tile
-//   owns 4 consecutive 128-item chunks; in chunk j lane l holds items
-//   4l..4l+3 (one 16-byte load), so a warp-load is 512 contiguous bytes and a
-//   lane's items stay in memory order.
+// Both are single-pass tile kernels with decoupled look-back.
 //
-// K3 reference analog: the CUDA SDK shfl_scan (warp scan with __shfl_up_sync,
-// warp sums in smem, block carry) that the reference can only express as a
-// lane-reversed shfl_down suffix scan (corpus.py:347-364);
-// its cross-block carries would need several launches through a host
-// description (runtime/hostdesc.py:109-129).  Here the carries flow between
-// tiles in the same launch through the look-back descriptors.
+// Main path (16-byte aligned buffers): a persistent grid (SMs x resident
+// CTAs, 7 per SM) of 256-thread CTAs.  Each CTA draws tile ids from an atomic
+// ticket, pulls the 32 KiB tile into shared memory with ONE 1-D bulk copy
+// (cp.async.bulk -> UBLKCP, completion on an mbarrier), and works on the
+// stage in two passes so registers stay at 32/thread:
+//   pass A  per-warp totals (REDUX.SUM) -> tile aggregate -> published;
+//           warp 0 runs the decoupled look-back for the exclusive prefix
+//   pass B  per 128-item chunk: thread-serial scan of 4 items, SHFL.UP warp
+//           scan (the SDK shfl_scan step), running carry; results go back
+//           into the stage and leave via a bulk store (K3), or selected items
+//           are written by ballot+popc position straight to global memory (K4)
+// Fallback path (misaligned buffers): one 16 KiB register tile per CTA.
+//
+// Measured design choices (tools/sweep*.sh, profiles/r01_*): tile
+// descriptors sit one per 128-byte line (hot-line polling otherwise halves
+// throughput); ONE stage per CTA (a prefetched tile holds its ticket without
+// publishing an aggregate and stalls every later look-back); look-back window
+// 32 tiles for the scan, 64 for compaction.
+//
+// K3 reference analog: the CUDA SDK shfl_scan that the reference can only
+// express as a lane-reversed shfl_down suffix scan (corpus.py:347-364,
+// SURVEY.md §8a C3); its cross-block carries would need several launches
+// through a host description (runtime/hostdesc.py:109-129).  Here the carries
+// flow between tiles inside one launch through the look-back descriptors.
 //
 // K4 reference analog: none expressible (no ballot / atomics in the DSL,
 // dsl/lexer.py:18-25); CUDA-semantics extension with the warp-aggregated
@@ -24,7 +38,38 @@
 
 #include <cstdlib>
 
+#ifndef WF_LBK
+#define WF_LBK 1  // scan: look-back predecessors per lane (window = 32 * WF_LBK)
+#endif
+#ifndef WF_LBK_COMPACT
+#define WF_LBK_COMPACT 2  // compaction look-back width (measured best, tools/sweep3.sh)
+#endif
+#ifndef WF_PVEC
+#define WF_PVEC 8  // persistent tile = 256 threads x 4 x WF_PVEC items
+#endif
+#ifndef WF_MINB
+#define WF_MINB 8  // __launch_bounds__ min blocks per SM of the tile kernels
+#endif
+#ifndef WF_TRACE
+#define WF_TRACE 0
+#endif
+#ifndef WF_PSTAGES
+#define WF_PSTAGES 1  // >1 prefetches tiles whose aggregates then publish late
+#endif
+
 namespace wf {
+#if WF_TRACE
+__device__ unsigned long long *g_wf_trace = nullptr;  // [tile][4] globaltimer stamps
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define WF_STAMP(tile, k) \
+  if (threadIdx.x == 0 && g_wf_trace) g_wf_trace[uint64_t(tile) * 4 + (k)] = gtimer()
+#else
+#define WF_STAMP(tile, k)
+#endif
 namespace {
 
 constexpr int BLOCK = kScanBlock;
@@ -67,9 +112,9 @@ __device__ __forceinline__ uint32_t tile_prefix(uint64_t *__restrict__ desc,
       excl = carry_in;
       if (threadIdx.x == 0) st_relaxed_gpu(desc, pack_desc(epoch, kStPrefix, excl + aggregate));
     } else {
-      if (threadIdx.x == 0) st_relaxed_gpu(desc + tile, pack_desc(epoch, kStAggregate, aggregate));
-      excl = lookback_exclusive_wide<8>(desc, tile, epoch);
-      if (threadIdx.x == 0) st_relaxed_gpu(desc + tile, pack_desc(epoch, kStPrefix, excl + aggregate));
+      if (threadIdx.x == 0) st_relaxed_gpu(desc + uint64_t(tile) * kDescStride, pack_desc(epoch, kStAggregate, aggregate));
+      excl = lookback_exclusive_wide<WF_LBK>(desc, tile, epoch);
+      if (threadIdx.x == 0) st_relaxed_gpu(desc + uint64_t(tile) * kDescStride, pack_desc(epoch, kStPrefix, excl + aggregate));
     }
     if (threadIdx.x == 0) s_prefix = excl;
   }
@@ -77,7 +122,7 @@ __device__ __forceinline__ uint32_t tile_prefix(uint64_t *__restrict__ desc,
   return s_prefix;
 }
 
-__global__ void __launch_bounds__(BLOCK)
+__global__ void __launch_bounds__(BLOCK, WF_MINB)
     scan_i32_kernel(const int32_t *__restrict__ in, int32_t *__restrict__ out,
                     uint64_t n, uint32_t ntiles, bool aligned,
                     const int32_t *__restrict__ carry_in,
@@ -95,6 +140,7 @@ __global__ void __launch_bounds__(BLOCK)
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t base = uint64_t(tile) * TILE + uint64_t(warp) * WSEG + lane * 4;
   const bool vec = aligned && uint64_t(tile + 1) * TILE <= n;
+  WF_STAMP(tile, 0);
 
   uint32_t x[VEC][4];
   load_tile(in, n, base, vec, x);
@@ -129,7 +175,9 @@ __global__ void __launch_bounds__(BLOCK)
     agg += v;
   }
   const uint32_t cin = (tile == 0 && carry_in != nullptr) ? uint32_t(*carry_in) : 0u;
+  WF_STAMP(tile, 1);
   const uint32_t add = tile_prefix(desc, tile, epoch, agg, cin) + wexcl;
+  WF_STAMP(tile, 2);
 
   if (vec) {
 #pragma unroll
@@ -147,9 +195,10 @@ __global__ void __launch_bounds__(BLOCK)
         if (idx < n) out[idx] = int32_t(x[j][k] + add);
       }
   }
+  WF_STAMP(tile, 3);
 }
 
-__global__ void __launch_bounds__(BLOCK)
+__global__ void __launch_bounds__(BLOCK, WF_MINB)
     compact_gt0_kernel(const int32_t *__restrict__ in, uint64_t n,
                        uint32_t ntiles, bool aligned,
                        int32_t *__restrict__ out, uint64_t *__restrict__ count,
@@ -232,11 +281,14 @@ __global__ void __launch_bounds__(BLOCK)
 // one over-draw per CTA), so the CTA whose draw returns ntiles + grid - 1 is
 // the last drawer: it resets the counter and bumps the epoch.  Every CTA read
 // the epoch before its first draw, hence before the bump.
-constexpr int PBLOCK = 256;
+#ifndef WF_PBLOCK
+#define WF_PBLOCK 256
+#endif
+constexpr int PBLOCK = WF_PBLOCK;
 constexpr int PNW = PBLOCK / 32;
-constexpr int PVEC = 8;                          // 128-item chunks per warp
+constexpr int PVEC = WF_PVEC;                     // 128-item chunks per warp
 constexpr uint32_t PTILE = uint32_t(PBLOCK) * PVEC * 4;   // 8192 items, 32 KiB
-constexpr int PSTAGES = 2;
+constexpr int PSTAGES = WF_PSTAGES;
 constexpr uint32_t kNoTile = 0xffffffffu;
 
 struct PersistShared {
@@ -272,6 +324,7 @@ __global__ void __launch_bounds__(PBLOCK)
   __shared__ PersistShared sh;
   int32_t *stage0 = reinterpret_cast<int32_t *>(dyn_smem);
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lt = lanemask_lt();
 
   bool drained = false;  // meaningful in thread 0 only
   if (threadIdx.x == 0) {
@@ -281,6 +334,7 @@ __global__ void __launch_bounds__(PBLOCK)
     __threadfence();
     for (int s = 0; s < PSTAGES; ++s) {
       const uint32_t t = drained ? kNoTile : draw_ticket(hdr, ntiles, sh.epoch, drained);
+      if (t != kNoTile) WF_STAMP(t, 0);
       sh.tile[s] = t;
       if (t != kNoTile && uint64_t(t + 1) * PTILE <= n) {
         mbar_arrive_expect_tx(&sh.full[s], PTILE * 4);
@@ -302,74 +356,34 @@ __global__ void __launch_bounds__(PBLOCK)
     if (full) {
       mbar_wait(&sh.full[s], (phase >> s) & 1u);
       phase ^= 1u << s;
-    } else {  // ragged last tile: guarded cooperative loads
+      WF_STAMP(tile, 1);
+    } else {  // ragged last tile: guarded cooperative loads, zero padding
       for (uint32_t i = threadIdx.x; i < PTILE; i += PBLOCK)
         buf[i] = base + i < n ? in[base + i] : 0;
       __syncthreads();
     }
-
-    uint32_t x[PVEC][4];
+    // warp w owns PVEC consecutive 128-item chunks of the stage
     const uint32_t off0 = warp * (PVEC * 128) + lane * 4;
-#pragma unroll
+
+    // pass A: warp totals (sum, or number of selected items)
+    uint32_t t = 0;
+#pragma unroll 4
     for (int j = 0; j < PVEC; ++j) {
       const uint4 q = *reinterpret_cast<const uint4 *>(buf + off0 + j * 128);
-      x[j][0] = q.x; x[j][1] = q.y; x[j][2] = q.z; x[j][3] = q.w;
+      if (COMPACT)
+        t += (int32_t(q.x) > 0) + (int32_t(q.y) > 0) + (int32_t(q.z) > 0) + (int32_t(q.w) > 0);
+      else
+        t += q.x + q.y + q.z + q.w;
     }
-
-    uint32_t carry = 0;
-    uint32_t pos[PVEC];
-    if (!COMPACT) {
-#pragma unroll
-      for (int j = 0; j < PVEC; ++j) {
-        x[j][1] += x[j][0];
-        x[j][2] += x[j][1];
-        x[j][3] += x[j][2];
-        const uint32_t t = x[j][3];
-        uint32_t v = t;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const uint32_t y = __shfl_up_sync(kFull, v, d);
-          if (lane >= uint32_t(d)) v += y;
-        }
-        const uint32_t add = carry + v - t;
-        carry += __shfl_sync(kFull, v, 31);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) x[j][k] += add;
-      }
-    } else {
-      const uint32_t lt = lanemask_lt();
-#pragma unroll
-      for (int j = 0; j < PVEC; ++j) {
-        uint32_t excl = 0, tot = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const bool f = int32_t(x[j][k]) > 0;  // padding of a ragged tile is 0
-          const uint32_t b = __ballot_sync(kFull, f);
-          excl += __popc(b & lt);
-          tot += __popc(b);
-          if (!f) x[j][k] = 0u;
-        }
-        pos[j] = carry + excl;
-        carry += tot;
-      }
-    }
-    if (lane == 0) sh.wtot[warp] = carry;
-    __syncthreads();  // also: every thread has its items in registers
+    t = __reduce_add_sync(kFull, t);
+    if (lane == 0) sh.wtot[warp] = t;
+    __syncthreads();
     uint32_t wexcl = 0, agg = 0;
 #pragma unroll
     for (int w = 0; w < PNW; ++w) {
       const uint32_t v = sh.wtot[w];
       wexcl += uint32_t(w) < warp ? v : 0u;
       agg += v;
-    }
-    if (COMPACT) {  // in-place tile-local compaction (items are in registers)
-#pragma unroll
-      for (int j = 0; j < PVEC; ++j) {
-        uint32_t p = wexcl + pos[j];
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (x[j][k] != 0u) buf[p++] = int32_t(x[j][k]);
-      }
     }
     // decoupled look-back (warp 0)
     if (warp == 0) {
@@ -378,21 +392,36 @@ __global__ void __launch_bounds__(PBLOCK)
         excl = (!COMPACT && carry_in != nullptr) ? uint32_t(*carry_in) : 0u;
         if (lane == 0) st_relaxed_gpu(desc, pack_desc(epoch, kStPrefix, excl + agg));
       } else {
-        if (lane == 0) st_relaxed_gpu(desc + tile, pack_desc(epoch, kStAggregate, agg));
-        excl = lookback_exclusive_wide<8>(desc, tile, epoch);
-        if (lane == 0) st_relaxed_gpu(desc + tile, pack_desc(epoch, kStPrefix, excl + agg));
+        if (lane == 0)
+          st_relaxed_gpu(desc + uint64_t(tile) * kDescStride, pack_desc(epoch, kStAggregate, agg));
+        excl = lookback_exclusive_wide<COMPACT ? WF_LBK_COMPACT : WF_LBK>(desc, tile, epoch);
+        if (lane == 0)
+          st_relaxed_gpu(desc + uint64_t(tile) * kDescStride, pack_desc(epoch, kStPrefix, excl + agg));
       }
       if (lane == 0) sh.prefix = excl;
     }
     __syncthreads();
     const uint32_t prefix = sh.prefix;
+    WF_STAMP(tile, 2);
 
+    // pass B: chunk-serial scan with the running warp carry
+    uint32_t carry = prefix + wexcl;
     if (!COMPACT) {
-      const uint32_t add = prefix + wexcl;
-#pragma unroll
+#pragma unroll 4
       for (int j = 0; j < PVEC; ++j) {
-        uint4 q;
-        q.x = x[j][0] + add; q.y = x[j][1] + add; q.z = x[j][2] + add; q.w = x[j][3] + add;
+        uint4 q = *reinterpret_cast<const uint4 *>(buf + off0 + j * 128);
+        q.y += q.x;
+        q.z += q.y;
+        q.w += q.z;
+        uint32_t v = q.w;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, v, d);
+          if (lane >= uint32_t(d)) v += y;
+        }
+        const uint32_t add = carry + v - q.w;
+        carry += __shfl_sync(kFull, v, 31);
+        q.x += add; q.y += add; q.z += add; q.w += add;
         *reinterpret_cast<uint4 *>(buf + off0 + j * 128) = q;
       }
       if (full) {
@@ -407,18 +436,36 @@ __global__ void __launch_bounds__(PBLOCK)
         for (uint32_t i = threadIdx.x; i < PTILE && base + i < n; i += PBLOCK) out[base + i] = buf[i];
       }
     } else {
-      int32_t *dst = out + prefix;
-      for (uint32_t i = threadIdx.x; i < agg; i += PBLOCK) dst[i] = buf[i];
+      // ballot + popc positions; each chunk's selected items land contiguously
+#pragma unroll 2
+      for (int j = 0; j < PVEC; ++j) {
+        const uint4 q = *reinterpret_cast<const uint4 *>(buf + off0 + j * 128);
+        const uint32_t v[4] = {q.x, q.y, q.z, q.w};
+        uint32_t b[4], excl = 0, tot = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          b[k] = __ballot_sync(kFull, int32_t(v[k]) > 0);
+          excl += __popc(b[k] & lt);
+          tot += __popc(b[k]);
+        }
+        uint32_t p = carry + excl;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (int32_t(v[k]) > 0) out[p++] = int32_t(v[k]);
+        carry += tot;
+      }
       if (tile == ntiles - 1 && threadIdx.x == 0) *count = uint64_t(prefix) + agg;
     }
+    WF_STAMP(tile, 3);
     __syncthreads();  // stage s fully consumed by the threads
     if (threadIdx.x == 0) {  // refill stage s with the next tile
-      const uint32_t t = drained ? kNoTile : draw_ticket(hdr, ntiles, epoch, drained);
-      sh.tile[s] = t;
-      if (!COMPACT && t != kNoTile) bulk_wait_read_all();  // bulk store has left stage s
-      if (t != kNoTile && uint64_t(t + 1) * PTILE <= n) {
+      const uint32_t tn = drained ? kNoTile : draw_ticket(hdr, ntiles, epoch, drained);
+      if (tn != kNoTile) WF_STAMP(tn, 0);
+      sh.tile[s] = tn;
+      if (!COMPACT && tn != kNoTile) bulk_wait_read_all();  // bulk store has left stage s
+      if (tn != kNoTile && uint64_t(tn + 1) * PTILE <= n) {
         mbar_arrive_expect_tx(&sh.full[s], PTILE * 4);
-        tma_load_1d(buf, in + uint64_t(t) * PTILE, PTILE * 4, &sh.full[s]);
+        tma_load_1d(buf, in + uint64_t(tn) * PTILE, PTILE * 4, &sh.full[s]);
       }
     }
     __syncthreads();
@@ -453,6 +500,13 @@ bool persistent_enabled() {
 }
 
 }  // namespace
+
+#if WF_TRACE
+extern "C" int wf_debug_set_trace(void *buf) {
+  unsigned long long *p = static_cast<unsigned long long *>(buf);
+  return int(cudaMemcpyToSymbol(g_wf_trace, &p, sizeof(p)));
+}
+#endif
 
 cudaError_t launch_scan_i32(const int32_t *in, int32_t *out, uint64_t n,
                             const int32_t *carry, void *ws, cudaStream_t s) {

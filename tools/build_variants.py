@@ -1,0 +1,28 @@
+"""Build experimental variants of the library into build/variants/ (travels to
+the GPU box; gitignored).  Usage: python tools/build_variants.py name="-DA=1 -DB=2" ..."""
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+from paper_2112_10034_b200 import build  # noqa: E402
+
+out_dir = ROOT / "build" / "variants"
+out_dir.mkdir(parents=True, exist_ok=True)
+for old in out_dir.glob("*.so"):
+    old.unlink()
+
+
+def one(spec):
+    name, flags = spec.split("=", 1)
+    cmd = [build.nvcc_path(), *build.NVCC_FLAGS, f"-I{build.INCLUDE}", *flags.split(),
+           "-o", str(out_dir / f"lib_{name}.so"), *map(str, build.sources())]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    return name, r.returncode, r.stderr[-500:]
+
+
+with ThreadPoolExecutor(8) as ex:
+    for name, rc, err in ex.map(one, sys.argv[1:]):
+        print(name, "OK" if rc == 0 else f"FAILED\n{err}")
