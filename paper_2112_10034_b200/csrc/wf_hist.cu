@@ -91,13 +91,9 @@ __global__ void __launch_bounds__(BLOCK, 2)
   }
   __shared__ bool am_last;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    am_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-  }
+  if (threadIdx.x == 0) am_last = atom_add_acq_rel_gpu(ticket, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!am_last) return;
-  __threadfence();
   if (threadIdx.x < 256) {
     const unsigned long long v = atomicExch(accum + threadIdx.x, 0ull);
     bins[threadIdx.x] = accumulate ? bins[threadIdx.x] + v : v;

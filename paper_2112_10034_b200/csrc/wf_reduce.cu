@@ -11,8 +11,10 @@
 //   2. the chains fold in a fixed pairwise order, then the warp folds with
 //      REDUX.SUM (i32) or a SHFL.BFLY butterfly (f32; REDUX has no f32 add);
 //   3. warp sums fold through shared memory inside the block;
-//   4. block partials go to the workspace; the last block to finish (atomic
-//      ticket) folds them in block-index order and resets the ticket.
+//   4. i32: one RED.ADD per block into a workspace accumulator; the block
+//      that draws the last acq_rel ticket publishes it and resets both.
+//      f32: block partials go to the workspace and the last block folds
+//      them in block-index order (no fp atomics -> reproducible bits).
 //
 // The element->thread assignment depends only on (n, block, grid), so the f32
 // result is bitwise reproducible run to run.  Roofline: HBM read, 4 B/elem.
@@ -25,6 +27,8 @@ namespace {
 struct SumI32 {
   using elem_t = int32_t;
   using acc_t = uint32_t;
+  static constexpr bool kOrderFree = true;
+  __device__ static uint32_t bits(acc_t v) { return v; }
   __device__ static acc_t zero() { return 0u; }
   __device__ static acc_t add(acc_t a, acc_t b) { return a + b; }
   __device__ static acc_t from_bits(uint32_t b) { return b; }
@@ -38,6 +42,8 @@ struct SumI32 {
 struct SumF32 {
   using elem_t = float;
   using acc_t = float;
+  static constexpr bool kOrderFree = false;  // fp: fixed-order fold for determinism
+  __device__ static uint32_t bits(acc_t v) { return __float_as_uint(v); }
   __device__ static acc_t zero() { return 0.0f; }
   __device__ static acc_t add(acc_t a, acc_t b) { return __fadd_rn(a, b); }
   __device__ static acc_t from_bits(uint32_t b) { return __uint_as_float(b); }
@@ -132,15 +138,26 @@ __global__ void __launch_bounds__(BLOCK)
 
   const acc_t bsum = block_sum<Op, BLOCK>(acc[0][0]);
 
+  if (Op::kOrderFree) {
+    // integer Σ is order-independent: one RED per block into the workspace
+    // accumulator, the last block (acq_rel ticket) publishes and resets it
+    if (threadIdx.x == 0) {
+      uint32_t *accum = reinterpret_cast<uint32_t *>(ticket) + 1;
+      red_add_relaxed_gpu(accum, Op::bits(bsum));
+      if (atom_add_acq_rel_gpu(ticket, 1u) == gridDim.x - 1) {
+        out[0] = Op::to_elem(Op::from_bits(atomicExch(accum, 0u)));
+        *ticket = 0u;
+      }
+    }
+    return;
+  }
   __shared__ bool am_last;
   if (threadIdx.x == 0) {
     partials[blockIdx.x] = bsum;
-    __threadfence();
-    am_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    am_last = atom_add_acq_rel_gpu(ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (!am_last) return;
-  __threadfence();
   // fixed-order fold of the block partials (thread t: t, t+BLOCK, ...)
   acc_t f = Op::zero();
   for (uint32_t j = threadIdx.x; j < gridDim.x; j += BLOCK) {

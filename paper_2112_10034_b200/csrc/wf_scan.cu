@@ -301,7 +301,7 @@ struct PersistShared {
 
 __device__ __forceinline__ uint32_t draw_ticket(TileHeader *hdr, uint32_t ntiles,
                                                 uint32_t epoch, bool &drained) {
-  const uint32_t t = atomicAdd(&hdr->ticket, 1u);
+  const uint32_t t = atom_add_acq_rel_gpu(&hdr->ticket, 1u);
   if (t >= ntiles) {
     drained = true;
     if (t == ntiles + gridDim.x - 1) {  // last of all draws
@@ -330,8 +330,7 @@ __global__ void __launch_bounds__(PBLOCK)
   if (threadIdx.x == 0) {
     for (int s = 0; s < PSTAGES; ++s) mbar_init(&sh.full[s], 1);
     fence_barrier_init();
-    sh.epoch = ld_volatile_u32(&hdr->epoch) & kEpochMask;
-    __threadfence();
+    sh.epoch = ld_volatile_u32(&hdr->epoch) & kEpochMask;  // ordered by the release draw
     for (int s = 0; s < PSTAGES; ++s) {
       const uint32_t t = drained ? kNoTile : draw_ticket(hdr, ntiles, sh.epoch, drained);
       if (t != kNoTile) WF_STAMP(t, 0);

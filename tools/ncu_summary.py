@@ -16,6 +16,7 @@ NAMES = {"reduce_kernel<wf::<unnamed>::SumI32": "reduce_sum_i32",
          "tile_persistent_kernel<(bool)0>": "scan_inclusive_i32",
          "tile_persistent_kernel<(bool)1>": "compact_gt0_i32",
          "tile_persistent_kernel<true>": "compact_gt0_i32",
+         "tile_persistent_kernel<0>": "scan_inclusive_i32", "tile_persistent_kernel<1>": "compact_gt0_i32",
          "compact_gt0_kernel": "compact_gt0_i32", "hist256_kernel": "histogram256_u8"}
 
 
