@@ -183,6 +183,19 @@ int wf_histogram256_u8_host(const uint8_t *host_in, uint64_t n,
                             size_t staging_bytes, void *ws, size_t ws_bytes,
                             wf_stream_t stream);
 
+/* ---- DSL kernels compiled natively (replaces hybrid_transform + run_mpmd)
+ * passes/pipeline.py:103-179 / interp/mpmd.py:237-255: the Python front end
+ * (paper_2112_10034_b200/dsl) emits CUDA C with the reference's scalar and
+ * collective semantics; these entry points compile it with NVRTC for sm_100a
+ * (--fmad=false: one rounding per f32 op), load the cubin and
+ * launch it.  `options` = extra space-separated NVRTC options (may be NULL);
+ * the compile log (or error) is copied into `log`. */
+int wf_jit_compile(const char *src, const char *kernel_name, const char *options,
+                   void **module, char *log, size_t log_bytes);
+int wf_jit_launch(void *module, uint32_t grid, uint32_t block, uint32_t smem_bytes,
+                  void **args, wf_stream_t stream);
+int wf_jit_unload(void *module);
+
 #ifdef __cplusplus
 }
 #endif

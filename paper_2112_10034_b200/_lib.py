@@ -61,6 +61,10 @@ SIGNATURES = {
     "wf_reduce_sum_f32_host": (C.c_int, [_vp, _u64, _vp, _vp, _sz, _vp, _sz, _vp]),
     "wf_reduce_sum_i32_host": (C.c_int, [_vp, _u64, _vp, _vp, _sz, _vp, _sz, _vp]),
     "wf_histogram256_u8_host": (C.c_int, [_vp, _u64, _vp, _vp, _sz, _vp, _sz, _vp]),
+    "wf_jit_compile": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p),
+                                 C.c_char_p, _sz]),
+    "wf_jit_launch": (C.c_int, [_vp, _u32, _u32, _u32, C.POINTER(C.c_void_p), _vp]),
+    "wf_jit_unload": (C.c_int, [_vp]),
 }
 
 _lock = threading.Lock()

@@ -25,6 +25,7 @@ NVCC_FLAGS = ARCH_FLAGS + [
     "-O3", "-lineinfo", "-std=c++17", "--fmad=false",
     "-Xcompiler", "-fPIC,-O3", "-shared", "-cudart", "static",
 ]
+LINK_FLAGS = ["-ldl"]
 
 
 def nvcc_path() -> str:
@@ -54,7 +55,8 @@ def build_library(force: bool = False, verbose: bool = False, out: Path = LIB_PA
     if not force and up_to_date(out):
         return out
     tmp = out.with_suffix(".so.tmp")
-    cmd = [nvcc_path(), *NVCC_FLAGS, f"-I{INCLUDE}", "-o", str(tmp), *map(str, sources())]
+    cmd = [nvcc_path(), *NVCC_FLAGS, f"-I{INCLUDE}", "-o", str(tmp), *map(str, sources()),
+           *LINK_FLAGS]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

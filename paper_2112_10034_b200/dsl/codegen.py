@@ -1,0 +1,330 @@
+"""DSL kernel -> CUDA C for sm_100a, with the reference's semantics.
+
+Replaces the collapsing pipeline (passes/pipeline.py:103-179) and the MPMD
+interpreter (interp/mpmd.py:237-255): the GPU runs the kernel as real SIMT
+code, so instead of wrapping regions in lane/warp loops the generator only has
+to make every scalar operation mean exactly what it means in the reference:
+
+* i32 wraps mod 2^32 (numerics.py:20-22) -> unsigned arithmetic helpers;
+  ``/`` and ``%`` truncate and fault on zero (numerics.py:25-37), including
+  INT_MIN / -1 = INT_MIN.
+* f32 is IEEE single, one rounding per op, no contraction ->
+  ``__fadd_rn``/``__fmul_rn``/``__fdiv_rn`` and NVRTC ``--fmad=false``;
+  i32 operands widen with round-to-nearest (np.float32(int)).
+* ``&&``/``||`` evaluate both operands (interp/evalexpr.py:36-40), results
+  are i32 0/1.
+* Locals live in one flat per-kernel namespace and read as zero until
+  assigned (interp/oracle.py:45-46): all are hoisted to the kernel top and
+  zero-initialised; a declaration with an initializer becomes an assignment.
+* Shared arrays are zero-filled per block (interp/oracle.py:214-216).
+* Every global/shared access is bounds-checked; a violation records the
+  reference's message ("out-of-bounds read a[100], length 32",
+  interp/oracle.py:65-81) in a device error record, the access reads 0 / is
+  dropped, and the host raises ExecutionError after the launch.
+* Collectives follow passes/warp_lower.py:17-45 / interp/oracle.py:147-161:
+  ``shfl_down`` hands out-of-range lanes their own value for ANY offset (one
+  SHFL.IDX with an explicitly computed source lane, not the 5-bit-masked
+  SHFL.DOWN), votes return 0/1.  The reference's warp of W lanes is a
+  W-lane segment of the hardware warp (W = LaunchConfig.warp_size).
+"""
+
+from __future__ import annotations
+
+import struct
+
+import numpy as np
+
+from ..errors import TransformError
+from . import nodes as n
+from .checker import SymbolTable, expr_kind
+
+I32, F32 = n.I32, n.F32
+CTYPE = {I32: "int", F32: "float"}
+
+PRELUDE = r"""
+#define WF_INT_MIN (-2147483647 - 1)
+struct wf_err_t { unsigned long long code; long long arg; long long index; long long length; };
+__device__ __noinline__ void wf_fail(wf_err_t *e, unsigned long long code, long long arg,
+                                     long long idx, long long len) {
+  if (atomicCAS(&e->code, 0ull, code) == 0ull) { e->arg = arg; e->index = idx; e->length = len; }
+}
+__device__ __forceinline__ int wf_add(int a, int b) { return (int)((unsigned)a + (unsigned)b); }
+__device__ __forceinline__ int wf_sub(int a, int b) { return (int)((unsigned)a - (unsigned)b); }
+__device__ __forceinline__ int wf_mul(int a, int b) { return (int)((unsigned)a * (unsigned)b); }
+__device__ __forceinline__ int wf_neg(int a) { return (int)(0u - (unsigned)a); }
+__device__ __forceinline__ int wf_div(int a, int b, wf_err_t *e) {
+  if (b == 0) { wf_fail(e, 3, -1, 0, 0); return 0; }
+  if (a == WF_INT_MIN && b == -1) return WF_INT_MIN;
+  return a / b;
+}
+__device__ __forceinline__ int wf_rem(int a, int b, wf_err_t *e) {
+  if (b == 0) { wf_fail(e, 4, -1, 0, 0); return 0; }
+  if (b == -1) return 0;
+  return a % b;
+}
+__device__ __forceinline__ float wf_f(int a) { return __int2float_rn(a); }
+__device__ __forceinline__ float wf_f(float a) { return a; }
+__device__ __forceinline__ int wf_land(int a, int b) { return (a != 0 && b != 0) ? 1 : 0; }
+__device__ __forceinline__ int wf_lor(int a, int b) { return (a != 0 || b != 0) ? 1 : 0; }
+template <typename T>
+__device__ __forceinline__ T wf_ld(const T *p, long long len, long long i, long long arg, wf_err_t *e) {
+  if (i < 0 || i >= len) { wf_fail(e, 1, arg, i, len); return (T)0; }
+  return p[i];
+}
+template <typename T>
+__device__ __forceinline__ void wf_st(T *p, long long len, long long i, T v, long long arg, wf_err_t *e) {
+  if (i < 0 || i >= len) { wf_fail(e, 2, arg, i, len); return; }
+  p[i] = v;
+}
+// ---- warp collectives over W-lane segments of the hardware warp ----------
+__device__ __forceinline__ unsigned wf_present() {
+  const unsigned k = blockDim.x - (threadIdx.x & ~31u);
+  return k >= 32u ? 0xffffffffu : ((1u << k) - 1u);
+}
+__device__ __forceinline__ unsigned wf_seg() { return (threadIdx.x & 31u) & ~(WF_W - 1u); }
+__device__ __forceinline__ unsigned wf_segbits() {
+  return WF_W == 32 ? 0xffffffffu : (((1u << WF_W) - 1u) << wf_seg());
+}
+template <typename T>
+__device__ __forceinline__ T wf_shfl_from(T v, long long src_in_seg, unsigned mask) {
+  const unsigned lane = threadIdx.x & 31u;
+  unsigned src = lane;
+  if (src_in_seg >= 0 && src_in_seg < WF_W) {
+    const unsigned s = wf_seg() + (unsigned)src_in_seg;
+    if ((mask >> s) & 1u) src = s;
+  }
+  return __shfl_sync(mask, v, src);
+}
+__device__ __forceinline__ long long wf_lane_in_seg() { return (long long)((threadIdx.x & 31u) - wf_seg()); }
+template <typename T> __device__ __forceinline__ T wf_shfl_down(T v, int off, unsigned m) {
+  return wf_shfl_from(v, wf_lane_in_seg() + off, m); }
+template <typename T> __device__ __forceinline__ T wf_shfl_up(T v, int off, unsigned m) {
+  return wf_shfl_from(v, wf_lane_in_seg() - off, m); }
+template <typename T> __device__ __forceinline__ T wf_shfl_xor(T v, int x, unsigned m) {
+  return wf_shfl_from(v, (long long)((unsigned)wf_lane_in_seg() ^ (unsigned)x), m); }
+template <typename T> __device__ __forceinline__ T wf_shfl_idx(T v, int s, unsigned m) {
+  long long r = (long long)s % WF_W; if (r < 0) r += WF_W; return wf_shfl_from(v, r, m); }
+__device__ __forceinline__ int wf_vote_all(int p, unsigned m) {
+  const unsigned part = m & wf_segbits();
+  return (__ballot_sync(m, p != 0) & part) == part ? 1 : 0; }
+__device__ __forceinline__ int wf_vote_any(int p, unsigned m) {
+  return (__ballot_sync(m, p != 0) & m & wf_segbits()) != 0u ? 1 : 0; }
+__device__ __forceinline__ int wf_ballot(int p, unsigned m) {
+  return (int)((__ballot_sync(m, p != 0) & m & wf_segbits()) >> wf_seg()); }
+__device__ __forceinline__ int wf_reduce_add(int v, unsigned m) {
+  if (WF_W == 32) return (int)__reduce_add_sync(m, (unsigned)v);
+  unsigned acc = 0;
+  for (unsigned j = 0; j < WF_W; ++j) {
+    const unsigned s = wf_seg() + j;
+    const bool ok = (m >> s) & 1u;
+    const unsigned t = __shfl_sync(m, (unsigned)v, ok ? s : (threadIdx.x & 31u));
+    acc += ok ? t : 0u;
+  }
+  return (int)acc;
+}
+"""
+
+ERR_MESSAGES = {1: "read", 2: "write"}
+
+
+def _f32_literal(v: float) -> str:
+    bits = struct.unpack("<I", struct.pack("<f", float(np.float32(v))))[0]
+    return f"__int_as_float(0x{bits:08x})"
+
+
+def _i32_literal(v: int) -> str:
+    v &= 0xFFFFFFFF
+    return f"((int)0x{v:08x}u)"
+
+
+class CudaGen:
+    def __init__(self, kernel: n.KernelDef, table: SymbolTable, warp_size: int,
+                 block_size: int | None = None, grid_size: int | None = None):
+        self.k, self.t, self.W = kernel, table, warp_size
+        self.block_size, self.grid_size = block_size, grid_size  # specialize (JIT mode)
+        self.lines: list[str] = []
+        self.arrays: list[str] = []  # error-record arg index -> array name
+        for p in kernel.params:
+            if p.is_buffer:
+                self.arrays.append(p.name)
+        for name in table.shared:
+            self.arrays.append(name)
+
+    # -- names
+    def arr_ptr(self, name: str) -> str:
+        return f"p_{name}" if name in self.t.params else f"s_{name}"
+
+    def arr_len(self, name: str) -> str:
+        if name in self.t.params:
+            return f"p_{name}_len"
+        length = self.t.shared[name][1]
+        return "wf_dyn_len" if length is None else f"{length}LL"
+
+    def arr_id(self, name: str) -> int:
+        return self.arrays.index(name)
+
+    def var(self, name: str) -> str:
+        return f"p_{name}" if name in self.t.params else f"v_{name}"
+
+    # -- expressions -> (code, kind)
+    def expr(self, e) -> tuple[str, str]:
+        if isinstance(e, n.IntLit):
+            return _i32_literal(e.value), I32
+        if isinstance(e, n.FloatLit):
+            return _f32_literal(e.value), F32
+        if isinstance(e, n.VarRef):
+            return self.var(e.name), expr_kind(e, self.t)
+        if isinstance(e, n.BuiltinRef):
+            if e.name == "blockDim.x" and self.block_size:
+                return f"{self.block_size}", I32
+            if e.name == "gridDim.x" and self.grid_size:
+                return f"{self.grid_size}", I32
+            return f"((int){e.name})", I32
+        if isinstance(e, n.IndexExpr):
+            idx, _ = self.expr(e.index)
+            kind = self.t.element_kind(e.base)
+            return (f"wf_ld<{CTYPE[kind]}>({self.arr_ptr(e.base)}, {self.arr_len(e.base)}, "
+                    f"(long long)({idx}), {self.arr_id(e.base)}, wf_e)"), kind
+        if isinstance(e, n.Unary):
+            c, k = self.expr(e.operand)
+            if e.op == "!":
+                return f"(({c}) == 0 ? 1 : 0)", I32
+            return (f"(-({c}))", F32) if k == F32 else (f"wf_neg({c})", I32)
+        if isinstance(e, n.Binary):
+            return self.binary(e)
+        if isinstance(e, n.CollectiveCall):
+            return self.collective(e)
+        raise TransformError(f"cannot generate {type(e).__name__}")
+
+    def binary(self, e: n.Binary) -> tuple[str, str]:
+        a, ak = self.expr(e.left)
+        b, bk = self.expr(e.right)
+        if e.op == "&&":
+            return f"wf_land({a}, {b})", I32
+        if e.op == "||":
+            return f"wf_lor({a}, {b})", I32
+        f32 = F32 in (ak, bk)
+        if e.op in ("==", "!=", "<", "<=", ">", ">="):
+            if f32:
+                a, b = f"wf_f({a})", f"wf_f({b})"
+            return f"(({a}) {e.op} ({b}) ? 1 : 0)", I32
+        if f32:
+            fn = {"+": "__fadd_rn", "-": "__fsub_rn", "*": "__fmul_rn", "/": "__fdiv_rn"}[e.op]
+            return f"{fn}(wf_f({a}), wf_f({b}))", F32
+        if e.op in ("/", "%"):
+            return f"{'wf_div' if e.op == '/' else 'wf_rem'}({a}, {b}, wf_e)", I32
+        fn = {"+": "wf_add", "-": "wf_sub", "*": "wf_mul"}[e.op]
+        return f"{fn}({a}, {b})", I32
+
+    def mask(self, e) -> str:
+        if e is None:
+            return "wf_present()"
+        m, _ = self.expr(e)
+        return f"((unsigned)({m}) & wf_present())"
+
+    def collective(self, e: n.CollectiveCall) -> tuple[str, str]:
+        m = self.mask(e.mask)
+        if e.op in ("shfl_down", "shfl_up", "shfl_xor", "shfl_idx"):
+            v, vk = self.expr(e.args[0])
+            o, _ = self.expr(e.args[1])
+            return f"wf_{e.op}<{CTYPE[vk]}>({v}, {o}, {m})", vk
+        a, _ = self.expr(e.args[0])
+        return f"wf_{e.op}({a}, {m})", I32
+
+    def convert(self, code: str, src: str, dst: str) -> str:
+        return f"wf_f({code})" if (dst == F32 and src == I32) else code
+
+    # -- statements
+    def emit(self, line: str, depth: int):
+        self.lines.append("  " * depth + line)
+
+    def assign(self, s: n.Assign, depth: int, as_expr: bool = False) -> str:
+        val, vk = self.expr(s.expr)
+        tg = s.target
+        if isinstance(tg, n.VarTarget):
+            code = f"{self.var(tg.name)} = {self.convert(val, vk, self.t.locals[tg.name])}"
+        else:
+            kind = self.t.element_kind(tg.base)
+            idx, _ = self.expr(tg.index)
+            code = (f"wf_st<{CTYPE[kind]}>({self.arr_ptr(tg.base)}, {self.arr_len(tg.base)}, "
+                    f"(long long)({idx}), {self.convert(val, vk, kind)}, {self.arr_id(tg.base)}, wf_e)")
+        if as_expr:
+            return code
+        self.emit(code + ";", depth)
+        return code
+
+    def stmts(self, body, depth: int):
+        for s in body:
+            self.stmt(s, depth)
+
+    def stmt(self, s, depth: int):
+        if isinstance(s, n.DeclLocal):
+            if s.init is not None:
+                v, vk = self.expr(s.init)
+                self.emit(f"v_{s.name} = {self.convert(v, vk, s.kind)};", depth)
+        elif isinstance(s, n.DeclShared):
+            pass  # hoisted
+        elif isinstance(s, n.Assign):
+            self.assign(s, depth)
+        elif isinstance(s, n.If):
+            c, _ = self.expr(s.cond)
+            self.emit(f"if (({c}) != 0) {{", depth)
+            self.stmts(s.then, depth + 1)
+            if s.orelse is not None:
+                self.emit("} else {", depth)
+                self.stmts(s.orelse, depth + 1)
+            self.emit("}", depth)
+        elif isinstance(s, n.For):
+            if isinstance(s.init, n.DeclLocal):
+                v, vk = self.expr(s.init.init)
+                init = f"v_{s.init.name} = {self.convert(v, vk, s.init.kind)}"
+            else:
+                init = self.assign(s.init, depth, as_expr=True)
+            c, _ = self.expr(s.cond)
+            step = self.assign(s.step, depth, as_expr=True)
+            self.emit(f"for ({init}; ({c}) != 0; {step}) {{", depth)
+            self.stmts(s.body, depth + 1)
+            self.emit("}", depth)
+        elif isinstance(s, n.SyncThreads):
+            self.emit("__syncthreads();", depth)
+        elif isinstance(s, n.SyncWarp):
+            self.emit(f"__syncwarp({self.mask(s.mask)});", depth)
+        elif isinstance(s, n.Return):
+            self.emit("return;", depth)
+        else:
+            raise TransformError(f"cannot generate {type(s).__name__}")
+
+    def generate(self) -> str:
+        params = []
+        for p in self.k.params:
+            if p.is_buffer:
+                params.append(f"{CTYPE[p.kind]} *__restrict__ p_{p.name}")
+                params.append(f"long long p_{p.name}_len")
+            else:
+                params.append(f"{CTYPE[p.kind]} p_{p.name}")
+        params += ["wf_err_t *__restrict__ wf_e", "long long wf_dyn_len"]
+        out = [f"#define WF_W {self.W}u", PRELUDE,
+               f'extern "C" __global__ void __launch_bounds__(1024) wf_kernel({", ".join(params)}) {{']
+        for name, (kind, length) in self.t.shared.items():
+            if length is None:
+                out.append(f"  extern __shared__ {CTYPE[kind]} s_{name}[];")
+            else:
+                out.append(f"  __shared__ {CTYPE[kind]} s_{name}[{length}];")
+        for name, (kind, length) in self.t.shared.items():
+            ln = "wf_dyn_len" if length is None else f"{length}LL"
+            out.append(f"  for (long long i = threadIdx.x; i < {ln}; i += blockDim.x) "
+                       f"s_{name}[i] = ({CTYPE[kind]})0;")
+        if self.t.shared:
+            out.append("  __syncthreads();")
+        for name, kind in self.t.locals.items():
+            out.append(f"  {CTYPE[kind]} v_{name} = ({CTYPE[kind]})0;")
+        self.stmts(self.k.body, 1)
+        out += self.lines
+        out.append("}")
+        return "\n".join(out) + "\n"
+
+
+def generate(kernel: n.KernelDef, table: SymbolTable, warp_size: int = 32,
+             block_size: int | None = None, grid_size: int | None = None) -> tuple[str, list]:
+    g = CudaGen(kernel, table, warp_size, block_size, grid_size)
+    return g.generate(), g.arrays

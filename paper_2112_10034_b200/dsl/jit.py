@@ -1,0 +1,158 @@
+"""``hybrid_transform`` for the GPU: DSL kernel -> native sm_100a program.
+
+Reference: ``hybrid_transform(kernel, config, mode, options, want_snapshots)
+-> MpmdProgram`` (passes/pipeline.py:103-179).  Same signature, same mode
+resolution (``resolve_mode``, pipeline.py:92-100) and the same ConfigError /
+UnsupportedFeatureError cases; the returned ``JitProgram`` is launched by
+``paper_2112_10034_b200.launch`` exactly like an MpmdProgram is launched by
+the reference's ``launch``.  Code generation is pure Python (runs anywhere);
+NVRTC compilation and loading happen in the native library on first launch
+and are cached per (source, warp size, specialisation).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .. import _lib
+from ..config import LaunchConfig
+from ..errors import ExecutionError, TransformError, UnsupportedFeatureError
+from . import nodes as n
+from .checker import SymbolTable, check_kernel
+from .codegen import generate
+
+_cache_lock = threading.Lock()
+_module_cache: dict = {}
+
+
+def resolve_mode(kernel: n.KernelDef, mode: str) -> str:
+    """passes/pipeline.py:92-100."""
+    warp = n.uses_warp_features(kernel)
+    if mode == "auto":
+        return "hier" if warp else "flat"
+    if mode == "flat" and warp:
+        raise UnsupportedFeatureError(
+            f"kernel {kernel.name!r} uses warp-level features (shuffle/vote/syncwarp); "
+            f"flat translation cannot express them, use --mode hier or auto")
+    return mode
+
+
+@dataclass
+class TransformOptions:
+    """Accepted for signature compatibility (passes/pipeline.py:35-44).  The
+    mutation knobs remove lane-buffer barriers in the CPU emulation; native
+    SIMT has no such barriers, so they have no effect here."""
+    check: bool = True
+    insert_raw: bool = True
+    insert_war: bool = True
+    insert_if_extras: bool = True
+
+
+@dataclass(eq=False)
+class JitProgram:
+    name: str
+    params: list
+    kernel: n.KernelDef
+    table: SymbolTable
+    mode: str
+    warp_size: int
+    specialized: dict | None = None
+    source: str = ""
+    arrays: list = field(default_factory=list)
+
+    def cuda_source(self, config: LaunchConfig | None = None) -> str:
+        spec = self.specialized or {}
+        src, arrays = generate(self.kernel, self.table, self.warp_size,
+                               spec.get("block_size"), spec.get("grid_size"))
+        self.arrays = arrays
+        return src
+
+    def _module(self):
+        src = self.source or self.cuda_source()
+        self.source = src
+        with _cache_lock:
+            mod = _module_cache.get(src)
+            if mod is None:
+                lib = _lib.load()
+                handle = C.c_void_p()
+                log = C.create_string_buffer(1 << 16)
+                rc = lib.wf_jit_compile(src.encode(), b"wf_kernel", None, C.byref(handle),
+                                        log, len(log))
+                if rc != 0:
+                    raise TransformError(
+                        f"NVRTC compilation of kernel {self.name!r} failed ({rc}): "
+                        f"{log.value.decode(errors='replace')}")
+                mod = handle
+                _module_cache[src] = mod
+        return mod
+
+    def run(self, config: LaunchConfig, memory, bound: dict) -> None:
+        import torch
+        if self.specialized and (self.specialized["block_size"] != config.block_size or
+                                 self.specialized["grid_size"] != config.grid_size):
+            raise TransformError("program was specialized for a different launch configuration")
+        if config.warp_size != self.warp_size:
+            raise TransformError(f"program was generated for warp size {self.warp_size}")
+        mod = self._module()
+        keep, argv = [], []
+        for p in self.params:
+            if p.is_buffer:
+                t = bound[p.name]
+                keep += [C.c_void_p(t.data_ptr()), C.c_longlong(t.numel())]
+            elif p.kind == n.I32:
+                keep.append(C.c_int32(int(bound[p.name])))
+            else:
+                keep.append(C.c_float(float(np.float32(bound[p.name]))))
+        err = torch.zeros(4, dtype=torch.int64, device=memory.device)
+        dyn = [s for s, (_, ln) in self.table.shared.items() if ln is None]
+        elem = 4
+        dyn_len = config.shared_bytes // elem if dyn else 0
+        keep += [C.c_void_p(err.data_ptr()), C.c_longlong(dyn_len)]
+        argv = (C.c_void_p * len(keep))(*[C.cast(C.pointer(k), C.c_void_p) for k in keep])
+        stream = torch.cuda.current_stream(memory.device).cuda_stream
+        rc = _lib.load().wf_jit_launch(mod, config.grid_size, config.block_size,
+                                       config.shared_bytes, argv, stream)
+        _lib.check(rc, f"launch of {self.name}")
+        torch.cuda.current_stream(memory.device).synchronize()
+        code, arg, idx, length = (int(v) for v in err.cpu().tolist())
+        if code:
+            raise ExecutionError(self._message(code, arg, idx, length))
+
+    def _message(self, code, arg, idx, length) -> str:
+        if code in (1, 2):
+            name = self.arrays[arg] if 0 <= arg < len(self.arrays) else f"#{arg}"
+            what = "read" if code == 1 else "write"
+            return f"out-of-bounds {what} {name}[{idx}], length {length}"
+        if code == 3:
+            return "integer division by zero"
+        if code == 4:
+            return "integer remainder by zero"
+        return f"device fault {code}"
+
+
+def hybrid_transform(kernel: n.KernelDef, config: LaunchConfig, mode: str | None = None,
+                     options: TransformOptions | None = None,
+                     want_snapshots: tuple = ()) -> JitProgram:
+    mode = resolve_mode(kernel, mode or config.mode)
+    config.validate(hierarchical=(mode == "hier"))
+    table = check_kernel(kernel)
+    spec = None
+    if config.specialize:  # the paper's JIT mode: fold the launch geometry
+        spec = {"block_size": config.block_size, "grid_size": config.grid_size}
+    prog = JitProgram(kernel.name, list(kernel.params), kernel, table, mode,
+                      config.warp_size, spec)
+    prog.source = prog.cuda_source()
+    return prog
+
+
+def specialize(program: JitProgram, config: LaunchConfig) -> JitProgram:
+    """passes/pipeline.py:264-344: fold blockDim/gridDim into the program."""
+    prog = JitProgram(program.name, program.params, program.kernel, program.table,
+                      program.mode, program.warp_size,
+                      {"block_size": config.block_size, "grid_size": config.grid_size})
+    prog.source = prog.cuda_source()
+    return prog

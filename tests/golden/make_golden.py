@@ -169,7 +169,7 @@ def c3_pin() -> dict:
 def corpus_golden() -> tuple[dict, dict]:
     arrays, manifest = {}, {}
     for k in corpus.ALL:
-        for grid, block, warp in ((2, 64, 32), (3, 32, 32)):
+        for grid, block, warp in ((2, 64, 32), (3, 32, 32), (2, 8, 4), (1, 16, 8)):
             mem, args = k.build(grid, block, 0)
             kernel = k.kernel()
             ids = [a for p, a in zip(kernel.params, args) if p.is_buffer]

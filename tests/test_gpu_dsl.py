@@ -1,0 +1,175 @@
+"""DSL kernels compiled natively for sm_100a, bit-exact against the reference's
+own lockstep oracle (run_oracle outputs committed in tests/golden/corpus.npz)
+— the GPU analogue of the reference's acceptance criterion 1 and
+tests/test_diff_corpus.py:19-50 (incl. warp size 4/8)."""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+from oracle import semantics  # noqa: E402
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+MANIFEST = json.loads((GOLDEN / "corpus_manifest.json").read_text())
+
+
+@pytest.fixture(scope="module")
+def wf():
+    from paper_2112_10034_b200 import build
+    build.build_library()
+    import paper_2112_10034_b200 as wf
+    return wf
+
+
+@pytest.fixture(scope="module")
+def arrays():
+    return np.load(GOLDEN / "corpus.npz")
+
+
+def _run(wf, source, cfg, buffers, scalars=(), specialize=False):
+    from paper_2112_10034_b200.dsl import hybrid_transform, parse_module
+    kernel = parse_module(source).kernel()
+    mem = wf.DeviceMemory()
+    ids = []
+    for kind, init in buffers:
+        b = mem.alloc(4 * len(init))
+        mem.write(b, init, kind)
+        ids.append(b)
+    args, it, sc = [], iter(ids), iter(scalars)
+    for p in kernel.params:
+        args.append(next(it) if p.is_buffer else next(sc))
+    cfg.specialize = specialize
+    wf.launch(hybrid_transform(kernel, cfg), cfg, mem, args)
+    return [mem.host_view(b, kind) for (kind, _), b in zip(buffers, ids)]
+
+
+@pytest.mark.parametrize("tag", sorted(MANIFEST))
+@pytest.mark.parametrize("specialize", [False, True])
+def test_corpus_bit_exact_vs_reference_oracle(wf, arrays, tag, specialize):
+    m = MANIFEST[tag]
+    kinds = m["kinds"]
+    bufs = [(k, arrays[f"{tag}__in{i}"]) for i, k in enumerate(kinds)]
+    scalars = [a[1] for a in m["args"] if a[0] == "scalar"]
+    cfg = wf.LaunchConfig(grid_size=m["grid"], block_size=m["block"], warp_size=m["warp"])
+    outs = _run(wf, m["source"], cfg, bufs, scalars, specialize)
+    for i, (kind, got) in enumerate(zip(kinds, outs)):
+        want = arrays[f"{tag}__out{i}"]
+        assert np.array_equal(got.view(np.int32), want.view(np.int32)), (tag, i)
+
+
+def test_reference_kats(wf, golden):
+    kat = np.load(golden / "oracle_kat.npz")
+    src = """
+    __global__ void reduce_warp(global i32* a, global i32* out) {
+        i32 tid = threadIdx.x + blockIdx.x * blockDim.x;
+        i32 val = a[tid];
+        if (threadIdx.x < 32) {
+            for (i32 offset = 16; offset > 0; offset = offset / 2) {
+                val = val + shfl_down(val, offset);
+            }
+        }
+        if (threadIdx.x == 0) { out[blockIdx.x] = val; }
+        a[tid] = val;
+    }"""
+    a, out = _run(wf, src, wf.LaunchConfig(grid_size=1, block_size=64),
+                  [("i32", np.ones(64)), ("i32", np.zeros(1))])
+    assert np.array_equal(a, kat["kat_ones_a"]) and np.array_equal(out, kat["kat_ones_out"])
+    a, out = _run(wf, src, wf.LaunchConfig(grid_size=2, block_size=64),
+                  [("i32", kat["kat_general_in"]), ("i32", np.zeros(2))])
+    assert np.array_equal(out, kat["kat_general_out"]) and np.array_equal(a, kat["kat_general_a"])
+
+
+def test_out_of_bounds_reports_index_and_length(wf):
+    # reference tests/test_oracle.py:134-138
+    with pytest.raises(wf.ExecutionError, match=r"a\[100\], length 32"):
+        _run(wf, "__global__ void k(global i32* a) { a[threadIdx.x + 100] = 1; }",
+             wf.LaunchConfig(grid_size=1, block_size=32), [("i32", np.zeros(32))])
+    with pytest.raises(wf.ExecutionError, match=r"out-of-bounds read a\[-1\]"):
+        _run(wf, "__global__ void k(global i32* a) { a[0] = a[threadIdx.x - 1]; }",
+             wf.LaunchConfig(grid_size=1, block_size=32), [("i32", np.zeros(32))])
+
+
+def test_division_by_zero_faults(wf):
+    with pytest.raises(wf.ExecutionError, match="integer division by zero"):
+        _run(wf, "__global__ void k(global i32* a, i32 d) { a[threadIdx.x] = 7 / d; }",
+             wf.LaunchConfig(grid_size=1, block_size=32), [("i32", np.zeros(32))], [0])
+
+
+def test_scalar_semantics(wf):
+    # wrap, trunc division, INT_MIN / -1, uninitialised locals read zero,
+    # f32 single precision (reference tests/test_oracle.py:162-182)
+    src = """
+    __global__ void k(global i32* a, global f32* f) {
+        i32 t = threadIdx.x;
+        i32 z;
+        a[t] = 2147483647 + t;
+        a[t + 4] = (0 - 7 - t) / 2;
+        a[t + 8] = (0 - 7 - t) % 3;
+        a[12] = (0 - 2147483647 - 1) / (0 - 1);
+        a[13] = z + 5;
+        f[t] = f[t] + 0.1;
+    }"""
+    a, f = _run(wf, src, wf.LaunchConfig(grid_size=1, block_size=4),
+                [("i32", np.zeros(14)), ("f32", np.ones(4))])
+    assert list(a[:4]) == [2147483647, -2147483648, -2147483647, -2147483646]
+    assert list(a[4:8]) == [int(-(7 + t) / 2) for t in range(4)]
+    assert list(a[8:12]) == [-((7 + t) % 3) for t in range(4)]
+    assert a[12] == -2147483648 and a[13] == 5
+    assert all(v == np.float32(np.float32(1.0) + np.float32(0.1)) for v in f)
+
+
+def test_grid_zero_runs_nothing(wf):
+    (a,) = _run(wf, "__global__ void k(global i32* a) { a[threadIdx.x] = 1; }",
+                wf.LaunchConfig(grid_size=0, block_size=32), [("i32", np.zeros(32))])
+    assert list(a) == [0] * 32
+
+
+@pytest.mark.parametrize("block,width", [(32, 32), (64, 32), (48, 32), (100, 32), (64, 4),
+                                         (40, 8), (32, 16)])
+def test_extension_collectives_vs_semantics(wf, block, width):
+    rng = np.random.default_rng(block + width)
+    n_thr = block * 2
+    a = rng.integers(-3, 4, n_thr).astype(np.int32)
+    b = rng.integers(-40, 40, n_thr).astype(np.int32)
+    for op in ("shfl_down", "shfl_up", "shfl_xor", "shfl_idx"):
+        src = f"""__global__ void k(global i32* a, global i32* b, global i32* o) {{
+            i32 i = threadIdx.x + blockIdx.x * blockDim.x;
+            o[i] = {op}(a[i], b[i]); }}"""
+        _, _, o = _run(wf, src, wf.LaunchConfig(grid_size=2, block_size=block, warp_size=width),
+                       [("i32", a), ("i32", b), ("i32", np.zeros(n_thr))])
+        want = semantics.collective(op, a, b, 0, block, width, 0xFFFFFFFF)
+        assert np.array_equal(o, want), op
+    for op in ("vote_all", "vote_any", "ballot", "reduce_add"):
+        src = f"""__global__ void k(global i32* a, global i32* o) {{
+            i32 i = threadIdx.x + blockIdx.x * blockDim.x;
+            o[i] = {op}(a[i]); }}"""
+        _, o = _run(wf, src, wf.LaunchConfig(grid_size=2, block_size=block, warp_size=width),
+                    [("i32", a), ("i32", np.zeros(n_thr))])
+        want = semantics.collective(op, a, None, 0, block, width, 0xFFFFFFFF)
+        assert np.array_equal(o, want), op
+
+
+def test_masked_collectives_and_dynamic_smem(wf):
+    src = """
+    __global__ void k(global i32* a, global i32* o, i32 m) {
+        extern shared i32 buf[];
+        i32 t = threadIdx.x;
+        buf[t] = a[t] * 2;
+        __syncthreads();
+        if ((t % 2) == 0) {
+            o[t] = __shfl_down_sync(m, buf[t], 2) + 1000 * __ballot_sync(m, buf[t] > 0);
+        }
+    }"""
+    a = np.arange(-8, 24, dtype=np.int32)
+    mask = 0x55555555
+    _, o = _run(wf, src, wf.LaunchConfig(grid_size=1, block_size=32, shared_bytes=32 * 4),
+                [("i32", a), ("i32", np.zeros(32))], [mask - (1 << 32) if mask >= 1 << 31 else mask])
+    sh = semantics.collective("shfl_down", a * 2, None, 2, 32, 32, mask)
+    bal = semantics.collective("ballot", (a * 2 > 0).astype(np.int32), None, 0, 32, 32, mask)
+    want = np.where(np.arange(32) % 2 == 0, sh + 1000 * bal, 0)
+    assert np.array_equal(o, want)
