@@ -52,6 +52,12 @@ def _run(wf, source, cfg, buffers, scalars=(), specialize=False):
 @pytest.mark.parametrize("specialize", [False, True])
 def test_corpus_bit_exact_vs_reference_oracle(wf, arrays, tag, specialize):
     m = MANIFEST[tag]
+    if m["kernel"] == "warp_neighbor" and m["warp"] < 32:
+        # the kernel hard-codes 32-lane warps (base = tx - tx % 32): at a
+        # smaller logical warp it reads another warp's smem after only a warp
+        # barrier — a race outside the aligned-barrier contract, for which the
+        # reference's serial warp order is just one legal interleaving
+        pytest.skip("racy at warp size < 32 (cross-warp read after __syncwarp)")
     kinds = m["kinds"]
     bufs = [(k, arrays[f"{tag}__in{i}"]) for i, k in enumerate(kinds)]
     scalars = [a[1] for a in m["args"] if a[0] == "scalar"]
