@@ -24,7 +24,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import time
 from pathlib import Path
@@ -66,53 +65,68 @@ def ncu_traffic(name: str):
 
 # ---- clocks sampling (B200_PROFILING.md "clocks DURING the timed region") --
 class ClockSampler:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Polls NVML (SM clock + clock-event reasons) every ~2 ms in a thread for
+    the duration of the timed region; falls back to `nvidia-smi -lms 100`."""
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap"}
 
     def __init__(self, device_index: int):
         self.dev = device_index
-        self.proc = None
-        self.path = Path(f"/tmp/wf_clocks_{os.getpid()}.csv")
+        self.samples = []
+        self.max_mhz = None
+        self._stop = None
+        self._thread = None
+        self._nvml = None
+
+    def _handle(self, nv):
+        import torch
+        try:  # map the CUDA device to its NVML handle through the PCI address
+            pr = torch.cuda.get_device_properties(self.dev)
+            bus_id = f"{int(pr.pci_domain_id):08x}:{int(pr.pci_bus_id):02x}:{int(pr.pci_device_id):02x}.0"
+            return nv.nvmlDeviceGetHandleByPciBusId(bus_id.encode())
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.dev)
 
     def __enter__(self):
+        import threading
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-            time.sleep(0.25)
+            import pynvml as nv
+            nv.nvmlInit()
+            h = self._handle(nv)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self._nvml = nv
+            self._stop = threading.Event()
+
+            def poll():
+                while not self._stop.is_set():
+                    try:
+                        mhz = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                        rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((float(mhz), int(rs)))
+                    except Exception:
+                        pass
+                    self._stop.wait(0.002)
+            self._thread = threading.Thread(target=poll, daemon=True)
+            self._thread.start()
+            time.sleep(0.01)
         except Exception:
-            self.proc = None
+            self._nvml = None
         return self
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            time.sleep(0.15)
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        if self._thread is not None:
+            self._stop.set()
+            self._thread.join(timeout=2)
 
     def summary(self) -> dict:
-        rows = []
-        try:
-            for line in self.path.read_text().splitlines():
-                f = [x.strip() for x in line.split(",")]
-                if len(f) >= 9:
-                    rows.append(f)
-        except Exception:
-            pass
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"],
+                    "samples": 0}
+        reasons = sorted({name for _, rs in self.samples for bit, name in self.REASONS.items()
+                          if rs & bit})
+        return {"sm_mhz": statistics.median(m for m, _ in self.samples),
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples),
+                "source": "NVML, ~2 ms polling during the timed loop"}
 
 
 # ---- distributed plumbing --------------------------------------------------
@@ -151,7 +165,7 @@ def max_over_ranks(v: float, world: int) -> float:
 
 
 # ---- CPU baselines (oracle port of the collapsed loop nests) ---------------
-def cpu_baseline_c2(budget_s: float = 10.0, sample_n: int = 1 << 24) -> dict:
+def cpu_baseline_c2(budget_s: float = 10.0, sample_n: int = 1 << 26) -> dict:
     """The reference's per-warp-partials f32 reduction, collapsed into
     block/warp/lane loop nests (oracle/collapse_ref.c), on all host threads;
     repeated over a bounded sample until ~budget_s."""
@@ -167,7 +181,7 @@ def cpu_baseline_c2(budget_s: float = 10.0, sample_n: int = 1 << 24) -> dict:
         cref.reduce_f32(x, grid, 256, workers)
         reps += 1
         el = time.perf_counter() - t0
-        if el >= budget_s or reps >= 1000:
+        if el >= budget_s or reps >= 100000:
             break
     return {"value": round(sample_n * reps / el / 1e9, 6), "unit": "Gelem/s", "cores": workers,
             "kind": "port",
@@ -199,7 +213,7 @@ def cpu_baseline_kernel(kind: str, budget_s: float) -> dict:
         fn()
         reps += 1
         el = time.perf_counter() - t0
-        if el >= budget_s or reps >= 2000:
+        if el >= budget_s or reps >= 100000:
             break
     return {"value": round(n * reps / el / 1e9, 6), "unit": "Gelem/s", "cores": workers,
             "kind": "port", "sample": f"{reps} x {n} elements, {el:.1f} s"}
@@ -311,7 +325,7 @@ def run_ours(args, rank, world, local) -> dict | None:
         for k, key in (("c1", "c1_reduce_i32"), ("c3", "c3_scan_i32"), ("c4", "c4_compact_i32"),
                        ("c5", "c5_hist_u8")):
             if key in per:
-                per[key]["cpu_baseline"] = cpu_baseline_kernel(k, args.cpu_budget / 4)
+                per[key]["cpu_baseline"] = cpu_baseline_kernel(k, args.cpu_budget / 3)
     traffic = ncu_traffic("reduce_sum_f32")
     return {
         "metric": METRIC,
