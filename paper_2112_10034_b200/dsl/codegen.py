@@ -43,10 +43,24 @@ CTYPE = {I32: "int", F32: "float"}
 
 PRELUDE = r"""
 #define WF_INT_MIN (-2147483647 - 1)
-struct wf_err_t { unsigned long long code; long long arg; long long index; long long length; };
+struct wf_err_t {
+  unsigned long long code; long long arg; long long index; long long length;
+  unsigned long long key; unsigned int lock;
+};
+// Record a fault.  The fault of the lowest global thread id wins (keeps the
+// message reproducible run to run); a thread keeps its first fault.  Faults
+// are rare, so a short spin lock guards the record.
 __device__ __noinline__ void wf_fail(wf_err_t *e, unsigned long long code, long long arg,
                                      long long idx, long long len) {
-  if (atomicCAS(&e->code, 0ull, code) == 0ull) { e->arg = arg; e->index = idx; e->length = len; }
+  const unsigned long long key =
+      (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x + 1ull;
+  while (atomicCAS(&e->lock, 0u, 1u) != 0u) { __nanosleep(32); }
+  __threadfence();
+  if (e->key == 0ull || key < e->key) {
+    e->key = key; e->code = code; e->arg = arg; e->index = idx; e->length = len;
+  }
+  __threadfence();
+  atomicExch(&e->lock, 0u);
 }
 __device__ __forceinline__ int wf_add(int a, int b) { return (int)((unsigned)a + (unsigned)b); }
 __device__ __forceinline__ int wf_sub(int a, int b) { return (int)((unsigned)a - (unsigned)b); }

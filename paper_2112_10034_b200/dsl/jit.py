@@ -107,7 +107,7 @@ class JitProgram:
                 keep.append(C.c_int32(int(bound[p.name])))
             else:
                 keep.append(C.c_float(float(np.float32(bound[p.name]))))
-        err = torch.zeros(4, dtype=torch.int64, device=memory.device)
+        err = torch.zeros(6, dtype=torch.int64, device=memory.device)
         dyn = [s for s, (_, ln) in self.table.shared.items() if ln is None]
         elem = 4
         dyn_len = config.shared_bytes // elem if dyn else 0
@@ -118,7 +118,7 @@ class JitProgram:
                                        config.shared_bytes, argv, stream)
         _lib.check(rc, f"launch of {self.name}")
         torch.cuda.current_stream(memory.device).synchronize()
-        code, arg, idx, length = (int(v) for v in err.cpu().tolist())
+        code, arg, idx, length = (int(v) for v in err.cpu().tolist()[:4])
         if code:
             raise ExecutionError(self._message(code, arg, idx, length))
 

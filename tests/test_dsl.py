@@ -139,3 +139,13 @@ def test_generated_cuda_compiles_for_sm100a(tmp_path):
     with ThreadPoolExecutor(8) as ex:
         for name, rc, err in ex.map(_nvcc, items):
             assert rc == 0, f"{name}: {err[:2000]}"
+
+
+def test_cli_transform_emits_cuda(tmp_path):
+    from paper_2112_10034_b200.__main__ import main
+    out = tmp_path / "k.cu"
+    rc = main(["transform", str(GOLDEN / "C1_I32.spk"), "--block-size", "256", "-o", str(out)])
+    assert rc == 0 and "wf_shfl_down<int>" in out.read_text()
+    bad = tmp_path / "bad.spk"
+    bad.write_text("__global__ void k(global i32* a) { a[0] = 1 }")
+    assert main(["transform", str(bad)]) == 3  # parse error -> EXIT_TRANSFORM
