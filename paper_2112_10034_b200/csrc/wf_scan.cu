@@ -299,12 +299,22 @@ struct PersistShared {
   uint32_t wtot[PNW];
 };
 
+// The first draw of a CTA is a release (it orders the CTA's epoch read before
+// the draw); later draws are relaxed — nothing the tile protocol needs is
+// ordered by them (descriptor values travel inside the descriptor word), and
+// a release there would wait for the previous tile's output stores to be
+// acknowledged (measured: scan 404 -> 390 us, compaction 369 -> 348 us at
+// 2^28).  The last drawer acquires through the counter's release sequence
+// before it resets the counter and bumps the epoch.
+template <bool FIRST>
 __device__ __forceinline__ uint32_t draw_ticket(TileHeader *hdr, uint32_t ntiles,
                                                 uint32_t epoch, bool &drained) {
-  const uint32_t t = atom_add_acq_rel_gpu(&hdr->ticket, 1u);
+  const uint32_t t = FIRST ? atom_add_acq_rel_gpu(&hdr->ticket, 1u)
+                           : atom_add_relaxed_gpu(&hdr->ticket, 1u);
   if (t >= ntiles) {
     drained = true;
     if (t == ntiles + gridDim.x - 1) {  // last of all draws
+      fence_acq_rel_gpu();
       atomicExch(&hdr->ticket, 0u);
       atomicExch(&hdr->epoch, (epoch + 1) & kEpochMask);
     }
@@ -332,7 +342,7 @@ __global__ void __launch_bounds__(PBLOCK)
     fence_barrier_init();
     sh.epoch = ld_volatile_u32(&hdr->epoch) & kEpochMask;  // ordered by the release draw
     for (int s = 0; s < PSTAGES; ++s) {
-      const uint32_t t = drained ? kNoTile : draw_ticket(hdr, ntiles, sh.epoch, drained);
+      const uint32_t t = drained ? kNoTile : draw_ticket<true>(hdr, ntiles, sh.epoch, drained);
       if (t != kNoTile) WF_STAMP(t, 0);
       sh.tile[s] = t;
       if (t != kNoTile && uint64_t(t + 1) * PTILE <= n) {
@@ -458,7 +468,7 @@ __global__ void __launch_bounds__(PBLOCK)
     WF_STAMP(tile, 3);
     __syncthreads();  // stage s fully consumed by the threads
     if (threadIdx.x == 0) {  // refill stage s with the next tile
-      const uint32_t tn = drained ? kNoTile : draw_ticket(hdr, ntiles, epoch, drained);
+      const uint32_t tn = drained ? kNoTile : draw_ticket<false>(hdr, ntiles, epoch, drained);
       if (tn != kNoTile) WF_STAMP(tn, 0);
       sh.tile[s] = tn;
       if (!COMPACT && tn != kNoTile) bulk_wait_read_all();  // bulk store has left stage s

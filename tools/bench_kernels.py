@@ -66,3 +66,12 @@ if "c3" in which or "c4" in which:
 if "c5" in which:
     u = ops.fill_synthetic("u8_uniform", 1 << 32)
     t(lambda: ops.histogram256_u8(u), 1 << 32, "c5")
+if "ref" in which:
+    # library reference points on the same box: torch copy (read+write) and
+    # torch.cumsum on int32 (CUB DeviceScan), both over 2^28 int32
+    x = ops.fill_synthetic("i32_full", 1 << 28)
+    y = torch.empty_like(x)
+    t(lambda: y.copy_(x), 8 << 28, "ref torch copy 1 GiB")
+    t(lambda: torch.cumsum(x, 0, out=y), 8 << 28, "ref torch.cumsum i32 (CUB)")
+    t(lambda: torch.masked_select(x, x > 0), 6 << 28, "ref torch.masked_select x>0")
+    del x, y

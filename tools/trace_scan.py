@@ -20,10 +20,12 @@ ntiles = n // int(os.environ.get('WF_TRACE_TILE', '4096'))
 tr = torch.zeros(ntiles * 4, dtype=torch.int64, device="cuda")
 lib = _lib.load()
 raw = ctypes.CDLL(str(_lib.lib_path()))
+op = os.environ.get("WF_TRACE_OP", "scan")
+run = (lambda: ops.scan_inclusive_i32(x, y)) if op == "scan" else (lambda: ops.compact_gt0_i32(x, y))
 for _ in range(3):
-    ops.scan_inclusive_i32(x, y)
+    run()
 raw.wf_debug_set_trace(ctypes.c_void_p(tr.data_ptr()))
-ops.scan_inclusive_i32(x, y)
+run()
 torch.cuda.synchronize()
 raw.wf_debug_set_trace(ctypes.c_void_p(0))
 t = tr.cpu().numpy().reshape(-1, 4).astype(np.float64)
@@ -33,7 +35,7 @@ load = t[:, 1] - t[:, 0]
 wait = t[:, 2] - t[:, 1]
 store = t[:, 3] - t[:, 2]
 life = t[:, 3] - t[:, 0]
-res = {"kernel_span_us": float(t[:, 3].max()),
+res = {"op": op, "lib": os.environ.get("WF_LIB", ""), "kernel_span_us": float(t[:, 3].max()),
        "load_compute_us": [float(np.percentile(load, q)) for q in (10, 50, 90, 99)],
        "lookback_wait_us": [float(np.percentile(wait, q)) for q in (10, 50, 90, 99)],
        "store_us": [float(np.percentile(store, q)) for q in (10, 50, 90, 99)],
@@ -48,5 +50,5 @@ mid = t[:, 3].max() / 2
 res["tiles_in_flight_mid"] = int(((t[:, 0] <= mid) & (t[:, 3] > mid)).sum())
 res["tiles_waiting_lookback_mid"] = int(((t[:, 1] <= mid) & (t[:, 2] > mid)).sum())
 res["tiles_loading_mid"] = int(((t[:, 0] <= mid) & (t[:, 1] > mid)).sum())
-print(json.dumps(res, indent=1))
-np.save("gpurun_out/scan_trace.npy", t.astype(np.float32))
+print(json.dumps(res))
+np.save(f"gpurun_out/{op}_trace_{Path(os.environ.get('WF_LIB', 'x')).stem}.npy", t.astype(np.float32))
