@@ -28,6 +28,7 @@ _LAZY = {
     "dsl": ("dsl", None),
     "parse_module": ("dsl", "parse_module"),
     "hybrid_transform": ("dsl", "hybrid_transform"),
+    "ExecTrace": ("trace", "ExecTrace"),
 }
 
 
@@ -42,7 +43,7 @@ def __getattr__(name):
     raise AttributeError(name)
 
 
-__all__ = ["LaunchConfig", "DeviceMemory", "launch", "bind_args", "PROGRAMS", "warp_program",
+__all__ = ["LaunchConfig", "DeviceMemory", "launch", "ExecTrace", "bind_args", "PROGRAMS", "warp_program",
            "ops", "distributed", "parse_module", "hybrid_transform", "WarpfoldError",
            "ParseError", "SemanticError", "UnsupportedFeatureError", "TransformError",
            "ConfigError", "LaunchError", "ExecutionError", "BarrierViolation",

@@ -26,11 +26,20 @@ to make every scalar operation mean exactly what it means in the reference:
   SHFL.IDX with an explicitly computed source lane, not the 5-bit-masked
   SHFL.DOWN), votes return 0/1.  The reference's warp of W lanes is a
   W-lane segment of the hardware warp (W = LaunchConfig.warp_size).
+
+Trace mode (``trace=True``) adds execution counting with the reference's
+instruction identities: uids are allocated in exactly the order
+cfg/build.py:37-186 allocates them (exit ``Ret`` first, collectives hoisted
+left to right before their statement, a guard and a latch ``CondBr`` per loop
+with the condition's collectives lowered twice, nothing after a ``return``),
+and every executed instruction / terminator bumps its counter once per thread,
+as ``interp/oracle.py:113-136`` counts them.
 """
 
 from __future__ import annotations
 
 import struct
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -62,6 +71,8 @@ __device__ __noinline__ void wf_fail(wf_err_t *e, unsigned long long code, long 
   __threadfence();
   atomicExch(&e->lock, 0u);
 }
+// execution counting (ExecTrace): one counter per reference CFG uid
+__device__ __forceinline__ void wf_tick(unsigned long long *t, int uid) { atomicAdd(t + uid, 1ull); }
 __device__ __forceinline__ int wf_add(int a, int b) { return (int)((unsigned)a + (unsigned)b); }
 __device__ __forceinline__ int wf_sub(int a, int b) { return (int)((unsigned)a - (unsigned)b); }
 __device__ __forceinline__ int wf_mul(int a, int b) { return (int)((unsigned)a * (unsigned)b); }
@@ -153,9 +164,15 @@ def _i32_literal(v: int) -> str:
 
 class CudaGen:
     def __init__(self, kernel: n.KernelDef, table: SymbolTable, warp_size: int,
-                 block_size: int | None = None, grid_size: int | None = None):
+                 block_size: int | None = None, grid_size: int | None = None,
+                 trace: bool = False):
         self.k, self.t, self.W = kernel, table, warp_size
         self.block_size, self.grid_size = block_size, grid_size  # specialize (JIT mode)
+        self.trace = trace
+        self.uid = 0                       # cfg/ir.py:154-161 (Cfg.new_uid)
+        self.instr_uids: list[int] = []    # Assign / DeclLocal / DeclShared / Collective / Barrier
+        self.term_uids: list[int] = []     # Br / CondBr / Ret allocated by the builder
+        self.uid_kind: dict[int, str] = {}  # uid -> reference IR class name (cfg/ir.py)
         self.lines: list[str] = []
         self.arrays: list[str] = []  # error-record arg index -> array name
         for p in kernel.params:
@@ -163,6 +180,17 @@ class CudaGen:
                 self.arrays.append(p.name)
         for name in table.shared:
             self.arrays.append(name)
+
+    # -- uids (trace mode)
+    def new_uid(self, kind: str) -> int:
+        self.uid += 1
+        term = kind in ("Br", "CondBr", "Ret")
+        (self.term_uids if term else self.instr_uids).append(self.uid)
+        self.uid_kind[self.uid] = kind
+        return self.uid
+
+    def tick(self, uid: int) -> str:
+        return f"wf_tick(wf_tr, {uid});" if self.trace else ""
 
     # -- names
     def arr_ptr(self, name: str) -> str:
@@ -237,13 +265,20 @@ class CudaGen:
         return f"((unsigned)({m}) & wf_present())"
 
     def collective(self, e: n.CollectiveCall) -> tuple[str, str]:
-        m = self.mask(e.mask)
+        # operands first, then the collective's own uid (cfg/build.py:153-159)
         if e.op in ("shfl_down", "shfl_up", "shfl_xor", "shfl_idx"):
             v, vk = self.expr(e.args[0])
             o, _ = self.expr(e.args[1])
-            return f"wf_{e.op}<{CTYPE[vk]}>({v}, {o}, {m})", vk
-        a, _ = self.expr(e.args[0])
-        return f"wf_{e.op}({a}, {m})", I32
+            m = self.mask(e.mask)
+            code, kind = f"wf_{e.op}<{CTYPE[vk]}>({v}, {o}, {m})", vk
+        else:
+            a, _ = self.expr(e.args[0])
+            m = self.mask(e.mask)
+            code, kind = f"wf_{e.op}({a}, {m})", I32
+        uid = self.new_uid("Collective")
+        if self.trace:
+            code = f"(wf_tick(wf_tr, {uid}), {code})"
+        return code, kind
 
     def convert(self, code: str, src: str, dst: str) -> str:
         return f"wf_f({code})" if (dst == F32 and src == I32) else code
@@ -253,60 +288,121 @@ class CudaGen:
         self.lines.append("  " * depth + line)
 
     def assign(self, s: n.Assign, depth: int, as_expr: bool = False) -> str:
-        val, vk = self.expr(s.expr)
+        # store index, then value, then the Assign's uid (cfg/build.py:67-73)
         tg = s.target
+        idx = self.expr(tg.index)[0] if isinstance(tg, n.IndexTarget) else None
+        val, vk = self.expr(s.expr)
+        uid = self.new_uid("Assign")
         if isinstance(tg, n.VarTarget):
             code = f"{self.var(tg.name)} = {self.convert(val, vk, self.t.locals[tg.name])}"
         else:
             kind = self.t.element_kind(tg.base)
-            idx, _ = self.expr(tg.index)
             code = (f"wf_st<{CTYPE[kind]}>({self.arr_ptr(tg.base)}, {self.arr_len(tg.base)}, "
                     f"(long long)({idx}), {self.convert(val, vk, kind)}, {self.arr_id(tg.base)}, wf_e)")
+        if self.trace:
+            code = f"{code}, wf_tick(wf_tr, {uid})"
         if as_expr:
             return code
         self.emit(code + ";", depth)
         return code
 
-    def stmts(self, body, depth: int):
+    def stmts(self, body, depth: int) -> bool:
+        """Returns False when control cannot fall through (after a return the
+        reference lowers nothing more of the list, cfg/build.py:56-58)."""
         for s in body:
-            self.stmt(s, depth)
+            if not self.stmt(s, depth):
+                return False
+        return True
 
-    def stmt(self, s, depth: int):
+    def decl_local(self, s: n.DeclLocal, depth: int) -> None:
+        uid = self.new_uid("DeclLocal")
+        if self.trace:
+            self.emit(self.tick(uid), depth)
+        if s.init is not None:
+            v, vk = self.expr(s.init)
+            a_uid = self.new_uid("Assign")
+            self.emit(f"v_{s.name} = {self.convert(v, vk, s.kind)};{self.tick(a_uid)}", depth)
+
+    def init_stmt(self, init, depth: int) -> None:
+        if isinstance(init, n.DeclLocal):
+            self.decl_local(init, depth)
+        else:
+            self.assign(init, depth)
+
+    def stmt(self, s, depth: int) -> bool:
         if isinstance(s, n.DeclLocal):
-            if s.init is not None:
-                v, vk = self.expr(s.init)
-                self.emit(f"v_{s.name} = {self.convert(v, vk, s.kind)};", depth)
+            self.decl_local(s, depth)
         elif isinstance(s, n.DeclShared):
-            pass  # hoisted
+            uid = self.new_uid("DeclShared")  # storage hoisted; the declaration still executes
+            if self.trace:
+                self.emit(self.tick(uid), depth)
         elif isinstance(s, n.Assign):
             self.assign(s, depth)
         elif isinstance(s, n.If):
             c, _ = self.expr(s.cond)
-            self.emit(f"if (({c}) != 0) {{", depth)
-            self.stmts(s.then, depth + 1)
+            cb = self.new_uid("CondBr")
+            self.emit(f"{self.tick(cb)}if (({c}) != 0) {{", depth)
+            if s.then and self.stmts(s.then, depth + 1):
+                self.emit(self.tick(self.new_uid("Br")), depth + 1)
             if s.orelse is not None:
                 self.emit("} else {", depth)
-                self.stmts(s.orelse, depth + 1)
+                if s.orelse and self.stmts(s.orelse, depth + 1):
+                    self.emit(self.tick(self.new_uid("Br")), depth + 1)
             self.emit("}", depth)
         elif isinstance(s, n.For):
+            self.loop(s, depth)
+        elif isinstance(s, n.SyncThreads):
+            uid = self.new_uid("Barrier")
+            self.emit(f"{self.tick(uid)}__syncthreads();", depth)
+        elif isinstance(s, n.SyncWarp):
+            m = self.mask(s.mask)
+            uid = self.new_uid("Barrier")
+            self.emit(f"{self.tick(uid)}__syncwarp({m});", depth)
+        elif isinstance(s, n.Return):
+            uid = self.new_uid("Br")
+            self.emit(f"{self.tick(uid)}goto wf_exit;" if self.trace else "return;", depth)
+            return False
+        else:
+            raise TransformError(f"cannot generate {type(s).__name__}")
+        return True
+
+    def loop(self, s: n.For, depth: int) -> None:
+        if not self.trace:
             if isinstance(s.init, n.DeclLocal):
+                self.new_uid("DeclLocal")
                 v, vk = self.expr(s.init.init)
+                self.new_uid("Assign")
                 init = f"v_{s.init.name} = {self.convert(v, vk, s.init.kind)}"
             else:
                 init = self.assign(s.init, depth, as_expr=True)
             c, _ = self.expr(s.cond)
-            step = self.assign(s.step, depth, as_expr=True)
-            self.emit(f"for ({init}; ({c}) != 0; {step}) {{", depth)
-            self.stmts(s.body, depth + 1)
+            self.new_uid("CondBr")
+            start = len(self.lines)
+            self.emit("", depth)  # header placeholder: the step is generated after the body
+            alive = self.stmts(s.body, depth + 1)
+            step = self.assign(s.step, depth, as_expr=True) if alive else ""
+            if alive:
+                self.expr(s.cond)
+                self.new_uid("CondBr")
+            self.lines[start] = "  " * depth + f"for ({init}; ({c}) != 0; {step}) {{"
             self.emit("}", depth)
-        elif isinstance(s, n.SyncThreads):
-            self.emit("__syncthreads();", depth)
-        elif isinstance(s, n.SyncWarp):
-            self.emit(f"__syncwarp({self.mask(s.mask)});", depth)
-        elif isinstance(s, n.Return):
-            self.emit("return;", depth)
+            return
+        # trace mode: the reference's bottom-tested shape (cfg/build.py:116-134)
+        # so the guard and the latch test are counted separately
+        self.init_stmt(s.init, depth)
+        c1, _ = self.expr(s.cond)
+        g = self.new_uid("CondBr")
+        self.emit(f"{self.tick(g)}if (({c1}) != 0) {{", depth)
+        self.emit("do {", depth + 1)
+        alive = self.stmts(s.body, depth + 2)
+        if alive:
+            self.assign(s.step, depth + 2)
+            c2, _ = self.expr(s.cond)
+            latch = self.new_uid("CondBr")
+            self.emit(f"}} while ((wf_tick(wf_tr, {latch}), ({c2}) != 0));", depth + 1)
         else:
-            raise TransformError(f"cannot generate {type(s).__name__}")
+            self.emit("} while (0);", depth + 1)
+        self.emit("}", depth)
 
     def generate(self) -> str:
         params = []
@@ -317,6 +413,9 @@ class CudaGen:
             else:
                 params.append(f"{CTYPE[p.kind]} p_{p.name}")
         params += ["wf_err_t *__restrict__ wf_e", "long long wf_dyn_len"]
+        if self.trace:
+            params.append("unsigned long long *__restrict__ wf_tr")
+        ret_uid = self.new_uid("Ret")  # the exit block's Ret is allocated first
         out = [f"#define WF_W {self.W}u", PRELUDE,
                f'extern "C" __global__ void __launch_bounds__(1024) wf_kernel({", ".join(params)}) {{']
         for name, (kind, length) in self.t.shared.items():
@@ -332,7 +431,12 @@ class CudaGen:
             out.append("  __syncthreads();")
         for name, kind in self.t.locals.items():
             out.append(f"  {CTYPE[kind]} v_{name} = ({CTYPE[kind]})0;")
-        self.stmts(self.k.body, 1)
+        if self.stmts(self.k.body, 1):
+            end = self.new_uid("Br")
+            if self.trace:
+                self.emit(self.tick(end), 1)
+        if self.trace:
+            self.emit(f"wf_exit: {self.tick(ret_uid)}", 0)
         out += self.lines
         out.append("}")
         return "\n".join(out) + "\n"
@@ -342,3 +446,21 @@ def generate(kernel: n.KernelDef, table: SymbolTable, warp_size: int = 32,
              block_size: int | None = None, grid_size: int | None = None) -> tuple[str, list]:
     g = CudaGen(kernel, table, warp_size, block_size, grid_size)
     return g.generate(), g.arrays
+
+
+@dataclass
+class TraceLayout:
+    """uids the reference's CFG builder allocates for a kernel."""
+    instr_uids: list
+    term_uids: list
+    max_uid: int
+    kinds: dict  # uid -> reference IR class name
+
+
+def generate_traced(kernel: n.KernelDef, table: SymbolTable, warp_size: int = 32,
+                    block_size: int | None = None,
+                    grid_size: int | None = None) -> tuple[str, list, TraceLayout]:
+    g = CudaGen(kernel, table, warp_size, block_size, grid_size, trace=True)
+    src = g.generate()
+    return src, g.arrays, TraceLayout(list(g.instr_uids), list(g.term_uids), g.uid,
+                                      dict(g.uid_kind))

@@ -23,7 +23,7 @@ from ..config import LaunchConfig
 from ..errors import ExecutionError, TransformError, UnsupportedFeatureError
 from . import nodes as n
 from .checker import SymbolTable, check_kernel
-from .codegen import generate
+from .codegen import generate, generate_traced
 
 _cache_lock = threading.Lock()
 _module_cache: dict = {}
@@ -63,6 +63,25 @@ class JitProgram:
     specialized: dict | None = None
     source: str = ""
     arrays: list = field(default_factory=list)
+    traced_source: str = ""
+    layout: object = None  # codegen.TraceLayout of the traced build
+
+    @property
+    def original_instr_uids(self) -> list:
+        """Instruction uids of the reference CFG (MpmdProgram.original_instr_uids)."""
+        return list(self._layout().instr_uids)
+
+    def src_map(self) -> dict:
+        """Identity: native compilation clones nothing (MpmdProgram.src_map)."""
+        return {}
+
+    def _layout(self):
+        if self.layout is None:
+            spec = self.specialized or {}
+            self.traced_source, _, self.layout = generate_traced(
+                self.kernel, self.table, self.warp_size, spec.get("block_size"),
+                spec.get("grid_size"))
+        return self.layout
 
     def cuda_source(self, config: LaunchConfig | None = None) -> str:
         spec = self.specialized or {}
@@ -71,9 +90,13 @@ class JitProgram:
         self.arrays = arrays
         return src
 
-    def _module(self):
-        src = self.source or self.cuda_source()
-        self.source = src
+    def _module(self, traced: bool = False):
+        if traced:
+            self._layout()
+            src = self.traced_source
+        else:
+            src = self.source or self.cuda_source()
+            self.source = src
         with _cache_lock:
             mod = _module_cache.get(src)
             if mod is None:
@@ -90,14 +113,14 @@ class JitProgram:
                 _module_cache[src] = mod
         return mod
 
-    def run(self, config: LaunchConfig, memory, bound: dict) -> None:
+    def run(self, config: LaunchConfig, memory, bound: dict, trace=None) -> None:
         import torch
         if self.specialized and (self.specialized["block_size"] != config.block_size or
                                  self.specialized["grid_size"] != config.grid_size):
             raise TransformError("program was specialized for a different launch configuration")
         if config.warp_size != self.warp_size:
             raise TransformError(f"program was generated for warp size {self.warp_size}")
-        mod = self._module()
+        mod = self._module(traced=trace is not None)
         keep, argv = [], []
         for p in self.params:
             if p.is_buffer:
@@ -112,6 +135,9 @@ class JitProgram:
         elem = 4
         dyn_len = config.shared_bytes // elem if dyn else 0
         keep += [C.c_void_p(err.data_ptr()), C.c_longlong(dyn_len)]
+        if trace is not None:
+            counts = torch.zeros(self.layout.max_uid + 1, dtype=torch.int64, device=memory.device)
+            keep.append(C.c_void_p(counts.data_ptr()))
         argv = (C.c_void_p * len(keep))(*[C.cast(C.pointer(k), C.c_void_p) for k in keep])
         stream = torch.cuda.current_stream(memory.device).cuda_stream
         rc = _lib.load().wf_jit_launch(mod, config.grid_size, config.block_size,
@@ -121,6 +147,14 @@ class JitProgram:
         code, arg, idx, length = (int(v) for v in err.cpu().tolist()[:4])
         if code:
             raise ExecutionError(self._message(code, arg, idx, length))
+        if trace is not None:
+            c = counts.cpu().tolist()
+            for uid in self.layout.instr_uids:
+                if c[uid]:
+                    trace.count_instr(uid, c[uid])
+            for uid in self.layout.term_uids:
+                if c[uid]:
+                    trace.count_term(uid, c[uid])
 
     def _message(self, code, arg, idx, length) -> str:
         if code in (1, 2):

@@ -78,12 +78,16 @@ def launch(program, config: LaunchConfig, memory: DeviceMemory, args, trace=None
     config.validate(hierarchical=(getattr(program, "mode", "hier") == "hier"))
     if config.grid_size == 0:
         return
-    if trace is not None:
+    if trace is not None and isinstance(program, NativeProgram):
         raise UnsupportedFeatureError(
-            "execution-count tracing (ExecTrace) is not provided by the GPU path")
+            f"execution-count tracing (ExecTrace) needs a DSL kernel; {program.name!r} is a "
+            f"named native op with no reference CFG")
     bound = bind_args(program.params, memory, args)
     with torch.cuda.device(memory.device):
-        program.run(config, memory, bound)
+        if trace is None:
+            program.run(config, memory, bound)
+        else:  # DSL kernel compiled with per-uid counters (interp/trace.py:9-50)
+            program.run(config, memory, bound, trace=trace)
         torch.cuda.current_stream(memory.device).synchronize()
 
 

@@ -16,6 +16,9 @@ the reference's own code paths:
   - c3_pin.npz: warp inclusive prefix scan (lane-reversed shfl_down, the only
     formulation the reference DSL can express) through run_oracle and launch
   - corpus.npz: all 17 corpus kernels (corpus.py) through run_oracle
+  - corpus_traces.json: run_oracle ExecTrace counts for the same runs and the
+    cfg/build.py uid -> IR-class catalogue of every kernel (--traces-only
+    regenerates just this file)
 """
 
 from __future__ import annotations
@@ -191,7 +194,40 @@ def corpus_golden() -> tuple[dict, dict]:
     return arrays, manifest
 
 
+def corpus_traces() -> dict:
+    """ExecTrace counts from run_oracle (interp/oracle.py:113-136) for every
+    corpus configuration, plus each kernel's uid -> IR-class catalogue as
+    cfg/build.py allocates it (pins the GPU trace build's uid numbering)."""
+    from warpfold import ExecTrace
+    from warpfold.cfg.build import build_cfg
+    out = {"runs": {}, "kernels": {}}
+    extra = [("C1_I32", C1_I32), ("C1_F32", C1_F32), ("C3_WARP_PREFIX", C3_WARP_PREFIX)]
+    for name, src in [(k.name, k.source) for k in corpus.ALL] + extra:
+        cfg = build_cfg(parse_module(src).kernel())
+        kinds = {}
+        for b in cfg.blocks.values():
+            for i in b.instrs:
+                kinds[str(i.uid)] = type(i).__name__
+            kinds[str(b.term.uid)] = type(b.term).__name__
+        out["kernels"][name] = {"uid_kinds": kinds, "max_uid": cfg._next_uid}
+    for k in corpus.ALL:
+        for grid, block, warp in ((2, 64, 32), (3, 32, 32), (2, 8, 4), (1, 16, 8)):
+            mem, args = k.build(grid, block, 0)
+            kernel = k.kernel()
+            cfg = LaunchConfig(grid_size=grid, block_size=block, warp_size=warp, workers=1)
+            tr = ExecTrace()
+            run_oracle(kernel, cfg, bind_args(kernel.params, mem, args), tr)
+            out["runs"][f"{k.name}__g{grid}b{block}w{warp}"] = {
+                "instr": {str(u): c for u, c in sorted(tr.instr_counts.items())},
+                "term": {str(u): c for u, c in sorted(tr.term_counts.items())}}
+    return out
+
+
 def main() -> None:
+    if "--traces-only" in sys.argv:
+        (HERE / "corpus_traces.json").write_text(json.dumps(corpus_traces(), indent=0))
+        return
+    (HERE / "corpus_traces.json").write_text(json.dumps(corpus_traces(), indent=0))
     (HERE / "warp_semantics.json").write_text(json.dumps(warp_semantics(), indent=1))
     np.savez_compressed(HERE / "oracle_kat.npz", **oracle_kat())
     np.savez_compressed(HERE / "c1c2_pin.npz", **c1c2_pin())

@@ -55,3 +55,15 @@ def test_cli_run_json_and_errors(built, capsys, tmp_path):
     # reference; thread 4 (lowest faulting id) reports
     assert "out-of-bounds read a[4], length 4" in capsys.readouterr().err
     assert main(["run", str(tmp_path / "missing.json")]) == 2
+
+
+def test_cli_run_trace_counts(built, tmp_path):
+    # cli.py:90-94: --trace-counts writes ExecTrace.to_json() of the DSL launches
+    from paper_2112_10034_b200.__main__ import main
+    out = tmp_path / "counts.json"
+    assert main(["run", str(DATA / "scan_pipeline.json"), "--trace-counts", str(out)]) == 0
+    data = json.loads(out.read_text())
+    assert set(data) >= {"instructions", "terminators"}
+    assert data["instructions"] and all(v > 0 for v in data["instructions"].values())
+    # uid 1 is every DSL kernel's exit Ret: reached once per launched thread
+    assert data["terminators"]["1"] % 32 == 0
