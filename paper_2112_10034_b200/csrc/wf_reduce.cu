@@ -139,14 +139,18 @@ __global__ void __launch_bounds__(BLOCK)
   const acc_t bsum = block_sum<Op, BLOCK>(acc[0][0]);
 
   if (Op::kOrderFree) {
-    // integer Σ is order-independent: one RED per block into the workspace
-    // accumulator, the last block (acq_rel ticket) publishes and resets it
+    // integer Σ is order-independent: ONE 64-bit atomic per block carries both
+    // the block sum (low 48 bits: 32 bits of sum + up to 2^16 wraps) and an
+    // arrival count (high 16 bits).  The block that sees count == grid-1 holds
+    // the full sum in the returned value — no fence, no second atomic, no
+    // separate ticket on the critical path of this latency-bound kernel.
     if (threadIdx.x == 0) {
-      uint32_t *accum = reinterpret_cast<uint32_t *>(ticket) + 1;
-      red_add_relaxed_gpu(accum, Op::bits(bsum));
-      if (atom_add_acq_rel_gpu(ticket, 1u) == gridDim.x - 1) {
-        out[0] = Op::to_elem(Op::from_bits(atomicExch(accum, 0u)));
-        *ticket = 0u;
+      auto *word = reinterpret_cast<unsigned long long *>(ticket);
+      const unsigned long long mine = (1ull << 48) | Op::bits(bsum);
+      const unsigned long long old = atomicAdd(word, mine);
+      if ((old >> 48) == gridDim.x - 1) {
+        out[0] = Op::to_elem(Op::from_bits(uint32_t(old + mine)));
+        *word = 0ull;  // next stream-ordered launch starts from zero
       }
     }
     return;
