@@ -65,7 +65,7 @@ static size_t ws_need(int op, uint64_t n) {
     case WF_OP_SCAN_INCLUSIVE_I32:
     case WF_OP_COMPACT_GT0_I32: {
       const uint64_t tiles = (n + kScanTile - 1) / kScanTile;
-      return kWsHeader + size_t(tiles < 1 ? 1 : tiles) * 8 * kDescStride;
+      return kTileWsHeader + size_t(tiles < 1 ? 1 : tiles) * 8 * kDescStride;
     }
     case WF_OP_HISTOGRAM256_U8:
       return kWsHeader + 256 * 8;

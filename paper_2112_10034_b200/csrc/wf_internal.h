@@ -10,6 +10,18 @@ namespace wf {
 
 // Workspace layout: a 256-byte header followed by op-specific arrays.
 constexpr size_t kWsHeader = 256;
+// Scan / compaction workspaces have a larger header: bytes [256, 8192) hold
+// the two-pass kernel's per-chunk arrival counters (16 B apart), which no
+// other kernel writes, so they stay zero between launches whatever the
+// single-pass kernel left in the descriptor array behind the header.
+constexpr size_t kTileWsHeader = 8192;
+constexpr size_t kChunkCnt2P = 1024;  // [256, 1024): two-pass tickets
+constexpr uint32_t kMaxChunks2P = uint32_t((kTileWsHeader - kChunkCnt2P) / 16);
+constexpr uint32_t kMaxChunkTiles2P = 1024;
+#ifndef WF_2P_MIN_N
+#define WF_2P_MIN_N (1ull << 22)
+#endif
+constexpr uint64_t kTwoPassMinN = WF_2P_MIN_N;
 constexpr uint32_t kMaxReduceGrid = 8192;   // partial slots for reductions
 constexpr int kScanBlock = 256;             // threads per scan/compact tile
 constexpr int kScanVec = 4;                 // int4 loads per thread per tile
@@ -40,6 +52,13 @@ cudaError_t launch_scan_i32(const int32_t *in, int32_t *out, uint64_t n,
 cudaError_t launch_compact_gt0_i32(const int32_t *in, uint64_t n,
                                    int32_t *out, uint64_t *count, void *ws,
                                    cudaStream_t s);
+
+// L2-streamed two-pass scan / compaction (wf_scan2p.cu), 16 B aligned buffers
+bool two_pass_usable(uint64_t n);
+cudaError_t launch_scan2p_i32(const int32_t *in, int32_t *out, uint64_t n,
+                              const int32_t *carry, void *ws, cudaStream_t s);
+cudaError_t launch_compact2p_i32(const int32_t *in, uint64_t n, int32_t *out,
+                                 uint64_t *count, void *ws, cudaStream_t s);
 
 // histogram (wf_hist.cu)
 cudaError_t launch_hist256(const uint8_t *in, uint64_t n, uint64_t *bins,

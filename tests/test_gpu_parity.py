@@ -223,6 +223,60 @@ def test_compact_full_config(ops):
     assert torch.equal(out[:m], want)
 
 
+# ---- K3/K4 opt-in L2-streamed two-pass variant (wf_scan2p.cu) ---------------
+
+@pytest.fixture
+def two_pass(monkeypatch):
+    """Enable the two-pass kernels with a tiny size threshold and small chunks
+    so modest inputs span many chunks (look-back over chunk descriptors,
+    ragged last chunk and tile)."""
+    monkeypatch.setenv("WF_SCAN_2P", "1")
+    monkeypatch.setenv("WF_2P_MIN_N", "1")
+    monkeypatch.setenv("WF_2P_CHUNK_TILES", "3")
+    yield monkeypatch
+
+
+@pytest.mark.parametrize("n", [1, 4097, 8192 * 7, 8192 * 7 + 3, 1 << 20, (1 << 22) + 13])
+def test_two_pass_scan_compact(ops, two_pass, n):
+    a = synthetic.generate("i32_full", n, seed=n + 5)
+    assert np.array_equal(host(ops.scan_inclusive_i32(dev(a))), no.scan_inclusive_i32(a))
+    carry = torch.tensor([-7], dtype=torch.int32, device="cuda")
+    assert np.array_equal(host(ops.scan_inclusive_i32(dev(a), carry=carry)),
+                          no.scan_inclusive_i32(a, carry=-7))
+    out, cnt = ops.compact_gt0_i32(dev(a))
+    want = no.compact_gt0_i32(a)
+    assert int(host(cnt)[0]) == len(want) and np.array_equal(host(out)[:len(want)], want)
+
+
+def test_two_pass_interleaved_with_single_pass(ops, two_pass):
+    # one cached workspace serves both designs: stale single-pass descriptors
+    # must never read as two-pass state (8 KiB header rule, epochs)
+    for i, n in enumerate([1 << 18, 5000, (1 << 18) + 77, 1 << 16]):
+        two_pass.setenv("WF_SCAN_2P", "1" if i % 2 == 0 else "0")
+        for chunk in ("1", "64"):
+            two_pass.setenv("WF_2P_CHUNK_TILES", chunk)
+            a = synthetic.generate("i32_select", n, seed=i, param=300)
+            assert np.array_equal(host(ops.scan_inclusive_i32(dev(a))), no.scan_inclusive_i32(a))
+            out, cnt = ops.compact_gt0_i32(dev(a))
+            want = no.compact_gt0_i32(a)
+            assert int(host(cnt)[0]) == len(want)
+            assert np.array_equal(host(out)[:len(want)], want)
+
+
+@pytest.mark.slow
+def test_two_pass_full_config(ops, monkeypatch):
+    monkeypatch.setenv("WF_SCAN_2P", "1")
+    n = 1 << 28
+    x = ops.fill_synthetic("i32_full", n, seed=9)
+    y = ops.scan_inclusive_i32(x)
+    d = (y[1:].to(torch.int64) - y[:-1].to(torch.int64) - x[1:].to(torch.int64)) % (1 << 32)
+    assert int(d.count_nonzero()) == 0 and host(y[:1])[0] == host(x[:1])[0]
+    del y, d
+    out, cnt = ops.compact_gt0_i32(x)
+    want = torch.masked_select(x, x > 0)
+    assert int(host(cnt)[0]) == want.numel() and torch.equal(out[:want.numel()], want)
+
+
 # ---- K5 ----------------------------------------------------------------------
 
 @pytest.mark.parametrize("n", SIZES + [(1 << 22) + 13])

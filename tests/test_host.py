@@ -112,9 +112,9 @@ def test_abi_metadata(lib):
     assert lib.wf_abi_version() == 1
     assert b"sm_100a" in lib.wf_version()
     assert lib.wf_workspace_bytes(_lib.OP_REDUCE_SUM_F32, 1 << 30, 256) >= 256
-    # scan workspace: header + one descriptor per 4096-element tile, each on
+    # scan workspace: 8 KiB header (two-pass chunk counters) + one descriptor per 4096-element tile, each on
     # its own 128-byte line (look-back polling must not share lines)
-    assert lib.wf_workspace_bytes(_lib.OP_SCAN_INCLUSIVE_I32, 1 << 28, 256) == 256 + (1 << 16) * 128
+    assert lib.wf_workspace_bytes(_lib.OP_SCAN_INCLUSIVE_I32, 1 << 28, 256) == 8192 + (1 << 16) * 128
     assert lib.wf_workspace_bytes(_lib.OP_HISTOGRAM256_U8, 1, 256) == 256 + 2048
 
 
