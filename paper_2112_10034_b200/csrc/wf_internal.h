@@ -53,6 +53,13 @@ cudaError_t launch_compact_gt0_i32(const int32_t *in, uint64_t n,
                                    int32_t *out, uint64_t *count, void *ws,
                                    cudaStream_t s);
 
+// TMEM-parked single-pass scan / compaction (wf_scan_tmem.cu), 16 B aligned
+bool tmem_scan_enabled();
+cudaError_t launch_scan_tmem_i32(const int32_t *in, int32_t *out, uint64_t n,
+                                 const int32_t *carry, void *ws, cudaStream_t s);
+cudaError_t launch_compact_tmem_i32(const int32_t *in, uint64_t n, int32_t *out,
+                                    uint64_t *count, void *ws, cudaStream_t s);
+
 // L2-streamed two-pass scan / compaction (wf_scan2p.cu), 16 B aligned buffers
 bool two_pass_usable(uint64_t n);
 cudaError_t launch_scan2p_i32(const int32_t *in, int32_t *out, uint64_t n,

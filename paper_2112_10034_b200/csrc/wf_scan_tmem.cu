@@ -1,0 +1,460 @@
+// wf_scan_tmem.cu — K3 scan / K4 compaction: warp-specialised single-pass
+// decoupled look-back with tiles PARKED IN TENSOR MEMORY while their prefix
+// resolves.
+//
+// Why: the smem-stage kernel of wf_scan.cu holds each 32 KiB stage from its
+// TMA load until the tile's prefix is known (~3 us after the latest
+// predecessor landed), so only a fraction of the stages is ever loading and
+// reads in flight cap at ~3 TB/s (profiles/r01_scan_compact_experiments.md).
+// A first TMEM version that parked one tile per CTA but aggregated the next
+// tile only after finishing the previous one measured slower (490 / 474 us):
+// every aggregate then waited behind a prefix (convoy).  Here every role has
+// its own warps and its own mbarrier pipeline, so a landed tile is reduced
+// and published at once whatever the state of older tiles:
+//
+//   producer warp    claims tile ids (ticket), TMA-loads them into a ring of
+//                    S smem stages (cp.async.bulk + mbarrier complete_tx)
+//   aggregator WG    warps 0-3: LDS the landed stage once (the x[j][k] layout
+//                    of the SDK shfl_scan), REDUX the tile value, tcgen05.st
+//                    the data into one of P TMEM slots (64 columns = 32 KiB)
+//                    and release the stage
+//   look-back warps  publish each tile aggregate and run the decoupled
+//                    look-back over the tile descriptors
+//   finisher warps   4-11, one per tile eighth: wait the prefix, tcgen05.ld it back,
+//                    scan (SHFL.UP) / compact (VOTE + POPC) it, store to HBM
+//                    (STG.128 for the scan) and release the TMEM slot
+//
+// Per SM (default: one CTA, S=6 stages, P=8 slots = all 512 TMEM columns,
+// 6 look-back warps): 6 stages loading + 8 parked tiles = 448 KiB of tiles on
+// chip, against 224 KiB for the smem-only kernel.
+//
+// Deadlock freedom: a CTA's tiles are claimed, aggregated, looked back and
+// finished in claim order; the smallest unfinished tile in the grid has all
+// predecessors finished, its CTA's older slots are free, so it progresses.
+//
+// Reference analog: as wf_scan.cu (corpus.py:347-364 warp-level scan; the
+// block/grid carries the reference needs several launches for,
+// runtime/hostdesc.py:109-129; compaction not expressible, dsl/lexer.py:18-25).
+#include "wf_device.cuh"
+#include "wf_internal.h"
+
+#include <cstdlib>
+
+#ifndef WF_TM_STAGES
+#define WF_TM_STAGES 6  // smem stages per CTA (32 KiB each)
+#endif
+#ifndef WF_TM_SLOTS
+#define WF_TM_SLOTS 8  // TMEM slots per CTA (64 columns each; power of two)
+#endif
+#ifndef WF_TM_NLB
+#define WF_TM_NLB 6  // look-back warps per CTA
+#endif
+#ifndef WF_TM_MINB
+#define WF_TM_MINB 1  // CTAs per SM the register budget must allow
+#endif
+#ifndef WF_LBK_TM
+#define WF_LBK_TM 1  // scan look-back predecessors per lane (window = 32 * K tiles)
+#endif
+#ifndef WF_LBK_COMPACT_TM
+#define WF_LBK_COMPACT_TM 2  // compaction look-back width
+#endif
+
+namespace wf {
+namespace {
+
+constexpr int S = WF_TM_STAGES;
+constexpr int P = WF_TM_SLOTS;
+constexpr int NLB = WF_TM_NLB;
+constexpr int W_FIN = 4;                  // aggregators: warps 0-3, finishers 4-11
+constexpr int NFIN = 8;                   // one finisher warp per tile eighth
+constexpr int W_LB = W_FIN + NFIN;        // look-back warps W_LB .. W_LB+NLB-1
+constexpr int W_PROD = W_LB + NLB;        // producer warp
+constexpr int TM_THREADS = (W_PROD + 1) * 32;
+constexpr int QVEC = 16;                  // 128-item chunks per warp-quarter of a tile
+constexpr uint32_t TM_TILE = 4u * QVEC * 128;  // 8192 items = 32 KiB
+constexpr uint32_t TM_COLS = uint32_t(P) * 64;
+constexpr uint32_t kNoTileTm = 0xffffffffu;
+static_assert((P & (P - 1)) == 0 && TM_COLS <= 512, "TMEM slots: power of two, <= 512 cols");
+static_assert(NLB >= 1 && NLB <= P, "look-back warps must not outnumber TMEM slots");
+
+// ---- TMEM helpers (tcgen05, cta_group::1) --------------------------------
+__device__ __forceinline__ void tmem_alloc(uint32_t *dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// 32 consecutive columns of this thread's TMEM lane <- / -> 32 registers
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
+      "%29, %30, %31, %32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),
+      "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
+      "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
+      "%29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+        "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+        "=r"(v[31])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// named barrier over the 128 aggregator threads (id 1; id 0 is __syncthreads)
+__device__ __forceinline__ void agg_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_arrive1(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+struct TmShared {
+  uint64_t full[S];    // producer -> aggregators: stage landed
+  uint64_t empty[S];   // aggregators -> producer: stage read (4 arrivals)
+  uint64_t parked[P];  // aggregators -> look-back + finishers: slot holds a tile
+  uint64_t freed[P];   // finishers -> aggregators: slot read back (NFIN arrivals)
+  uint64_t pref[P];    // look-back -> finishers: prefix known
+  uint32_t stage_tile[S];
+  uint32_t slot_tile[P];
+  uint32_t slot_agg[P];
+  uint32_t slot_prefix[P];
+  uint32_t slot_wtot[P][4][2];  // per tile quarter and half
+  uint32_t tmem_base;
+  uint32_t epoch;
+};
+
+template <bool COMPACT>
+__global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
+    tile_tmem_kernel(const int32_t *__restrict__ in, int32_t *__restrict__ out, uint64_t n,
+                     uint32_t ntiles, const int32_t *__restrict__ carry_in,
+                     uint64_t *__restrict__ count, uint64_t *__restrict__ desc,
+                     TileHeader *__restrict__ hdr) {
+  extern __shared__ __align__(128) uint8_t dyn_smem[];
+  __shared__ TmShared sh;
+  int32_t *stages = reinterpret_cast<int32_t *>(dyn_smem);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  if (warp == 0) tmem_alloc(&sh.tmem_base, TM_COLS);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&sh.full[s], 1);
+      mbar_init(&sh.empty[s], 4);
+    }
+    for (int p = 0; p < P; ++p) {
+      mbar_init(&sh.parked[p], 1);
+      mbar_init(&sh.freed[p], NFIN);
+      mbar_init(&sh.pref[p], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == W_PROD && lane == 0)
+    sh.epoch = ld_volatile_u32(&hdr->epoch) & kEpochMask;  // before this CTA's first (release) draw
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t epoch = sh.epoch;
+
+  if (warp == W_PROD) {
+    // ------------------------------ producer ------------------------------
+    // Tickets are drawn one stage ahead: the atomic's round trip overlaps the
+    // wait for the next free stage instead of serialising with it.
+    auto draw = [&](bool first) -> uint32_t {
+      uint32_t t = first ? atom_add_acq_rel_gpu(&hdr->ticket, 1u) : atom_add_relaxed_gpu(&hdr->ticket, 1u);
+      if (t >= ntiles) {
+        if (t == ntiles + gridDim.x - 1) {  // last of all draws: reset for the next launch
+          fence_acq_rel_gpu();
+          atomicExch(&hdr->ticket, 0u);
+          atomicExch(&hdr->epoch, (epoch + 1) & kEpochMask);
+        }
+        t = kNoTileTm;
+      }
+      return t;
+    };
+    uint32_t ahead = lane == 0 ? draw(true) : 0u;
+    for (uint32_t i = 0;; ++i) {
+      const int s = int(i % S);
+      const uint32_t k = i / S;
+      if (k > 0) mbar_wait(&sh.empty[s], (k - 1) & 1u);
+      uint32_t t = ahead;
+      if (lane == 0 && t != kNoTileTm) ahead = draw(false);
+      t = __shfl_sync(kFull, t, 0);
+      int32_t *stage = stages + s * TM_TILE;
+      const uint64_t tbase = uint64_t(t) * TM_TILE;
+      if (t != kNoTileTm && tbase + TM_TILE <= n) {
+        if (lane == 0) {
+          sh.stage_tile[s] = t;
+          mbar_arrive_expect_tx(&sh.full[s], TM_TILE * 4);
+          tma_load_1d(stage, in + tbase, TM_TILE * 4, &sh.full[s]);
+        }
+      } else {
+        if (t != kNoTileTm)  // ragged last tile: guarded copy, zero padding
+          for (uint32_t e = lane; e < TM_TILE; e += 32) stage[e] = tbase + e < n ? in[tbase + e] : 0;
+        __syncwarp();
+        if (lane == 0) {
+          sh.stage_tile[s] = t;
+          mbar_arrive1(&sh.full[s]);
+        }
+      }
+      if (t == kNoTileTm) break;
+    }
+  } else if (warp < W_FIN) {
+    // ----------------------------- aggregators ----------------------------
+    const uint32_t q = warp;  // tile quarter and TMEM lane quarter
+    const uint32_t tcol = sh.tmem_base + ((32u * q) << 16);
+    for (uint32_t i = 0;; ++i) {
+      const int s = int(i % S), p = int(i % P);
+      const uint32_t kp = i / P;
+      mbar_wait(&sh.full[s], (i / S) & 1u);
+      const uint32_t t = sh.stage_tile[s];
+      if (kp > 0) mbar_wait(&sh.freed[p], (kp - 1) & 1u);
+      tc_fence_after();
+      if (t == kNoTileTm) {
+        // one stop item per look-back warp (items i .. i+NLB-1); the finishers
+        // stop at the first.  Slot p is free (waited above); the next NLB-1
+        // slots held items that the finishers have completed or will complete.
+        for (uint32_t e = 0; e < uint32_t(NLB); ++e) {
+          const uint32_t ie = i + e;
+          const int pe = int(ie % P);
+          if (e > 0 && ie / P > 0) mbar_wait(&sh.freed[pe], (ie / P - 1) & 1u);
+          if (threadIdx.x == 0) {
+            sh.slot_tile[pe] = kNoTileTm;
+            mbar_arrive1(&sh.parked[pe]);
+          }
+        }
+        break;
+      }
+      const int32_t *stage = stages + s * TM_TILE + q * (QVEC * 128) + lane * 4;
+      uint32_t hsum[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t v[32], sum = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint4 x = *reinterpret_cast<const uint4 *>(stage + (8 * h + j) * 128);
+          v[4 * j] = x.x; v[4 * j + 1] = x.y; v[4 * j + 2] = x.z; v[4 * j + 3] = x.w;
+          if (COMPACT)
+            sum += (int32_t(x.x) > 0) + (int32_t(x.y) > 0) + (int32_t(x.z) > 0) + (int32_t(x.w) > 0);
+          else
+            sum += x.x + x.y + x.z + x.w;
+        }
+        tmem_st32(tcol + uint32_t(p) * 64u + 32u * h, v);
+        hsum[h] = sum;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive1(&sh.empty[s]);  // this warp is done with the stage
+      hsum[0] = __reduce_add_sync(kFull, hsum[0]);
+      hsum[1] = __reduce_add_sync(kFull, hsum[1]);
+      if (lane == 0) {
+        sh.slot_wtot[p][q][0] = hsum[0];
+        sh.slot_wtot[p][q][1] = hsum[1];
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      agg_sync();
+      if (threadIdx.x == 0) {
+        uint32_t a = 0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) a += sh.slot_wtot[p][w][0] + sh.slot_wtot[p][w][1];
+        sh.slot_tile[p] = t;
+        sh.slot_agg[p] = a;
+        mbar_arrive1(&sh.parked[p]);
+      }
+    }
+  } else if (warp < W_LB) {
+    // ------------------------------ finishers -----------------------------
+    // warp f handles tile eighth (q, h): TMEM lane quarter q = warp % 4 (the
+    // only lanes it may read), columns 32h..32h+31 of the slot
+    const uint32_t q = warp & 3u, h = (warp - W_FIN) >> 2;
+    const uint32_t tcol = sh.tmem_base + ((32u * q) << 16) + 32u * h;
+    const uint32_t lt = lanemask_lt();
+    for (uint32_t i = 0;; ++i) {
+      const int p = int(i % P);
+      const uint32_t kp = i / P;
+      mbar_wait(&sh.parked[p], kp & 1u);
+      const uint32_t t = sh.slot_tile[p];
+      if (t == kNoTileTm) break;
+      mbar_wait(&sh.pref[p], kp & 1u);
+      tc_fence_after();
+      const uint32_t prefix = sh.slot_prefix[p];
+      uint32_t wexcl = h ? sh.slot_wtot[p][q][0] : 0u;
+#pragma unroll
+      for (uint32_t w = 0; w < 4; ++w) wexcl += w < q ? sh.slot_wtot[p][w][0] + sh.slot_wtot[p][w][1] : 0u;
+      const uint32_t agg = sh.slot_agg[p];
+      const uint64_t base = uint64_t(t) * TM_TILE + q * (QVEC * 128) + h * (8 * 128) + lane * 4;
+      const bool full = uint64_t(t + 1) * TM_TILE <= n;
+      uint32_t carry = prefix + wexcl;
+      uint32_t v[32];
+      tmem_ld32(tcol + uint32_t(p) * 64u, v);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive1(&sh.freed[p]);  // slot data is in registers
+      if (!COMPACT) {
+        // the 8 chunk scans are independent until the carry: interleave them
+        uint32_t sc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          uint32_t *x = v + 4 * j;
+          x[1] += x[0];
+          x[2] += x[1];
+          x[3] += x[2];
+          sc[j] = x[3];
+        }
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t y = __shfl_up_sync(kFull, sc[j], d);
+            if (lane >= uint32_t(d)) sc[j] += y;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          uint32_t *x = v + 4 * j;
+          const uint32_t add = carry + sc[j] - x[3];
+          carry += __shfl_sync(kFull, sc[j], 31);
+          const uint64_t e = base + j * 128;
+          if (full) {
+            uint4 o;
+            o.x = x[0] + add; o.y = x[1] + add; o.z = x[2] + add; o.w = x[3] + add;
+            stg_stream(reinterpret_cast<uint4 *>(out + e), o);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (e + k < n) out[e + k] = int32_t(x[k] + add);
+          }
+        }
+      } else {
+        // ballot + popc positions; each lane stores its selected items
+        // (staging them in smem for 16-byte stores measured slower: 330 vs
+        // 290 us at 2^28)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t *x = v + 4 * j;
+          uint32_t excl = 0, tot = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t b = __ballot_sync(kFull, int32_t(x[k]) > 0);
+            excl += __popc(b & lt);
+            tot += __popc(b);
+          }
+          uint32_t pos = carry + excl;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (int32_t(x[k]) > 0) out[pos++] = int32_t(x[k]);
+          carry += tot;
+        }
+      }
+      if (COMPACT && t == ntiles - 1 && warp == W_FIN && lane == 0) *count = uint64_t(prefix) + agg;
+    }
+  } else {
+    // ----------------------------- look-back ------------------------------
+    const uint32_t me = warp - W_LB;
+    for (uint32_t i = me;; i += NLB) {
+      const int p = int(i % P);
+      const uint32_t kp = i / P;
+      mbar_wait(&sh.parked[p], kp & 1u);
+      const uint32_t t = sh.slot_tile[p];
+      if (t == kNoTileTm) break;
+      const uint32_t agg = sh.slot_agg[p];
+      uint32_t excl;
+      if (t == 0) {
+        excl = (!COMPACT && carry_in != nullptr) ? uint32_t(*carry_in) : 0u;
+        if (lane == 0) st_relaxed_gpu(desc, pack_desc(epoch, kStPrefix, excl + agg));
+      } else {
+        if (lane == 0)
+          st_relaxed_gpu(desc + uint64_t(t) * kDescStride, pack_desc(epoch, kStAggregate, agg));
+        excl = lookback_exclusive_wide<COMPACT ? WF_LBK_COMPACT_TM : WF_LBK_TM>(desc, t, epoch);
+        if (lane == 0)
+          st_relaxed_gpu(desc + uint64_t(t) * kDescStride, pack_desc(epoch, kStPrefix, excl + agg));
+      }
+      if (lane == 0) {
+        sh.slot_prefix[p] = excl;
+        mbar_arrive1(&sh.pref[p]);
+      }
+      __syncwarp();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(sh.tmem_base, TM_COLS);
+  }
+}
+
+template <bool COMPACT>
+constexpr size_t tm_smem() {
+  return size_t(S) * TM_TILE * 4;
+}
+
+template <bool COMPACT>
+int tmem_grid(uint32_t ntiles) {
+  static int per_sm[2] = {0, 0};
+  int &b = per_sm[COMPACT];
+  if (b == 0) {
+    cudaFuncSetAttribute(tile_tmem_kernel<COMPACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(tm_smem<COMPACT>()));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tile_tmem_kernel<COMPACT>, TM_THREADS,
+                                                  tm_smem<COMPACT>());
+    if (b > int(512 / TM_COLS)) b = int(512 / TM_COLS);  // TMEM: 512 columns per SM
+    if (b < 1) b = 1;
+  }
+  const uint32_t g = uint32_t(b) * uint32_t(sm_count(current_device()));
+  return int(ntiles < g ? ntiles : g);
+}
+
+}  // namespace
+
+bool tmem_scan_enabled() {
+  const char *e = getenv("WF_SCAN_TMEM");
+  return e == nullptr || e[0] != '0';
+}
+
+cudaError_t launch_scan_tmem_i32(const int32_t *in, int32_t *out, uint64_t n,
+                                 const int32_t *carry, void *ws, cudaStream_t s) {
+  auto *hdr = reinterpret_cast<TileHeader *>(ws);
+  auto *desc = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + kTileWsHeader);
+  const uint32_t nt = uint32_t((n + TM_TILE - 1) / TM_TILE);
+  tile_tmem_kernel<false><<<tmem_grid<false>(nt), TM_THREADS, tm_smem<false>(), s>>>(
+      in, out, n, nt, carry, nullptr, desc, hdr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compact_tmem_i32(const int32_t *in, uint64_t n, int32_t *out, uint64_t *count,
+                                    void *ws, cudaStream_t s) {
+  auto *hdr = reinterpret_cast<TileHeader *>(ws);
+  auto *desc = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + kTileWsHeader);
+  const uint32_t nt = uint32_t((n + TM_TILE - 1) / TM_TILE);
+  tile_tmem_kernel<true><<<tmem_grid<true>(nt), TM_THREADS, tm_smem<true>(), s>>>(
+      in, out, n, nt, nullptr, count, desc, hdr);
+  return cudaGetLastError();
+}
+
+}  // namespace wf
