@@ -18,8 +18,9 @@
 //                    of the SDK shfl_scan), REDUX the tile value, tcgen05.st
 //                    the data into one of P TMEM slots (64 columns = 32 KiB)
 //                    and release the stage
-//   look-back warps  publish each tile aggregate and run the decoupled
-//                    look-back over the tile descriptors
+//   look-back warps  run the decoupled look-back over the tile descriptors
+//                    (the aggregator publishes each aggregate itself, so a
+//                    look-back warp busy with an older tile never delays it)
 //   finisher warps   4-11, one per tile eighth: wait the prefix, tcgen05.ld it back,
 //                    scan (SHFL.UP) / compact (VOTE + POPC) it, store to HBM
 //                    (STG.128 for the scan) and release the TMEM slot
@@ -49,6 +50,9 @@
 #ifndef WF_TM_NLB
 #define WF_TM_NLB 6  // look-back warps per CTA
 #endif
+#ifndef WF_TM_NFG
+#define WF_TM_NFG 1  // finisher groups (8 warps each), taking tiles round-robin
+#endif
 #ifndef WF_TM_MINB
 #define WF_TM_MINB 1  // CTAs per SM the register budget must allow
 #endif
@@ -59,14 +63,32 @@
 #define WF_LBK_COMPACT_TM 2  // compaction look-back width
 #endif
 
+#ifndef WF_TM_TRACE
+#define WF_TM_TRACE 0
+#endif
+
 namespace wf {
+#if WF_TM_TRACE
+// per tile: [0] claimed+TMA issued  [1] aggregator start (landed, slot free)
+// [2] parked  [3] prefix known  [4] finisher done (warp W_FIN)
+__device__ unsigned long long *g_tm_trace = nullptr;
+__device__ __forceinline__ void tm_stamp(uint32_t tile, int k) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (g_tm_trace) g_tm_trace[uint64_t(tile) * 5 + k] = t;
+}
+#define TM_STAMP(tile, k) tm_stamp(tile, k)
+#else
+#define TM_STAMP(tile, k)
+#endif
 namespace {
 
 constexpr int S = WF_TM_STAGES;
 constexpr int P = WF_TM_SLOTS;
 constexpr int NLB = WF_TM_NLB;
 constexpr int W_FIN = 4;                  // aggregators: warps 0-3, finishers 4-11
-constexpr int NFIN = 8;                   // one finisher warp per tile eighth
+constexpr int NFG = WF_TM_NFG;
+constexpr int NFIN = 8 * NFG;             // per group: one finisher warp per tile eighth
 constexpr int W_LB = W_FIN + NFIN;        // look-back warps W_LB .. W_LB+NLB-1
 constexpr int W_PROD = W_LB + NLB;        // producer warp
 constexpr int TM_THREADS = (W_PROD + 1) * 32;
@@ -76,6 +98,7 @@ constexpr uint32_t TM_COLS = uint32_t(P) * 64;
 constexpr uint32_t kNoTileTm = 0xffffffffu;
 static_assert((P & (P - 1)) == 0 && TM_COLS <= 512, "TMEM slots: power of two, <= 512 cols");
 static_assert(NLB >= 1 && NLB <= P, "look-back warps must not outnumber TMEM slots");
+static_assert(NFG <= NLB, "every finisher group must see one of the NLB stop items");
 
 // ---- TMEM helpers (tcgen05, cta_group::1) --------------------------------
 __device__ __forceinline__ void tmem_alloc(uint32_t *dst_smem, uint32_t ncols) {
@@ -169,7 +192,7 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
     }
     for (int p = 0; p < P; ++p) {
       mbar_init(&sh.parked[p], 1);
-      mbar_init(&sh.freed[p], NFIN);
+      mbar_init(&sh.freed[p], 8);
       mbar_init(&sh.pref[p], 1);
     }
     fence_barrier_init();
@@ -210,6 +233,7 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       if (t != kNoTileTm && tbase + TM_TILE <= n) {
         if (lane == 0) {
           sh.stage_tile[s] = t;
+          TM_STAMP(t, 0);
           mbar_arrive_expect_tx(&sh.full[s], TM_TILE * 4);
           tma_load_1d(stage, in + tbase, TM_TILE * 4, &sh.full[s]);
         }
@@ -235,6 +259,7 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       const uint32_t t = sh.stage_tile[s];
       if (kp > 0) mbar_wait(&sh.freed[p], (kp - 1) & 1u);
       tc_fence_after();
+      if (threadIdx.x == 0 && t != kNoTileTm) TM_STAMP(t, 1);
       if (t == kNoTileTm) {
         // one stop item per look-back warp (items i .. i+NLB-1); the finishers
         // stop at the first.  Slot p is free (waited above); the next NLB-1
@@ -284,6 +309,15 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
         for (int w = 0; w < 4; ++w) a += sh.slot_wtot[p][w][0] + sh.slot_wtot[p][w][1];
         sh.slot_tile[p] = t;
         sh.slot_agg[p] = a;
+        // publish the aggregate right here, not in the look-back warp: a
+        // look-back warp busy with an older tile must never delay it
+        if (t == 0) {
+          const uint32_t c0 = (!COMPACT && carry_in != nullptr) ? uint32_t(*carry_in) : 0u;
+          st_relaxed_gpu(desc, pack_desc(epoch, kStPrefix, c0 + a));
+        } else {
+          st_relaxed_gpu(desc + uint64_t(t) * kDescStride, pack_desc(epoch, kStAggregate, a));
+        }
+        TM_STAMP(t, 2);
         mbar_arrive1(&sh.parked[p]);
       }
     }
@@ -291,10 +325,11 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
     // ------------------------------ finishers -----------------------------
     // warp f handles tile eighth (q, h): TMEM lane quarter q = warp % 4 (the
     // only lanes it may read), columns 32h..32h+31 of the slot
-    const uint32_t q = warp & 3u, h = (warp - W_FIN) >> 2;
+    const uint32_t q = warp & 3u, h = ((warp - W_FIN) >> 2) & 1u;
+    const uint32_t grp = (warp - W_FIN) >> 3;
     const uint32_t tcol = sh.tmem_base + ((32u * q) << 16) + 32u * h;
     const uint32_t lt = lanemask_lt();
-    for (uint32_t i = 0;; ++i) {
+    for (uint32_t i = grp;; i += NFG) {
       const int p = int(i % P);
       const uint32_t kp = i / P;
       mbar_wait(&sh.parked[p], kp & 1u);
@@ -371,7 +406,8 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
           carry += tot;
         }
       }
-      if (COMPACT && t == ntiles - 1 && warp == W_FIN && lane == 0) *count = uint64_t(prefix) + agg;
+      if (COMPACT && t == ntiles - 1 && q == 0 && h == 0 && lane == 0) *count = uint64_t(prefix) + agg;
+      if (q == 0 && h == 0 && lane == 0) TM_STAMP(t, 4);
     }
   } else {
     // ----------------------------- look-back ------------------------------
@@ -384,18 +420,16 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       if (t == kNoTileTm) break;
       const uint32_t agg = sh.slot_agg[p];
       uint32_t excl;
-      if (t == 0) {
+      if (t == 0) {  // its prefix descriptor was published by the aggregator
         excl = (!COMPACT && carry_in != nullptr) ? uint32_t(*carry_in) : 0u;
-        if (lane == 0) st_relaxed_gpu(desc, pack_desc(epoch, kStPrefix, excl + agg));
       } else {
-        if (lane == 0)
-          st_relaxed_gpu(desc + uint64_t(t) * kDescStride, pack_desc(epoch, kStAggregate, agg));
         excl = lookback_exclusive_wide<COMPACT ? WF_LBK_COMPACT_TM : WF_LBK_TM>(desc, t, epoch);
         if (lane == 0)
           st_relaxed_gpu(desc + uint64_t(t) * kDescStride, pack_desc(epoch, kStPrefix, excl + agg));
       }
       if (lane == 0) {
         sh.slot_prefix[p] = excl;
+        TM_STAMP(t, 3);
         mbar_arrive1(&sh.pref[p]);
       }
       __syncwarp();
@@ -431,6 +465,13 @@ int tmem_grid(uint32_t ntiles) {
 }
 
 }  // namespace
+
+#if WF_TM_TRACE
+extern "C" int wf_debug_set_trace_tm(void *buf) {
+  unsigned long long *p = static_cast<unsigned long long *>(buf);
+  return int(cudaMemcpyToSymbol(g_tm_trace, &p, sizeof(p)));
+}
+#endif
 
 bool tmem_scan_enabled() {
   const char *e = getenv("WF_SCAN_TMEM");

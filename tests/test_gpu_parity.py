@@ -223,6 +223,31 @@ def test_compact_full_config(ops):
     assert torch.equal(out[:m], want)
 
 
+# ---- K3/K4 smem-stage persistent kernel (WF_SCAN_TMEM=0 fallback) -----------
+
+@pytest.mark.parametrize("n", [1, 4097, 8192 * 5 + 3, (1 << 20) + 3, (1 << 22) + 13])
+def test_smem_stage_kernel_scan_compact(ops, monkeypatch, n):
+    """The pre-TMEM persistent kernel stays selectable (A/B baseline)."""
+    monkeypatch.setenv("WF_SCAN_TMEM", "0")
+    a = synthetic.generate("i32_full", n, seed=n + 9)
+    assert np.array_equal(host(ops.scan_inclusive_i32(dev(a))), no.scan_inclusive_i32(a))
+    out, cnt = ops.compact_gt0_i32(dev(a))
+    want = no.compact_gt0_i32(a)
+    assert int(host(cnt)[0]) == len(want) and np.array_equal(host(out)[:len(want)], want)
+
+
+def test_tmem_kernel_many_launches_interleaved(ops, monkeypatch):
+    """TMEM-parked kernel: epochs/tickets survive interleaving with the smem
+    kernel on one workspace, and sizes from one ragged tile to many tiles."""
+    for i, n in enumerate([8192 * 148 * 3 + 17, 5, 8192, 8193, 1 << 21, 77777]):
+        monkeypatch.setenv("WF_SCAN_TMEM", "0" if i % 3 == 2 else "1")
+        a = synthetic.generate("i32_select", n, seed=i, param=700)
+        assert np.array_equal(host(ops.scan_inclusive_i32(dev(a))), no.scan_inclusive_i32(a))
+        out, cnt = ops.compact_gt0_i32(dev(a))
+        want = no.compact_gt0_i32(a)
+        assert int(host(cnt)[0]) == len(want) and np.array_equal(host(out)[:len(want)], want)
+
+
 # ---- K3/K4 opt-in L2-streamed two-pass variant (wf_scan2p.cu) ---------------
 
 @pytest.fixture
