@@ -403,7 +403,17 @@ def per_kernel(args, rank, world, local, dev, peak) -> dict:
                           flush=lambda: flush_buf.fill_(1))
         res["c1_reduce_i32"] = stats(t, N_C1, 4, N_C1)
         res["c1_reduce_i32"]["l2"] = "flushed (256 MiB write) before every launch"
-        del x1, flush_buf
+        # latency context for this 4 MiB (0.6 us of HBM time) kernel, same
+        # flushed methodology: K1 on 4 elements (launch + one atomic) and the
+        # library reduction torch.sum of the same input
+        tiny = x1[:4]
+        t0 = time_launches(lambda: ops.reduce_sum_i32(tiny, block=256), steps, warm,
+                           flush=lambda: flush_buf.fill_(1))
+        tl = time_launches(lambda: torch.sum(x1), steps, warm, flush=lambda: flush_buf.fill_(1))
+        res["c1_reduce_i32"]["latency_context_us"] = {
+            "k1_on_4_elements": round(statistics.mean(t0) * 1e3, 2),
+            "torch_sum_same_input": round(statistics.mean(tl) * 1e3, 2)}
+        del x1, flush_buf, tiny
     # C3 scan
     lo, hi = wd.shard_range(N_C3, rank, world)
     x = ops.fill_synthetic("i32_full", hi - lo, seed=0, base=lo, device=dev)
