@@ -1,0 +1,97 @@
+"""The N>1 combine path on real kernels, one GPU.
+
+The GPU runs of this project are single-GPU, so NCCL with world_size > 1
+cannot run here.  These tests drive `paper_2112_10034_b200.distributed` as
+rank r of a world of W with the collective replaced by its exact result (the
+stacked per-rank values that an all-gather / all-reduce would deliver, computed
+by the same sm_100a kernels on the other ranks' shards).  What is under test
+is everything the product does around the collective on the device: the
+fixed-order fold of partials (bit-identical on every rank), the exclusive
+carry fed to the scan, the global compaction offsets and the bin sums —
+checked against the oracle over the whole (unsharded) input."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from oracle import numpy_oracle as no, synthetic  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def wd():
+    from paper_2112_10034_b200 import build
+    build.build_library()
+    from paper_2112_10034_b200 import distributed
+    torch.cuda.init()
+    return distributed
+
+
+def _as_rank(monkeypatch, wd, rank, world, gathered):
+    """Make `wd` believe it is rank `rank` of `world`; all-gathers return the
+    per-rank values in `gathered[dtype]`, all-reduces sum `gathered['bins']`."""
+    monkeypatch.setattr(wd, "_world", lambda group=None: (rank, world))
+
+    def exchange(local, group=None):
+        rows = gathered[local.dtype]
+        assert torch.equal(rows[rank].reshape(local.shape), local), "local value differs"
+        return torch.stack([r.reshape(local.shape) for r in rows])
+
+    def all_reduce(t, op=None, group=None):
+        t.copy_(torch.stack(gathered["bins"]).sum(0))
+
+    monkeypatch.setattr(wd, "exchange", exchange)
+    monkeypatch.setattr(wd.dist, "all_reduce", all_reduce)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_sharded_reductions_scan_compaction(wd, monkeypatch, world):
+    from paper_2112_10034_b200 import ops
+    n = 5 * 8192 * world + 4099  # ragged: the last shard is short
+    shards = [wd.shard_range(n, r, world) for r in range(world)]
+    xf = [ops.fill_synthetic("f32_unit", hi - lo, seed=4, base=lo) for lo, hi in shards]
+    xi = [ops.fill_synthetic("i32_full", hi - lo, seed=5, base=lo) for lo, hi in shards]
+    gathered = {
+        torch.float32: [ops.reduce_sum_f32(x) for x in xf],
+        torch.int32: [ops.reduce_sum_i32(x) for x in xi],
+        torch.int64: [ops.compact_gt0_i32(x)[1] for x in xi],
+    }
+    whole_i = synthetic.generate("i32_full", n, seed=5)
+    whole_f = synthetic.generate("f32_unit", n, seed=4)
+    f32_bits, i32_vals, scan_parts, comp_parts = set(), set(), [], []
+    for r in range(world):
+        _as_rank(monkeypatch, wd, r, world, gathered)
+        f32_bits.add(int(wd.reduce_sum_f32(xf[r]).view(torch.int32).item()))
+        i32_vals.add(int(wd.reduce_sum_i32(xi[r]).item()))
+        scan_parts.append(wd.scan_inclusive_i32(xi[r]).cpu().numpy())
+        out, cnt, off, tot = wd.compact_gt0_i32(xi[r])
+        m = int(cnt.item())
+        comp_parts.append((int(off.item()), out[:m].cpu().numpy(), int(tot.item())))
+    assert len(f32_bits) == 1, "fp32 fold must be bit-identical on every rank"
+    got = np.array([f32_bits.pop()], dtype=np.int32).view(np.float32)[0]
+    assert abs(float(got) - no.reduce_sum_f32_exact(whole_f)) <= no.f32_tolerance(n, no.abs_sum(whole_f))
+    assert i32_vals == {int(no.reduce_sum_i32(whole_i))}
+    assert np.array_equal(np.concatenate(scan_parts), no.scan_inclusive_i32(whole_i))
+    want = no.compact_gt0_i32(whole_i)
+    pos = 0
+    for off, part, tot in comp_parts:
+        assert off == pos and tot == len(want)
+        assert np.array_equal(part, want[pos:pos + len(part)])
+        pos += len(part)
+    assert pos == len(want)
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_sharded_histogram(wd, monkeypatch, world):
+    from paper_2112_10034_b200 import ops
+    n = 3 * 4096 * world + 77
+    shards = [wd.shard_range(n, r, world) for r in range(world)]
+    xs = [ops.fill_synthetic("u8_uniform", hi - lo, seed=6, base=lo) for lo, hi in shards]
+    gathered = {"bins": [ops.histogram256_u8(x).clone() for x in xs]}
+    want = no.histogram256_u8(synthetic.generate("u8_uniform", n, seed=6))
+    for r in range(world):
+        _as_rank(monkeypatch, wd, r, world, gathered)
+        got = wd.histogram256_u8(xs[r]).cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, want)

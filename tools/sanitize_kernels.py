@@ -1,0 +1,25 @@
+"""Small invocation of every hot-path kernel for compute-sanitizer
+(memcheck / racecheck / synccheck):  compute-sanitizer --tool racecheck
+python tools/sanitize_kernels.py"""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2112_10034_b200 import ops  # noqa: E402
+
+torch.cuda.set_device(0)
+n = 8192 * 300 + 123  # > one persistent wave of tiles, ragged tail
+x = ops.fill_synthetic("i32_full", n, seed=1)
+f = ops.fill_synthetic("f32_unit", n, seed=2)
+u = ops.fill_synthetic("u8_uniform", 4 * n + 5, seed=3)
+r = [ops.reduce_sum_i32(x), ops.reduce_sum_f32(f), ops.scan_inclusive_i32(x),
+     ops.compact_gt0_i32(x)[1], ops.histogram256_u8(u),
+     ops.scan_inclusive_i32(x[1:]), ops.compact_gt0_i32(x[3:])[1]]
+a = torch.arange(96, dtype=torch.int32, device="cuda")
+for kind in ("shfl_down", "shfl_up", "shfl_xor", "shfl_idx", "vote_all", "vote_any", "ballot", "reduce_add"):
+    r.append(ops.warp_collective(kind, a, operand=3, block=96))
+torch.cuda.synchronize()
+print("ok", [int(t.reshape(-1)[0].item()) if t.dtype != torch.float32 else float(t[0]) for t in r[:5]])
