@@ -201,7 +201,10 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0) out[0] = s;
 }
 
-constexpr int kUnroll = 4;
+#ifndef WF_RED_UNROLL
+#define WF_RED_UNROLL 4  // 16-byte loads in flight per thread
+#endif
+constexpr int kUnroll = WF_RED_UNROLL;
 
 template <class Op, int BLOCK>
 cudaError_t launch_block(const typename Op::elem_t *in, uint64_t n,

@@ -95,3 +95,32 @@ def test_sharded_histogram(wd, monkeypatch, world):
         _as_rank(monkeypatch, wd, r, world, gathered)
         got = wd.histogram256_u8(xs[r]).cpu().numpy().view(np.uint64)
         assert np.array_equal(got, want)
+
+
+@pytest.mark.slow
+def test_bench_n2_path_simulated(wd, monkeypatch):
+    """bench.py's N>1 code path (rank 0 of 2) end to end on one GPU: the
+    collectives return what a peer holding identical values would deliver.
+    Catches host-side errors in the sharded bench legs the driver's scaling
+    run would take; the numbers are not a measurement."""
+    import argparse
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+    import torch.distributed as dist
+
+    monkeypatch.setattr(wd, "_world", lambda group=None: (0, 2))
+    monkeypatch.setattr(wd, "exchange", lambda local, group=None:
+                        torch.stack([local.reshape(local.shape)] * 2))
+    monkeypatch.setattr(dist, "barrier", lambda *a, **k: None)
+    monkeypatch.setattr(dist, "all_reduce", lambda t, *a, **k: t)
+    args = argparse.Namespace(gpus=2, steps=3, warmup=3, impl="ours", headline_only=False,
+                              no_cpu_baseline=True, cpu_budget=1.0)
+    line = bench.run_ours(args, 0, 2, 0)
+    assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "shard2"
+    assert line["gpu_launches"] == 2 * args.steps  # K2 + fold per step
+    per = line["per_kernel"]
+    assert per["c3_scan_i32"]["bytes_per_elem"] == 12  # reduce-then-scan across GPUs
+    for k in ("c1_reduce_i32", "c3_scan_i32", "c4_compact_i32", "c5_hist_u8"):
+        assert per[k]["gelem_s"] > 0
