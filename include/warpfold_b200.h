@@ -117,6 +117,32 @@ int wf_fold_i32(const int32_t *vals, uint32_t count, int32_t *out,
 int wf_fold_u64(const uint64_t *vals, uint32_t count, uint64_t *out,
                 wf_stream_t stream);
 
+/* ---- multi-GPU: fused reduce + exchange over peer memory --------------
+ * Replaces, for the sharded C2 reduction, the all-gather of per-rank partials
+ * plus wf_fold_f32 (the reference's only parallelism is the
+ * block-range split of runtime/launch.py:137-147) with ONE kernel per rank:
+ * its last block stores the rank partial straight into every rank's mailbox
+ * (CUDA IPC mappings over NVLink / NVSwitch), waits for all ranks' partials in
+ * its own mailbox and folds them with wf_fold_f32's association, so out[0] is
+ * bit-identical on every rank and to the NCCL path.
+ *   mailbox:   wf_mailbox_bytes(world) bytes of device memory per rank
+ *              (wf_mailbox_alloc: cudaMalloc + zero), exported with
+ *              wf_ipc_handle (64-byte cudaIpcMemHandle) and mapped by the other
+ *              ranks with wf_ipc_open.
+ *   d_peers:   device array of `world` mailbox pointers (rank order).
+ *   epoch:     1, 2, 3, ... — the same sequence on every rank, one per call.
+ * A rank whose peers do not arrive within ~4 s writes NaN to out[0]. */
+size_t wf_mailbox_bytes(int world);
+int wf_mailbox_alloc(int world, void **d_mailbox);
+int wf_mailbox_free(void *d_mailbox);
+int wf_ipc_handle(void *d_ptr, void *handle64);
+int wf_ipc_open(const void *handle64, void **d_ptr);
+int wf_ipc_close(void *d_ptr);
+int wf_reduce_sum_f32_mg(const float *in, uint64_t n, float *out, int block,
+                         int grid, void *ws, size_t ws_bytes,
+                         void *const *d_peers, const void *d_mailbox, int rank,
+                         int world, uint32_t epoch, wf_stream_t stream);
+
 /* ---- K3: shfl_scan inclusive prefix sum --------------------------------
  * out[i] = carry + in[0] + ... + in[i] (wrapping), single pass with
  * decoupled look-back.  d_carry_in: device int32 (NULL = 0), used by the

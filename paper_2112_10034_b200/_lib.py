@@ -50,6 +50,14 @@ SIGNATURES = {
     "wf_reduce_sum_i32": (C.c_int, [_vp, _u64, _vp, C.c_int, C.c_int, _vp, _sz, _vp]),
     "wf_reduce_sum_f32": (C.c_int, [_vp, _u64, _vp, C.c_int, C.c_int, _vp, _sz, _vp]),
     "wf_fold_f32": (C.c_int, [_vp, _u32, _vp, _vp]),
+    "wf_mailbox_bytes": (_sz, [C.c_int]),
+    "wf_mailbox_alloc": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+    "wf_mailbox_free": (C.c_int, [_vp]),
+    "wf_ipc_handle": (C.c_int, [_vp, _vp]),
+    "wf_ipc_open": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "wf_ipc_close": (C.c_int, [_vp]),
+    "wf_reduce_sum_f32_mg": (C.c_int, [_vp, _u64, _vp, C.c_int, C.c_int, _vp, _sz, _vp, _vp,
+                                       C.c_int, C.c_int, _u32, _vp]),
     "wf_fold_i32": (C.c_int, [_vp, _u32, _vp, _vp]),
     "wf_fold_u64": (C.c_int, [_vp, _u32, _vp, _vp]),
     "wf_scan_inclusive_i32": (C.c_int, [_vp, _vp, _u64, _vp, _vp, _sz, _vp]),

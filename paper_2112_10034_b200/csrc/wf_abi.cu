@@ -211,6 +211,56 @@ int wf_reduce_sum_f32(const float *in, uint64_t n, float *out, int block, int gr
                      "reduce_sum_f32");
 }
 
+size_t wf_mailbox_bytes(int world) {
+  return world < 1 ? 0 : (size_t(2) * size_t(world) * 8 + 255) & ~size_t(255);
+}
+
+int wf_mailbox_alloc(int world, void **d_mailbox) {
+  if (d_mailbox == nullptr || world < 1 || world > 32)
+    return fail(WF_ERR_ARG, "mailbox: world must be in [1, 32]");
+  const size_t b = wf_mailbox_bytes(world);
+  int rc = cuda_status(cudaMalloc(d_mailbox, b), "mailbox alloc");
+  if (rc) return rc;
+  return cuda_status(cudaMemset(*d_mailbox, 0, b), "mailbox zero");
+}
+
+int wf_mailbox_free(void *d_mailbox) { return cuda_status(cudaFree(d_mailbox), "mailbox free"); }
+
+int wf_ipc_handle(void *d_ptr, void *handle64) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  if (d_ptr == nullptr || handle64 == nullptr) return fail(WF_ERR_ARG, "NULL pointer");
+  cudaIpcMemHandle_t h;
+  int rc = cuda_status(cudaIpcGetMemHandle(&h, d_ptr), "cudaIpcGetMemHandle");
+  if (rc) return rc;
+  memcpy(handle64, &h, sizeof h);
+  return WF_OK;
+}
+
+int wf_ipc_open(const void *handle64, void **d_ptr) {
+  if (d_ptr == nullptr || handle64 == nullptr) return fail(WF_ERR_ARG, "NULL pointer");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof h);
+  return cuda_status(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess),
+                     "cudaIpcOpenMemHandle");
+}
+
+int wf_ipc_close(void *d_ptr) { return cuda_status(cudaIpcCloseMemHandle(d_ptr), "cudaIpcCloseMemHandle"); }
+
+int wf_reduce_sum_f32_mg(const float *in, uint64_t n, float *out, int block, int grid, void *ws,
+                         size_t ws_bytes, void *const *d_peers, const void *d_mailbox, int rank,
+                         int world, uint32_t epoch, wf_stream_t stream) {
+  int rc = reduce_common(WF_OP_REDUCE_SUM_F32, in, n, out, block, grid, ws, ws_bytes);
+  if (rc) return rc;
+  if (d_peers == nullptr || d_mailbox == nullptr) return fail(WF_ERR_ARG, "NULL mailbox pointer");
+  if (world < 1 || world > 32 || rank < 0 || rank >= world)
+    return fail(WF_ERR_ARG, "rank %d / world %d out of range (world <= 32)", rank, world);
+  if (epoch == 0) return fail(WF_ERR_ARG, "epoch must start at 1");
+  if (grid == 0) grid = auto_reduce_grid(true, block, n);
+  return cuda_status(launch_reduce_f32_mg(in, n, out, block, grid, ws, d_peers, d_mailbox, rank,
+                                          world, epoch, static_cast<cudaStream_t>(stream)),
+                     "reduce_sum_f32_mg");
+}
+
 int wf_fold_f32(const float *vals, uint32_t count, float *out, wf_stream_t stream) {
   if (out == nullptr || (count && vals == nullptr)) return fail(WF_ERR_ARG, "NULL pointer");
   return cuda_status(launch_fold_f32(vals, count, out, static_cast<cudaStream_t>(stream)), "fold_f32");

@@ -39,6 +39,9 @@ cudaError_t launch_reduce_i32(const int32_t *in, uint64_t n, int32_t *out,
 cudaError_t launch_reduce_f32(const float *in, uint64_t n, float *out,
                               int block, int grid, void *ws, cudaStream_t s);
 int auto_reduce_grid(bool is_f32, int block, uint64_t n);
+cudaError_t launch_reduce_f32_mg(const float *in, uint64_t n, float *out, int block, int grid,
+                                 void *ws, void *const *peers, const void *mine, int rank,
+                                 int world, uint32_t epoch, cudaStream_t s);
 cudaError_t launch_fold_f32(const float *v, uint32_t count, float *out,
                             cudaStream_t s);
 cudaError_t launch_fold_i32(const int32_t *v, uint32_t count, int32_t *out,

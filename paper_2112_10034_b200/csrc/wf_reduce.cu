@@ -74,12 +74,37 @@ __device__ __forceinline__ typename Op::acc_t block_sum(typename Op::acc_t v) {
   return r;         // valid in warp 0
 }
 
-template <class Op, int BLOCK, int UNROLL>
+// Multi-GPU fused exchange (wf_reduce_sum_f32_mg): the last block of every
+// rank writes its rank partial, tagged with the call's epoch, into slot
+// [epoch & 1][rank] of EVERY rank's mailbox over peer memory (NVLink, CUDA IPC
+// mappings), then waits for all ranks' slots in its own mailbox and folds them
+// with the association of fold_kernel (so the result is bit-identical to the
+// NCCL all-gather + wf_fold_f32 path, and identical on every rank).  Two banks
+// by epoch parity: a rank can be at most one call ahead of a peer (it needs
+// the peer's slot of the current call to finish it), so it never overwrites a
+// slot the peer has not read yet.
+struct MgArgs {
+  unsigned long long *const *peers;  // [world] mailbox of each rank (device array)
+  const unsigned long long *mine;    // this rank's mailbox
+  int rank, world;
+  uint32_t epoch;
+};
+
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <class Op, int BLOCK, int UNROLL, bool MG = false>
 __global__ void __launch_bounds__(BLOCK)
     reduce_kernel(const typename Op::elem_t *__restrict__ in, uint64_t n,
                   typename Op::elem_t *__restrict__ out,
                   typename Op::acc_t *__restrict__ partials,
-                  uint32_t *__restrict__ ticket) {
+                  uint32_t *__restrict__ ticket, MgArgs mg = MgArgs{}) {
   using acc_t = typename Op::acc_t;
   using elem_t = typename Op::elem_t;
   const uint64_t gtid = uint64_t(blockIdx.x) * BLOCK + threadIdx.x;
@@ -168,6 +193,36 @@ __global__ void __launch_bounds__(BLOCK)
     f = Op::add(f, __ldcg(partials + j));
   }
   f = block_sum<Op, BLOCK>(f);
+  if constexpr (MG) {
+    __shared__ acc_t s_part;
+    if (threadIdx.x == 0) {
+      s_part = f;
+      *ticket = 0u;
+    }
+    __syncthreads();
+    const uint32_t bank = mg.epoch & 1u;
+    const unsigned long long tag = (unsigned long long)mg.epoch << 32;
+    if (int(threadIdx.x) < mg.world)  // one peer store per thread, all in flight at once
+      st_relaxed_sys(mg.peers[threadIdx.x] + bank * mg.world + mg.rank, tag | Op::bits(s_part));
+    acc_t v = Op::zero();
+    if (int(threadIdx.x) < mg.world) {
+      const unsigned long long *slot = mg.mine + bank * mg.world + threadIdx.x;
+      unsigned long long w = ld_relaxed_sys(slot);
+      uint32_t spins = 0;
+      while (uint32_t(w >> 32) != mg.epoch) {
+        if (++spins > (1u << 25)) {  // ~4 s: a peer never arrived
+          w = tag | 0x7fc00000u;     // NaN marks the failure to the host
+          break;
+        }
+        __nanosleep(128);
+        w = ld_relaxed_sys(slot);
+      }
+      v = Op::add(Op::zero(), Op::from_bits(uint32_t(w)));
+    }
+    v = block_sum<Op, BLOCK>(v);  // fold_kernel's association for world <= 32
+    if (threadIdx.x == 0) out[0] = Op::to_elem(v);
+    return;
+  }
   if (threadIdx.x == 0) {
     out[0] = Op::to_elem(f);
     *ticket = 0u;
@@ -249,7 +304,35 @@ int resident_blocks(int block) {
   }
 }
 
+template <int BLOCK>
+cudaError_t launch_mg_block(const float *in, uint64_t n, float *out, int grid, void *ws,
+                            const MgArgs &mg, cudaStream_t s) {
+  auto *ticket = reinterpret_cast<uint32_t *>(ws);
+  auto *partials = reinterpret_cast<float *>(static_cast<char *>(ws) + kWsHeader);
+  reduce_kernel<SumF32, BLOCK, kUnroll, true><<<grid, BLOCK, 0, s>>>(in, n, out, partials,
+                                                                     ticket, mg);
+  return cudaGetLastError();
+}
+
 }  // namespace
+
+cudaError_t launch_reduce_f32_mg(const float *in, uint64_t n, float *out, int block, int grid,
+                                 void *ws, void *const *peers, const void *mine, int rank,
+                                 int world, uint32_t epoch, cudaStream_t s) {
+  MgArgs mg;
+  mg.peers = reinterpret_cast<unsigned long long *const *>(peers);
+  mg.mine = static_cast<const unsigned long long *>(mine);
+  mg.rank = rank;
+  mg.world = world;
+  mg.epoch = epoch;
+  switch (block) {
+    case 128: return launch_mg_block<128>(in, n, out, grid, ws, mg, s);
+    case 256: return launch_mg_block<256>(in, n, out, grid, ws, mg, s);
+    case 512: return launch_mg_block<512>(in, n, out, grid, ws, mg, s);
+    case 1024: return launch_mg_block<1024>(in, n, out, grid, ws, mg, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 int auto_reduce_grid(bool is_f32, int block, uint64_t n) {
   static int cache[2][11] = {};

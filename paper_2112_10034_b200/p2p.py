@@ -1,0 +1,158 @@
+"""Fused reduce + exchange over peer memory (NVLink 5 / NVSwitch) for the
+sharded fp32 reduction (BASELINE config 2).
+
+The NCCL path of ``distributed.reduce_sum_f32`` is three stream operations per
+step: the K2 kernel, an all-gather of one float per rank and the fixed-order
+fold kernel.  ``PeerReducer`` makes it ONE kernel per rank
+(``wf_reduce_sum_f32_mg``): the kernel's last block stores the rank partial
+straight into every rank's mailbox through CUDA IPC mappings and folds the
+arriving partials with the same association as ``wf_fold_f32`` — so the result
+is bit-identical to the NCCL path and on every rank.  Mailbox handles are
+exchanged once, at construction, through ``torch.distributed``.
+
+Reference anchor: the reference's only parallelism is the block-range split
+over CPU workers with join semantics (runtime/launch.py:95-147); SURVEY.md §8e
+maps C2 to "independent units + one exchange".
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+import torch.distributed as dist
+
+from . import _lib, ops
+from .errors import LaunchError
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise LaunchError(f"{what}: {_lib.last_error()}")
+
+
+class Mailboxes:
+    """`world` mailboxes and the device array of their pointers, as seen by
+    one rank.  Built either across processes (``from_process_group``) or
+    inside one process for tests (``local``: all mailboxes on this device)."""
+
+    def __init__(self, own: int, ptrs: list[int], opened: list[int], device: torch.device,
+                 owned: list[int]):
+        self.own = own
+        self.ptrs = ptrs
+        self.peers = torch.tensor(ptrs, dtype=torch.int64, device=device)
+        self._opened = opened
+        self._owned = owned
+
+    @classmethod
+    def from_process_group(cls, device: torch.device, group=None) -> "Mailboxes":
+        """Collective: every rank of `group` must call it.  Failures on any
+        rank (no IPC, no peer access) make every rank raise, after the same
+        sequence of collectives, so no rank is left waiting in one."""
+        lib = _lib.load()
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        mine, handle, err = C.c_void_p(), (C.c_char * 64)(), None
+        try:
+            _check(lib.wf_mailbox_alloc(world, C.byref(mine)), "wf_mailbox_alloc")
+            _check(lib.wf_ipc_handle(mine, handle), "wf_ipc_handle")
+        except LaunchError as e:
+            err = str(e)
+        handles: list = [None] * world
+        dist.all_gather_object(handles, None if err else bytes(handle), group=group)
+        ptrs, opened = [], []
+        if err is None:
+            try:
+                for r, h in enumerate(handles):
+                    if r == rank:
+                        ptrs.append(mine.value)
+                        continue
+                    if h is None:
+                        raise LaunchError(f"rank {r} could not export its mailbox")
+                    p = C.c_void_p()
+                    _check(lib.wf_ipc_open(C.create_string_buffer(h, 64), C.byref(p)), "wf_ipc_open")
+                    ptrs.append(p.value)
+                    opened.append(p.value)
+            except LaunchError as e:
+                err = str(e)
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        box = cls(mine.value, ptrs if not err else [0] * world, opened, device,
+                  [mine.value] if mine.value else [])
+        if int(ok.item()) != 1:
+            box.close()
+            raise LaunchError(err or "a peer rank could not set up its mailbox")
+        return box
+
+    @classmethod
+    def local(cls, world: int, device: torch.device) -> list["Mailboxes"]:
+        """In-process stand-in for `world` ranks on one GPU (tests): every
+        rank's view shares the same pointer array."""
+        lib = _lib.load()
+        own = []
+        for _ in range(world):
+            p = C.c_void_p()
+            _check(lib.wf_mailbox_alloc(world, C.byref(p)), "wf_mailbox_alloc")
+            own.append(p.value)
+        views = [cls(own[r], own, [], device, []) for r in range(world)]
+        views[0]._owned = own  # freed once
+        return views
+
+    def close(self) -> None:
+        lib = _lib.load()
+        for p in self._opened:
+            lib.wf_ipc_close(C.c_void_p(p))
+        for p in self._owned:
+            lib.wf_mailbox_free(C.c_void_p(p))
+        self._opened, self._owned = [], []
+
+
+class PeerReducer:
+    """`reduce_sum_f32` of the sharded input, exchanged over peer memory."""
+
+    def __init__(self, boxes: Mailboxes, rank: int, world: int):
+        self.boxes, self.rank, self.world = boxes, rank, world
+        self.epoch = 0
+
+    @classmethod
+    def for_process_group(cls, device: torch.device, group=None) -> "PeerReducer":
+        boxes = Mailboxes.from_process_group(device, group)
+        return cls(boxes, dist.get_rank(group), dist.get_world_size(group))
+
+    def reduce_sum_f32(self, x_local: torch.Tensor, out: torch.Tensor | None = None,
+                       block: int = 256, stream=None) -> torch.Tensor:
+        ops._require_cuda(x_local, torch.float32, "x")
+        if out is None:
+            out = torch.empty(1, dtype=torch.float32, device=x_local.device)
+        self.epoch += 1
+        ws = ops.workspace(_lib.OP_REDUCE_SUM_F32, x_local.numel(), x_local.device, stream)
+        lib = _lib.load()
+        _check(lib.wf_reduce_sum_f32_mg(x_local.data_ptr(), x_local.numel(), out.data_ptr(),
+                                        block, 0, ws.data_ptr(), ws.numel(),
+                                        self.boxes.peers.data_ptr(), self.boxes.own,
+                                        self.rank, self.world, self.epoch,
+                                        ops._stream_handle(stream)),
+               "wf_reduce_sum_f32_mg")
+        return out
+
+    def close(self) -> None:
+        self.boxes.close()
+
+
+def try_peer_reducer(device: torch.device, x_probe: torch.Tensor, group=None):
+    """Collective.  Build a PeerReducer and check it bit-for-bit against the
+    NCCL path on `x_probe` (this rank's shard of a probe input).  Returns
+    (reducer, "ok") or (None, reason) — the same outcome on every rank."""
+    from . import distributed as wd
+    try:
+        pr = PeerReducer.for_process_group(device, group)
+    except Exception as e:  # identical on all ranks (consensus inside)
+        return None, f"{type(e).__name__}: {e}"
+    want = wd.reduce_sum_f32(x_probe, group=group)
+    got = pr.reduce_sum_f32(x_probe)
+    same = torch.equal(got.view(torch.int32), want.view(torch.int32))
+    ok = torch.tensor([1 if same else 0], dtype=torch.int32, device=device)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+    if int(ok.item()) != 1:
+        pr.close()
+        return None, "peer-memory result differs from the NCCL path"
+    return pr, "ok"

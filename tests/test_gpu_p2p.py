@@ -1,0 +1,153 @@
+"""Fused reduce + exchange over peer memory (wf_reduce_sum_f32_mg,
+paper_2112_10034_b200/p2p.py).
+
+Multi-GPU boxes are not available to these tests, so the protocol runs with
+`world` ranks inside one process on one GPU: every rank's kernel on its own
+stream, all mailboxes in this device's memory.  The kernels really run
+concurrently and really wait for each other, so epochs, bank alternation,
+late ranks and the fold association are exercised; the result must be
+bit-identical on every rank and to the NCCL path (per-rank K2 partials ->
+all-gather -> wf_fold_f32).  A second test maps a mailbox into another
+process through the CUDA IPC handle path the multi-process code uses."""
+
+import multiprocessing as mp
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from oracle import numpy_oracle as no, synthetic  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def mods():
+    from paper_2112_10034_b200 import build
+    build.build_library()
+    from paper_2112_10034_b200 import distributed, ops, p2p
+    torch.cuda.init()
+    return ops, p2p, distributed
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_fused_exchange_in_process(mods, world):
+    ops, p2p, wd = mods
+    dev = torch.device("cuda", 0)
+    n = (1 << 22) * world + 1234
+    shards = [wd.shard_range(n, r, world) for r in range(world)]
+    xs = [ops.fill_synthetic("f32_unit", hi - lo, seed=9, base=lo) for lo, hi in shards]
+    want = ops.fold(torch.cat([ops.reduce_sum_f32(x) for x in xs]))  # the NCCL path's combine
+    whole = synthetic.generate("f32_unit", n, seed=9)
+    assert abs(float(want.item()) - no.reduce_sum_f32_exact(whole)) <= no.f32_tolerance(n, no.abs_sum(whole))
+    boxes = p2p.Mailboxes.local(world, dev)
+    reducers = [p2p.PeerReducer(boxes[r], r, world) for r in range(world)]
+    streams = [torch.cuda.Stream(dev) for _ in range(world)]
+    torch.cuda.synchronize()
+    try:
+        for step in range(5):
+            order = range(world) if step % 2 == 0 else reversed(range(world))
+            outs = [None] * world
+            for r in order:  # odd steps launch the last rank first
+                with torch.cuda.stream(streams[r]):
+                    outs[r] = reducers[r].reduce_sum_f32(xs[r], stream=streams[r])
+            torch.cuda.synchronize()
+            for r in range(world):
+                assert torch.equal(outs[r].view(torch.int32), want.view(torch.int32)), (step, r)
+    finally:
+        torch.cuda.synchronize()
+        boxes[0].close()
+
+
+def _child_read_mailbox(handle: bytes, world: int, q) -> None:
+    import ctypes as C
+    import torch as T
+    from paper_2112_10034_b200 import _lib
+    T.cuda.set_device(0)
+    lib = _lib.load()
+    p = C.c_void_p()
+    rc = lib.wf_ipc_open(C.create_string_buffer(handle, 64), C.byref(p))
+    if rc != 0:
+        q.put(("error", _lib.last_error()))
+        return
+    out = T.zeros(1, dtype=T.int64, device="cuda")
+    rc = lib.wf_fold_u64(p, 2 * world, out.data_ptr(), None)
+    T.cuda.synchronize()
+    q.put(("ok", int(out.item())) if rc == 0 else ("error", _lib.last_error()))
+    lib.wf_ipc_close(p)
+
+
+def test_mailbox_ipc_mapping_across_processes(mods):
+    """The parent writes a pattern into its mailbox; a spawned process maps
+    it with wf_ipc_open (the multi-process path of Mailboxes) and reads it
+    back with a kernel."""
+    import ctypes as C
+    from paper_2112_10034_b200 import _lib
+    lib = _lib.load()
+    world = 4
+    box = C.c_void_p()
+    assert lib.wf_mailbox_alloc(world, C.byref(box)) == 0
+    try:
+        vals = torch.arange(1, 2 * world + 1, dtype=torch.int64, device="cuda") * 1000003
+        for i in range(2 * world):  # one-element folds = device copies into the slots
+            assert lib.wf_fold_u64(C.c_void_p(vals.data_ptr() + 8 * i), 1,
+                                   C.c_void_p(box.value + 8 * i), None) == 0
+        torch.cuda.synchronize()
+        handle = (C.c_char * 64)()
+        assert lib.wf_ipc_handle(box, handle) == 0, _lib.last_error()
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        proc = ctx.Process(target=_child_read_mailbox, args=(bytes(handle), world, q))
+        proc.start()
+        status, value = q.get(timeout=180)
+        proc.join(timeout=60)
+        assert status == "ok", value
+        assert value == int(vals.sum().item())
+    finally:
+        lib.wf_mailbox_free(box)
+
+
+def _rank_main(rank: int, world: int, port: int, n: int, q) -> None:
+    import os
+    import torch as T
+    import torch.distributed as D
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    T.cuda.set_device(0)
+    D.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2112_10034_b200 import distributed as wd, ops, p2p
+        dev = T.device("cuda", 0)
+        shards = [wd.shard_range(n, r, world) for r in range(world)]
+        xs = [ops.fill_synthetic("f32_unit", hi - lo, seed=11, base=lo, device=dev)
+              for lo, hi in shards]
+        want = ops.fold(T.cat([ops.reduce_sum_f32(x) for x in xs]))  # NCCL-path combine, locally
+        pr = p2p.PeerReducer.for_process_group(dev)
+        got = [pr.reduce_sum_f32(xs[rank]).clone() for _ in range(3)]
+        T.cuda.synchronize()
+        q.put((rank, [bool(T.equal(g.view(T.int32), want.view(T.int32))) for g in got]))
+        D.barrier()
+        pr.close()
+    except Exception as e:  # reported to the parent
+        q.put((rank, f"{type(e).__name__}: {e}"))
+    finally:
+        D.destroy_process_group()
+
+
+def test_peer_reducer_two_processes_one_gpu(mods):
+    """The real multi-process path (mailbox export, IPC open, consensus,
+    fused kernel) with two ranks sharing one GPU: their kernels time-slice
+    rather than run concurrently, so each waits for the other's context —
+    slow, but the protocol and the result are the multi-GPU ones."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, (1 << 20) + 33, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res[0] == [True] * 3 and res[1] == [True] * 3, res
