@@ -26,7 +26,10 @@ constexpr uint32_t kMaxReduceGrid = 8192;   // partial slots for reductions
 constexpr int kScanBlock = 256;             // threads per scan/compact tile
 constexpr int kScanVec = 4;                 // int4 loads per thread per tile
 constexpr uint64_t kScanTile = uint64_t(kScanBlock) * kScanVec * 4;  // 4096
-constexpr int kHistBlock = 1024;
+#ifndef WF_HIST_BLOCK
+#define WF_HIST_BLOCK 1024
+#endif
+constexpr int kHistBlock = WF_HIST_BLOCK;
 constexpr size_t kHistSmem = 256 * 32 * sizeof(uint32_t);  // 32 KiB
 
 int sm_count(int device);
