@@ -475,3 +475,53 @@ def test_host_entry_points(ops):
     assert ops.reduce_sum_i32_host(a) == no.reduce_sum_i32(a)
     u = synthetic.generate("u8_uniform", 3 * (128 << 20) + 11, seed=8)
     assert np.array_equal(ops.histogram256_u8_host(u), no.histogram256_u8(u))
+
+
+@pytest.mark.slow
+def test_scan_beyond_2p32_elements(ops):
+    """Maximum-size check: > 2^32 elements (16 GiB in + 16 GiB out), so tile
+    offsets, descriptors and stores need 64-bit addressing.  Verified in
+    2^28-element slices: first differences == input and the carry across
+    slice boundaries is continuous (wrapping)."""
+    n = (1 << 32) + 4097
+    free, _ = torch.cuda.mem_get_info()
+    if free < 40 << 30:
+        pytest.skip("needs ~40 GiB of free HBM")
+    x = ops.fill_synthetic("i32_small", n, seed=21)
+    y = ops.scan_inclusive_i32(x)
+    torch.cuda.synchronize()
+    step = 1 << 28
+    prev = 0
+    for lo in range(0, n, step):
+        hi = min(n, lo + step)
+        xs = x[lo:hi].to(torch.int64)
+        ys = y[lo:hi].to(torch.int64)
+        want_first = (prev + int(xs[0].item())) & 0xFFFFFFFF
+        assert int(ys[0].item()) & 0xFFFFFFFF == want_first, lo
+        d = (ys[1:] - ys[:-1] - xs[1:]) % (1 << 32)
+        assert int(d.count_nonzero().item()) == 0, lo
+        prev = int(ys[-1].item())
+        del xs, ys, d
+    total = int(ops.reduce_sum_i32(x).item()) & 0xFFFFFFFF
+    assert prev & 0xFFFFFFFF == total
+
+
+@pytest.mark.slow
+def test_compact_max_size(ops):
+    """Largest compaction one call takes (n < 2^32): count and ordered
+    output checked slice by slice against masked_select."""
+    n = (1 << 32) - 5
+    free, _ = torch.cuda.mem_get_info()
+    if free < 40 << 30:
+        pytest.skip("needs ~40 GiB of free HBM")
+    x = ops.fill_synthetic("i32_full", n, seed=22)
+    out, cnt = ops.compact_gt0_i32(x)
+    m = int(cnt.item())
+    step = 1 << 28
+    pos = 0
+    for lo in range(0, n, step):
+        want = torch.masked_select(x[lo:lo + step], x[lo:lo + step] > 0)
+        assert torch.equal(out[pos:pos + want.numel()], want), lo
+        pos += want.numel()
+        del want
+    assert pos == m
