@@ -92,9 +92,14 @@ constexpr int NFIN = 8 * NFG;             // per group: one finisher warp per ti
 constexpr int W_LB = W_FIN + NFIN;        // look-back warps W_LB .. W_LB+NLB-1
 constexpr int W_PROD = W_LB + NLB;        // producer warp
 constexpr int TM_THREADS = (W_PROD + 1) * 32;
-constexpr int QVEC = 16;                  // 128-item chunks per warp-quarter of a tile
-constexpr uint32_t TM_TILE = 4u * QVEC * 128;  // 8192 items = 32 KiB
-constexpr uint32_t TM_COLS = uint32_t(P) * 64;
+#ifndef WF_TM_TMUL
+#define WF_TM_TMUL 1  // tile = 32 KiB x TMUL
+#endif
+constexpr int TMUL = WF_TM_TMUL;
+constexpr int QVEC = 16 * TMUL;           // 128-item chunks per warp-quarter of a tile
+constexpr uint32_t TM_TILE = 4u * QVEC * 128;  // 8192 x TMUL items
+constexpr uint32_t SLOT_COLS = 64u * TMUL;     // TMEM columns per parked tile
+constexpr uint32_t TM_COLS = uint32_t(P) * SLOT_COLS;
 constexpr uint32_t kNoTileTm = 0xffffffffu;
 static_assert((P & (P - 1)) == 0 && TM_COLS <= 512, "TMEM slots: power of two, <= 512 cols");
 static_assert(NLB >= 1 && NLB <= P, "look-back warps must not outnumber TMEM slots");
@@ -276,21 +281,24 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
         break;
       }
       const int32_t *stage = stages + s * TM_TILE + q * (QVEC * 128) + lane * 4;
-      uint32_t hsum[2];
+      uint32_t hsum[2] = {0u, 0u};
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        uint32_t v[32], sum = 0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint4 x = *reinterpret_cast<const uint4 *>(stage + (8 * h + j) * 128);
-          v[4 * j] = x.x; v[4 * j + 1] = x.y; v[4 * j + 2] = x.z; v[4 * j + 3] = x.w;
-          if (COMPACT)
-            sum += (int32_t(x.x) > 0) + (int32_t(x.y) > 0) + (int32_t(x.z) > 0) + (int32_t(x.w) > 0);
-          else
-            sum += x.x + x.y + x.z + x.w;
+        for (int m = 0; m < TMUL; ++m) {
+          uint32_t v[32], sum = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint4 x = *reinterpret_cast<const uint4 *>(stage + (8 * (TMUL * h + m) + j) * 128);
+            v[4 * j] = x.x; v[4 * j + 1] = x.y; v[4 * j + 2] = x.z; v[4 * j + 3] = x.w;
+            if (COMPACT)
+              sum += (int32_t(x.x) > 0) + (int32_t(x.y) > 0) + (int32_t(x.z) > 0) + (int32_t(x.w) > 0);
+            else
+              sum += x.x + x.y + x.z + x.w;
+          }
+          tmem_st32(tcol + uint32_t(p) * SLOT_COLS + 32u * (TMUL * h + m), v);
+          hsum[h] += sum;
         }
-        tmem_st32(tcol + uint32_t(p) * 64u + 32u * h, v);
-        hsum[h] = sum;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive1(&sh.empty[s]);  // this warp is done with the stage
@@ -324,10 +332,10 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
   } else if (warp < W_LB) {
     // ------------------------------ finishers -----------------------------
     // warp f handles tile eighth (q, h): TMEM lane quarter q = warp % 4 (the
-    // only lanes it may read), columns 32h..32h+31 of the slot
+    // only lanes it may read), columns 32*TMUL*h .. +32*TMUL of the slot
     const uint32_t q = warp & 3u, h = ((warp - W_FIN) >> 2) & 1u;
     const uint32_t grp = (warp - W_FIN) >> 3;
-    const uint32_t tcol = sh.tmem_base + ((32u * q) << 16) + 32u * h;
+    const uint32_t tcol = sh.tmem_base + ((32u * q) << 16);
     const uint32_t lt = lanemask_lt();
     for (uint32_t i = grp;; i += NFG) {
       const int p = int(i % P);
@@ -342,68 +350,74 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
 #pragma unroll
       for (uint32_t w = 0; w < 4; ++w) wexcl += w < q ? sh.slot_wtot[p][w][0] + sh.slot_wtot[p][w][1] : 0u;
       const uint32_t agg = sh.slot_agg[p];
-      const uint64_t base = uint64_t(t) * TM_TILE + q * (QVEC * 128) + h * (8 * 128) + lane * 4;
       const bool full = uint64_t(t + 1) * TM_TILE <= n;
       uint32_t carry = prefix + wexcl;
+#pragma unroll 1
+      for (int m = 0; m < TMUL; ++m) {
+      const uint64_t base =
+          uint64_t(t) * TM_TILE + q * (QVEC * 128) + (8 * (TMUL * h + m)) * 128 + lane * 4;
       uint32_t v[32];
-      tmem_ld32(tcol + uint32_t(p) * 64u, v);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive1(&sh.freed[p]);  // slot data is in registers
+      tmem_ld32(tcol + uint32_t(p) * SLOT_COLS + 32u * (TMUL * h + m), v);
+      if (m == TMUL - 1) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive1(&sh.freed[p]);  // slot data is in registers
+      }
       if (!COMPACT) {
-        // the 8 chunk scans are independent until the carry: interleave them
-        uint32_t sc[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          uint32_t *x = v + 4 * j;
-          x[1] += x[0];
-          x[2] += x[1];
-          x[3] += x[2];
-          sc[j] = x[3];
-        }
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
+          // the 8 chunk scans are independent until the carry: interleave them
+          uint32_t sc[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const uint32_t y = __shfl_up_sync(kFull, sc[j], d);
-            if (lane >= uint32_t(d)) sc[j] += y;
+            uint32_t *x = v + 4 * j;
+            x[1] += x[0];
+            x[2] += x[1];
+            x[3] += x[2];
+            sc[j] = x[3];
           }
-        }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          uint32_t *x = v + 4 * j;
-          const uint32_t add = carry + sc[j] - x[3];
-          carry += __shfl_sync(kFull, sc[j], 31);
-          const uint64_t e = base + j * 128;
-          if (full) {
-            uint4 o;
-            o.x = x[0] + add; o.y = x[1] + add; o.z = x[2] + add; o.w = x[3] + add;
-            stg_stream(reinterpret_cast<uint4 *>(out + e), o);
-          } else {
+          for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t y = __shfl_up_sync(kFull, sc[j], d);
+              if (lane >= uint32_t(d)) sc[j] += y;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            uint32_t *x = v + 4 * j;
+            const uint32_t add = carry + sc[j] - x[3];
+            carry += __shfl_sync(kFull, sc[j], 31);
+            const uint64_t e = base + j * 128;
+            if (full) {
+              uint4 o;
+              o.x = x[0] + add; o.y = x[1] + add; o.z = x[2] + add; o.w = x[3] + add;
+              stg_stream(reinterpret_cast<uint4 *>(out + e), o);
+            } else {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                if (e + k < n) out[e + k] = int32_t(x[k] + add);
+            }
+          }
+        } else {
+          // ballot + popc positions; each lane stores its selected items
+          // (staging them in smem for 16-byte stores measured slower: 330 vs
+          // 290 us at 2^28)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t *x = v + 4 * j;
+            uint32_t excl = 0, tot = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t b = __ballot_sync(kFull, int32_t(x[k]) > 0);
+              excl += __popc(b & lt);
+              tot += __popc(b);
+            }
+            uint32_t pos = carry + excl;
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              if (e + k < n) out[e + k] = int32_t(x[k] + add);
+              if (int32_t(x[k]) > 0) out[pos++] = int32_t(x[k]);
+            carry += tot;
           }
-        }
-      } else {
-        // ballot + popc positions; each lane stores its selected items
-        // (staging them in smem for 16-byte stores measured slower: 330 vs
-        // 290 us at 2^28)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t *x = v + 4 * j;
-          uint32_t excl = 0, tot = 0;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint32_t b = __ballot_sync(kFull, int32_t(x[k]) > 0);
-            excl += __popc(b & lt);
-            tot += __popc(b);
-          }
-          uint32_t pos = carry + excl;
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (int32_t(x[k]) > 0) out[pos++] = int32_t(x[k]);
-          carry += tot;
         }
       }
       if (COMPACT && t == ntiles - 1 && q == 0 && h == 0 && lane == 0) *count = uint64_t(prefix) + agg;
