@@ -15,6 +15,14 @@ the reference's own code paths:
     (i32 and f32) through BOTH run_oracle and launch(hybrid_transform(...))
   - c3_pin.npz: warp inclusive prefix scan (lane-reversed shfl_down, the only
     formulation the reference DSL can express) through run_oracle and launch
+  - c4c5_pin.npz: ordered stream compaction (x > 0) and the 256-bin byte
+    histogram.  The reference DSL has no ballot, atomics or u8
+    (dsl/lexer.py:18-25, dsl/parser.py:83-88), so the warp-aggregated /
+    smem-privatised algorithms are not expressible; these are the semantic
+    formulations it CAN express (a serial in-order compaction thread; one
+    thread per bin counting i32-widened bytes), run through run_oracle and
+    launch(hybrid_transform(...)) — reference-produced vectors that pin the
+    results K4 / K5 must reproduce
   - corpus.npz: all 17 corpus kernels (corpus.py) through run_oracle
   - corpus_traces.json: run_oracle ExecTrace counts for the same runs and the
     cfg/build.py uid -> IR-class catalogue of every kernel (--traces-only
@@ -169,6 +177,60 @@ def c3_pin() -> dict:
     return {"warp_prefix_out": o1, "meta": np.array([n, grid, block, 3], dtype=np.int64)}
 
 
+C4_COMPACT_SERIAL = """
+__global__ void compact_gt0(global i32* a, global i32* out, global i32* count, i32 n) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        i32 m = 0;
+        for (i32 i = 0; i < n; i = i + 1) {
+            if (a[i] > 0) {
+                out[m] = a[i];
+                m = m + 1;
+            }
+        }
+        count[0] = m;
+    }
+}
+"""
+
+C5_HIST_PER_BIN = """
+__global__ void hist256(global i32* a, global i32* bins, i32 n) {
+    i32 b = threadIdx.x + blockIdx.x * blockDim.x;
+    i32 c = 0;
+    for (i32 i = 0; i < n; i = i + 1) {
+        if (a[i] == b) {
+            c = c + 1;
+        }
+    }
+    bins[b] = c;
+}
+"""
+
+
+def c4c5_pin() -> dict:
+    out = {}
+    cases = [("i32_full", 0, 1 << 12, 5), ("i32_select", 0, 2000, 6), ("i32_select", 10, 2000, 7),
+             ("i32_select", 500, 2000, 8), ("i32_select", 1000, 2000, 9)]
+    for gen, param, n, seed in cases:
+        a = synthetic.generate(gen, n, seed=seed, param=param)
+        bufs = [("i32", a), ("i32", np.zeros(n)), ("i32", np.zeros(1))]
+        _, o1, c1 = _run("oracle", C4_COMPACT_SERIAL, 1, 32, bufs, [n])
+        _, o2, c2 = _run("launch", C4_COMPACT_SERIAL, 1, 32, bufs, [n])
+        assert np.array_equal(o1, o2) and np.array_equal(c1, c2)
+        tag = f"c4_{gen}_{param}"
+        out[f"{tag}_in"], out[f"{tag}_out"], out[f"{tag}_count"] = a, o1[:int(c1[0])], c1
+    for gen, param, n, seed in (("u8_uniform", 0, 1 << 12, 5), ("u8_const", 0, 1000, 6),
+                                ("u8_geom", 0, 3000, 7)):
+        a8 = synthetic.generate(gen, n, seed=seed, param=param)
+        a = a8.astype(np.int32)  # the DSL has no u8: bytes widened to i32
+        bufs = [("i32", a), ("i32", np.zeros(256))]
+        _, b1 = _run("oracle", C5_HIST_PER_BIN, 1, 256, bufs, [n])
+        _, b2 = _run("launch", C5_HIST_PER_BIN, 1, 256, bufs, [n])
+        assert np.array_equal(b1, b2)
+        tag = f"c5_{gen}"
+        out[f"{tag}_in"], out[f"{tag}_bins"] = a8, b1
+    return out
+
+
 def corpus_golden() -> tuple[dict, dict]:
     arrays, manifest = {}, {}
     for k in corpus.ALL:
@@ -224,6 +286,11 @@ def corpus_traces() -> dict:
 
 
 def main() -> None:
+    if "--c4c5-only" in sys.argv:
+        np.savez_compressed(HERE / "c4c5_pin.npz", **c4c5_pin())
+        (HERE / "C4_COMPACT_SERIAL.spk").write_text(C4_COMPACT_SERIAL)
+        (HERE / "C5_HIST_PER_BIN.spk").write_text(C5_HIST_PER_BIN)
+        return
     if "--traces-only" in sys.argv:
         (HERE / "corpus_traces.json").write_text(json.dumps(corpus_traces(), indent=0))
         return
@@ -232,12 +299,15 @@ def main() -> None:
     np.savez_compressed(HERE / "oracle_kat.npz", **oracle_kat())
     np.savez_compressed(HERE / "c1c2_pin.npz", **c1c2_pin())
     np.savez_compressed(HERE / "c3_pin.npz", **c3_pin())
+    np.savez_compressed(HERE / "c4c5_pin.npz", **c4c5_pin())
     arrays, manifest = corpus_golden()
     np.savez_compressed(HERE / "corpus.npz", **arrays)
     (HERE / "corpus_manifest.json").write_text(json.dumps(manifest, indent=1))
     (HERE / "C1_I32.spk").write_text(C1_I32)
     (HERE / "C1_F32.spk").write_text(C1_F32)
     (HERE / "C3_WARP_PREFIX.spk").write_text(C3_WARP_PREFIX)
+    (HERE / "C4_COMPACT_SERIAL.spk").write_text(C4_COMPACT_SERIAL)
+    (HERE / "C5_HIST_PER_BIN.spk").write_text(C5_HIST_PER_BIN)
     print("golden vectors written to", HERE)
 
 

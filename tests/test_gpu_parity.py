@@ -525,3 +525,21 @@ def test_compact_max_size(ops):
         pos += want.numel()
         del want
     assert pos == m
+
+
+@pytest.mark.parametrize("tmem", ["1", "0"])
+def test_c4_c5_reference_pins_on_gpu(ops, golden, monkeypatch, tmem):
+    """K4 / K5 reproduce the reference-produced vectors of
+    tests/golden/c4c5_pin.npz (the reference's expressible serial compaction
+    and per-bin counting kernels), through both scan/compaction kernels."""
+    monkeypatch.setenv("WF_SCAN_TMEM", tmem)
+    g = np.load(golden / "c4c5_pin.npz")
+    for tag in [k[:-3] for k in g.files if k.endswith("_in")]:
+        a = g[f"{tag}_in"]
+        if tag.startswith("c4_"):
+            out, cnt = ops.compact_gt0_i32(dev(a))
+            m = int(host(cnt)[0])
+            assert m == int(g[f"{tag}_count"][0]) and np.array_equal(host(out)[:m], g[f"{tag}_out"]), tag
+        else:
+            bins = host(ops.histogram256_u8(dev(a))).view(np.uint64)
+            assert np.array_equal(bins.astype(np.int64), g[f"{tag}_bins"].astype(np.int64)), tag

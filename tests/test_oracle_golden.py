@@ -158,3 +158,29 @@ def test_splitmix64_known_values():
 def test_f32_tolerance_contract():
     assert no.f32_tolerance(1 << 30, 1.0) == pytest.approx(60 * 2.0 ** -24)
     assert no.f32_tolerance(1, 5.0) == 0.0
+
+
+
+def test_c4_compaction_pinned(golden):
+    """Ordered compaction: the oracle reproduces the reference's own serial
+    in-order compaction kernel (C4_COMPACT_SERIAL.spk via run_oracle and
+    launch(hybrid_transform)) at 0/1/50/100 % selectivity."""
+    g = np.load(golden / "c4c5_pin.npz")
+    cases = [k[:-3] for k in g.files if k.startswith("c4_") and k.endswith("_in")]
+    assert len(cases) == 5
+    for tag in cases:
+        want = g[f"{tag}_out"]
+        assert int(g[f"{tag}_count"][0]) == len(want)
+        assert np.array_equal(no.compact_gt0_i32(g[f"{tag}_in"]), want), tag
+
+
+def test_c5_histogram_pinned(golden):
+    """256-bin byte histogram: the oracle reproduces the reference's
+    one-thread-per-bin counting kernel (C5_HIST_PER_BIN.spk) on uniform,
+    constant and geometric bytes."""
+    g = np.load(golden / "c4c5_pin.npz")
+    cases = [k[:-3] for k in g.files if k.startswith("c5_") and k.endswith("_in")]
+    assert len(cases) == 3
+    for tag in cases:
+        got = no.histogram256_u8(g[f"{tag}_in"])
+        assert np.array_equal(got.astype(np.int64), g[f"{tag}_bins"].astype(np.int64)), tag
