@@ -168,11 +168,11 @@ struct TmShared {
   uint64_t empty[S];   // aggregators -> producer: stage read (4 arrivals)
   uint64_t parked[P];  // aggregators -> look-back + finishers: slot holds a tile
   uint64_t freed[P];   // finishers -> aggregators: slot read back (NFIN arrivals)
-  uint64_t pref[P];    // look-back -> finishers: prefix known
+  uint64_t pref[2 * P];  // look-back -> finishers: prefix of item i known (ring by i % 2P)
   uint32_t stage_tile[S];
   uint32_t slot_tile[P];
   uint32_t slot_agg[P];
-  uint32_t slot_prefix[P];
+  uint32_t item_prefix[2 * P];  // prefix of item i at i % 2P (outlives the slot's reuse)
   uint32_t slot_wtot[P][4][2];  // per tile quarter and half
   uint32_t tmem_base;
   uint32_t epoch;
@@ -198,8 +198,8 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
     for (int p = 0; p < P; ++p) {
       mbar_init(&sh.parked[p], 1);
       mbar_init(&sh.freed[p], 8);
-      mbar_init(&sh.pref[p], 1);
     }
+    for (int p = 0; p < 2 * P; ++p) mbar_init(&sh.pref[p], 1);
     fence_barrier_init();
   }
   if (warp == W_PROD && lane == 0)
@@ -343,32 +343,33 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       mbar_wait(&sh.parked[p], kp & 1u);
       const uint32_t t = sh.slot_tile[p];
       if (t == kNoTileTm) break;
-      mbar_wait(&sh.pref[p], kp & 1u);
       tc_fence_after();
-      const uint32_t prefix = sh.slot_prefix[p];
+      // everything that does not need the prefix happens before waiting for
+      // it: read the slot (metadata + TMEM), free it at once — the tile now
+      // waits in this warp's registers, not in TMEM — and do the local scan /
+      // ballot positions
       uint32_t wexcl = h ? sh.slot_wtot[p][q][0] : 0u;
 #pragma unroll
       for (uint32_t w = 0; w < 4; ++w) wexcl += w < q ? sh.slot_wtot[p][w][0] + sh.slot_wtot[p][w][1] : 0u;
       const uint32_t agg = sh.slot_agg[p];
+      uint32_t v[TMUL][32];
+#pragma unroll
+      for (int m = 0; m < TMUL; ++m) tmem_ld32(tcol + uint32_t(p) * SLOT_COLS + 32u * (TMUL * h + m), v[m]);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive1(&sh.freed[p]);
       const bool full = uint64_t(t + 1) * TM_TILE <= n;
-      uint32_t carry = prefix + wexcl;
-#pragma unroll 1
+      const uint64_t base0 = uint64_t(t) * TM_TILE + q * (QVEC * 128) + (8 * TMUL * h) * 128 + lane * 4;
+      uint32_t loc[TMUL][8];  // scan: chunk add (local); compaction: chunk write position (local)
+      uint32_t run = 0;
+#pragma unroll
       for (int m = 0; m < TMUL; ++m) {
-      const uint64_t base =
-          uint64_t(t) * TM_TILE + q * (QVEC * 128) + (8 * (TMUL * h + m)) * 128 + lane * 4;
-      uint32_t v[32];
-      tmem_ld32(tcol + uint32_t(p) * SLOT_COLS + 32u * (TMUL * h + m), v);
-      if (m == TMUL - 1) {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive1(&sh.freed[p]);  // slot data is in registers
-      }
-      if (!COMPACT) {
+        if (!COMPACT) {
           // the 8 chunk scans are independent until the carry: interleave them
           uint32_t sc[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            uint32_t *x = v + 4 * j;
+            uint32_t *x = v[m] + 4 * j;
             x[1] += x[0];
             x[2] += x[1];
             x[3] += x[2];
@@ -384,10 +385,39 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
           }
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            uint32_t *x = v + 4 * j;
-            const uint32_t add = carry + sc[j] - x[3];
-            carry += __shfl_sync(kFull, sc[j], 31);
-            const uint64_t e = base + j * 128;
+            loc[m][j] = run + sc[j] - v[m][4 * j + 3];
+            run += __shfl_sync(kFull, sc[j], 31);
+          }
+        } else {
+          // ballot + popc positions (per-lane stores after the prefix; staging
+          // in smem for 16-byte stores measured slower: 330 vs 290 us)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t *x = v[m] + 4 * j;
+            uint32_t excl = 0, tot = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t b = __ballot_sync(kFull, int32_t(x[k]) > 0);
+              excl += __popc(b & lt);
+              tot += __popc(b);
+            }
+            loc[m][j] = run + excl;
+            run += tot;
+          }
+        }
+      }
+      const int r = int(i % (2 * P));
+      mbar_wait(&sh.pref[r], (i / (2 * P)) & 1u);
+      const uint32_t prefix = sh.item_prefix[r];
+      const uint32_t off = prefix + wexcl;
+#pragma unroll
+      for (int m = 0; m < TMUL; ++m) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t *x = v[m] + 4 * j;
+          const uint64_t e = base0 + (8 * m + j) * 128;
+          if (!COMPACT) {
+            const uint32_t add = off + loc[m][j];
             if (full) {
               uint4 o;
               o.x = x[0] + add; o.y = x[1] + add; o.z = x[2] + add; o.w = x[3] + add;
@@ -397,26 +427,11 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
               for (int k = 0; k < 4; ++k)
                 if (e + k < n) out[e + k] = int32_t(x[k] + add);
             }
-          }
-        } else {
-          // ballot + popc positions; each lane stores its selected items
-          // (staging them in smem for 16-byte stores measured slower: 330 vs
-          // 290 us at 2^28)
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const uint32_t *x = v + 4 * j;
-            uint32_t excl = 0, tot = 0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint32_t b = __ballot_sync(kFull, int32_t(x[k]) > 0);
-              excl += __popc(b & lt);
-              tot += __popc(b);
-            }
-            uint32_t pos = carry + excl;
+          } else {
+            uint32_t pos = off + loc[m][j];
 #pragma unroll
             for (int k = 0; k < 4; ++k)
               if (int32_t(x[k]) > 0) out[pos++] = int32_t(x[k]);
-            carry += tot;
           }
         }
       }
@@ -442,9 +457,10 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
           st_relaxed_gpu(desc + uint64_t(t) * kDescStride, pack_desc(epoch, kStPrefix, excl + agg));
       }
       if (lane == 0) {
-        sh.slot_prefix[p] = excl;
+        const int r = int(i % (2 * P));
+        sh.item_prefix[r] = excl;
         TM_STAMP(t, 3);
-        mbar_arrive1(&sh.pref[p]);
+        mbar_arrive1(&sh.pref[r]);
       }
       __syncwarp();
     }
