@@ -21,6 +21,14 @@
 #include "wf_device.cuh"
 #include "wf_internal.h"
 
+#ifndef WF_RED_PDL
+#define WF_RED_PDL 0  // programmatic dependent launch between consecutive K2 launches
+#endif
+#ifndef WF_RED_PDL_EARLY
+#define WF_RED_PDL_EARLY 0  // 1: wait only before touching ws/out (unsafe if the
+                            // previous kernel in the stream produced `in`)
+#endif
+
 namespace wf {
 namespace {
 
@@ -109,6 +117,16 @@ __global__ void __launch_bounds__(BLOCK)
   using elem_t = typename Op::elem_t;
   const uint64_t gtid = uint64_t(blockIdx.x) * BLOCK + threadIdx.x;
   const uint64_t nthreads = uint64_t(gridDim.x) * BLOCK;
+#if WF_RED_PDL
+  // let the next launch in the stream get its CTAs resident while this grid's
+  // tail (last CTAs, partial fold) finishes
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#if !WF_RED_PDL_EARLY
+  // ... but touch nothing before every earlier grid in the stream (e.g. the
+  // producer of `in`) has completed and flushed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+#endif
 
   // head (scalar until 16 B alignment) | body (16 B vectors) | tail (scalar)
   const uintptr_t addr = reinterpret_cast<uintptr_t>(in);
@@ -162,6 +180,10 @@ __global__ void __launch_bounds__(BLOCK)
     for (int u = 0; u + s < UNROLL; u += 2 * s) acc[u][0] = Op::add(acc[u][0], acc[u + s][0]);
 
   const acc_t bsum = block_sum<Op, BLOCK>(acc[0][0]);
+#if WF_RED_PDL && WF_RED_PDL_EARLY
+  // early variant: the streaming above overlapped the previous grid's tail
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
 
   if (Op::kOrderFree) {
     // integer Σ is order-independent: ONE 64-bit atomic per block carries both
@@ -268,9 +290,23 @@ cudaError_t launch_block(const typename Op::elem_t *in, uint64_t n,
   auto *ticket = reinterpret_cast<uint32_t *>(ws);
   auto *partials = reinterpret_cast<typename Op::acc_t *>(
       static_cast<char *>(ws) + kWsHeader);
+#if WF_RED_PDL
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(BLOCK);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, reduce_kernel<Op, BLOCK, kUnroll, false>, in, n, out, partials,
+                            ticket, MgArgs{});
+#else
   reduce_kernel<Op, BLOCK, kUnroll>
       <<<grid, BLOCK, 0, s>>>(in, n, out, partials, ticket);
   return cudaGetLastError();
+#endif
 }
 
 template <class Op>
