@@ -109,3 +109,37 @@ def test_shard_range_partitions(n, world):
 def test_shard_range_rejects_bad_rank():
     with pytest.raises(ValueError):
         wd.shard_range(10, 2, 2)
+
+
+def _p2p_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2112_10034_b200 import p2p
+        try:
+            p2p.Mailboxes.from_process_group(torch.device("cpu"))
+            q.put((rank, "built"))
+        except Exception as e:  # expected here: no GPU for the mailbox
+            q.put((rank, f"raised {type(e).__name__}"))
+        dist.barrier()  # every rank left the set-up collective sequence together
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_mailbox_setup_failure_is_collective():
+    """Without a GPU the mailbox allocation fails; the set-up is a consensus
+    collective, so EVERY rank raises (and none is left waiting in a
+    collective) — the bench then keeps the NCCL exchange on all ranks."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert out == {0: "raised LaunchError", 1: "raised LaunchError"}
