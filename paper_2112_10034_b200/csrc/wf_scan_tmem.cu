@@ -12,18 +12,25 @@
 // its own warps and its own mbarrier pipeline, so a landed tile is reduced
 // and published at once whatever the state of older tiles:
 //
-//   producer warp    claims tile ids (ticket), TMA-loads them into a ring of
-//                    S smem stages (cp.async.bulk + mbarrier complete_tx)
-//   aggregator WG    warps 0-3: LDS the landed stage once (the x[j][k] layout
-//                    of the SDK shfl_scan), REDUX the tile value, tcgen05.st
-//                    the data into one of P TMEM slots (64 columns = 32 KiB)
-//                    and release the stage
+//   producer warp    claims tile ids (ticket, drawn one stage ahead) and
+//                    TMA-loads them into a ring of S smem stages
+//                    (cp.async.bulk + mbarrier complete_tx); ragged last tile
+//                    by guarded copy
+//   aggregator warps 0-3: LDS the landed stage once (the x[j][k] layout of the
+//                    SDK shfl_scan), tcgen05.st it into one of P TMEM slots
+//                    (64 columns = 32 KiB), release the stage, REDUX the tile
+//                    value and publish its look-back descriptor at once
 //   look-back warps  run the decoupled look-back over the tile descriptors
-//                    (the aggregator publishes each aggregate itself, so a
-//                    look-back warp busy with an older tile never delays it)
-//   finisher warps   4-11, one per tile eighth: wait the prefix, tcgen05.ld it back,
-//                    scan (SHFL.UP) / compact (VOTE + POPC) it, store to HBM
-//                    (STG.128 for the scan) and release the TMEM slot
+//                    (round-robin over tiles, so several resolve at once) and
+//                    post each prefix into a 2P-entry ring
+//   finisher warps   4-11, one per tile eighth: tcgen05.ld the tile back, free
+//                    the slot, scan (SHFL.UP, 8 chunk chains interleaved) /
+//                    ballot-compact (VOTE + POPC) it locally, then wait for
+//                    the prefix and store (STG.128 for the scan)
+//
+// Hand-offs are mbarriers (full / empty per stage; parked / freed per slot;
+// pref per ring entry), each with a phase per use, so no role ever waits on a
+// CTA-wide barrier.
 //
 // Per SM (default: one CTA, S=6 stages, P=8 slots = all 512 TMEM columns,
 // 6 look-back warps): 6 stages loading + 8 parked tiles = 448 KiB of tiles on
