@@ -400,6 +400,13 @@ def per_kernel(args, rank, world, local, dev, peak) -> dict:
     import torch
     from paper_2112_10034_b200 import distributed as wd, ops
     res = {}
+    pc, exchange = None, None
+    if world > 1:  # C3-C5 exchanges over peer memory when every rank can map every mailbox
+        from paper_2112_10034_b200 import p2p
+        pc, why = p2p.try_peer_collectives(dev)
+        exchange = ("peer-memory kernel (wf_peer_exchange)" if pc
+                    else f"NCCL (peer path unavailable: {why})")
+        log(f"rank {rank}: C3-C5 exchange = {exchange}")
     steps, warm = max(5, args.steps), max(3, args.warmup)
 
     def stats(times_ms, n_elems, bytes_per_elem, n_total):
@@ -433,11 +440,11 @@ def per_kernel(args, rank, world, local, dev, peak) -> dict:
     lo, hi = wd.shard_range(N_C3, rank, world)
     x = ops.fill_synthetic("i32_full", hi - lo, seed=0, base=lo, device=dev)
     y = torch.empty_like(x)
-    t = time_launches(lambda: wd.scan_inclusive_i32(x, y), steps, warm)
+    t = time_launches(lambda: wd.scan_inclusive_i32(x, y, peer=pc), steps, warm)
     res["c3_scan_i32"] = stats(t, hi - lo, 8 if world == 1 else 12, N_C3)
     # C4 compaction
     out = torch.empty_like(x)
-    t = time_launches(lambda: wd.compact_gt0_i32(x, out), steps, warm)
+    t = time_launches(lambda: wd.compact_gt0_i32(x, out, peer=pc), steps, warm)
     res["c4_compact_i32"] = stats(t, hi - lo, 6, N_C4)
     res["c4_compact_i32"]["bytes_per_elem_note"] = "4 B read + 4 B x selectivity (~0.5) written"
     del x, y, out
@@ -445,8 +452,11 @@ def per_kernel(args, rank, world, local, dev, peak) -> dict:
     # C5 histogram
     lo, hi = wd.shard_range(N_C5, rank, world)
     u = ops.fill_synthetic("u8_uniform", hi - lo, seed=0, base=lo, device=dev)
-    t = time_launches(lambda: wd.histogram256_u8(u), steps, warm)
+    t = time_launches(lambda: wd.histogram256_u8(u, peer=pc), steps, warm)
     res["c5_hist_u8"] = stats(t, hi - lo, 1, N_C5)
+    if exchange is not None:
+        for k in ("c3_scan_i32", "c4_compact_i32", "c5_hist_u8"):
+            res[k]["exchange"] = exchange
     del u
     torch.cuda.empty_cache()
     return res

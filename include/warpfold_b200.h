@@ -143,6 +143,27 @@ int wf_reduce_sum_f32_mg(const float *in, uint64_t n, float *out, int block,
                          void *const *d_peers, const void *d_mailbox, int rank,
                          int world, uint32_t epoch, wf_stream_t stream);
 
+/* Small collectives over the same kind of peer-memory mailboxes, one
+ * single-block kernel per rank (replace NCCL all-gather / all-reduce + fold
+ * for the exchange steps of C3-C5).  A peer mailbox holds `cap` payload words
+ * per source rank (wf_peer_mailbox_alloc; free with wf_mailbox_free).
+ *   mode WF_PEER_ALLGATHER: d_out[r * count + i] = vals_r[i]          (u64)
+ *   mode WF_PEER_EXSCAN:    d_out = {sum_{r<rank} vals_r[0], sum_r vals_r[0]} (u64)
+ *   mode WF_PEER_ALLREDUCE: d_out[i] = sum_r vals_r[i]               (u64)
+ *   mode WF_PEER_EXSCAN_U32: as EXSCAN on u32 values mod 2^32, d_out = 2 x u32
+ * Results are identical on every rank (rank-order combine).  *d_err is set to
+ * 1 when a peer did not arrive within ~4 s (results then undefined). */
+#define WF_PEER_ALLGATHER 0
+#define WF_PEER_EXSCAN 1
+#define WF_PEER_ALLREDUCE 2
+#define WF_PEER_EXSCAN_U32 3
+size_t wf_peer_mailbox_bytes(int world, uint32_t cap);
+int wf_peer_mailbox_alloc(int world, uint32_t cap, void **d_mailbox);
+int wf_peer_exchange(int mode, const void *d_vals, uint32_t count, uint32_t cap,
+                     void *d_out, void *const *d_peers, const void *d_mailbox,
+                     int rank, int world, uint32_t epoch, uint32_t *d_err,
+                     wf_stream_t stream);
+
 /* ---- K3: shfl_scan inclusive prefix sum --------------------------------
  * out[i] = carry + in[0] + ... + in[i] (wrapping), single pass with
  * decoupled look-back.  d_carry_in: device int32 (NULL = 0), used by the

@@ -261,6 +261,39 @@ int wf_reduce_sum_f32_mg(const float *in, uint64_t n, float *out, int block, int
                      "reduce_sum_f32_mg");
 }
 
+size_t wf_peer_mailbox_bytes(int world, uint32_t cap) {
+  return world < 1 ? 0 : peer_mailbox_bytes(world, cap);
+}
+
+int wf_peer_mailbox_alloc(int world, uint32_t cap, void **d_mailbox) {
+  if (d_mailbox == nullptr || world < 1 || world > 256 || cap < 1 || cap > (1u << 20))
+    return fail(WF_ERR_ARG, "peer mailbox: world in [1, 256], cap in [1, 2^20]");
+  const size_t b = peer_mailbox_bytes(world, cap);
+  int rc = cuda_status(cudaMalloc(d_mailbox, b), "peer mailbox alloc");
+  if (rc) return rc;
+  return cuda_status(cudaMemset(*d_mailbox, 0, b), "peer mailbox zero");
+}
+
+int wf_peer_exchange(int mode, const void *d_vals, uint32_t count, uint32_t cap, void *d_out,
+                     void *const *d_peers, const void *d_mailbox, int rank, int world,
+                     uint32_t epoch, uint32_t *d_err, wf_stream_t stream) {
+  if (mode < WF_PEER_ALLGATHER || mode > WF_PEER_EXSCAN_U32)
+    return fail(WF_ERR_ARG, "unknown peer exchange mode %d", mode);
+  if (d_vals == nullptr || d_out == nullptr || d_peers == nullptr || d_mailbox == nullptr ||
+      d_err == nullptr)
+    return fail(WF_ERR_ARG, "NULL pointer");
+  if (world < 1 || world > 256 || rank < 0 || rank >= world)
+    return fail(WF_ERR_ARG, "rank %d / world %d out of range", rank, world);
+  if (count < 1 || count > cap) return fail(WF_ERR_ARG, "count %u must be in [1, cap=%u]", count, cap);
+  if ((mode == WF_PEER_EXSCAN || mode == WF_PEER_EXSCAN_U32) && count != 1)
+    return fail(WF_ERR_ARG, "exclusive scan exchanges one value per rank");
+  if (epoch == 0) return fail(WF_ERR_ARG, "epoch must start at 1");
+  return cuda_status(launch_peer_exchange(mode, d_vals, count, cap, d_out, d_peers, d_mailbox,
+                                          rank, world, epoch, d_err,
+                                          static_cast<cudaStream_t>(stream)),
+                     "peer_exchange");
+}
+
 int wf_fold_f32(const float *vals, uint32_t count, float *out, wf_stream_t stream) {
   if (out == nullptr || (count && vals == nullptr)) return fail(WF_ERR_ARG, "NULL pointer");
   return cuda_status(launch_fold_f32(vals, count, out, static_cast<cudaStream_t>(stream)), "fold_f32");

@@ -45,6 +45,10 @@ int auto_reduce_grid(bool is_f32, int block, uint64_t n);
 cudaError_t launch_reduce_f32_mg(const float *in, uint64_t n, float *out, int block, int grid,
                                  void *ws, void *const *peers, const void *mine, int rank,
                                  int world, uint32_t epoch, cudaStream_t s);
+size_t peer_mailbox_bytes(int world, uint32_t count);
+cudaError_t launch_peer_exchange(int mode, const void *vals, uint32_t count, uint32_t cap,
+                                 void *out, void *const *peers, const void *mine, int rank,
+                                 int world, uint32_t epoch, uint32_t *err, cudaStream_t s);
 cudaError_t launch_fold_f32(const float *v, uint32_t count, float *out,
                             cudaStream_t s);
 cudaError_t launch_fold_i32(const int32_t *v, uint32_t count, int32_t *out,

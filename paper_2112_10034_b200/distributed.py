@@ -20,7 +20,10 @@ one small collective:
 
 The exchange helpers are backend-agnostic (NCCL on GPUs, gloo in the CPU
 tests) and the carries/offsets are computed by the device kernels, so a step
-needs no host round trip.
+needs no host round trip.  With a ``p2p.PeerCollectives`` (``peer=``) the
+scan carries, compaction offsets and bin sums instead travel over peer memory
+(NVLink, CUDA IPC mailboxes) in one single-block kernel per rank; the fp32
+reduction has its own fused form (``p2p.PeerReducer``).
 """
 
 from __future__ import annotations
@@ -80,16 +83,22 @@ def reduce_sum_i32(x_local: torch.Tensor, group=None, block: int = 256) -> torch
 
 
 def scan_inclusive_i32(x_local: torch.Tensor, out: torch.Tensor | None = None,
-                       group=None) -> torch.Tensor:
+                       group=None, peer=None) -> torch.Tensor:
+    """`peer`: a p2p.PeerCollectives — the shard totals then travel over peer
+    memory in one kernel instead of NCCL all-gather + fold."""
     rank, world = _world(group)
     if world == 1:
         return ops.scan_inclusive_i32(x_local, out)
+    if peer is not None:
+        carry = peer.exscan_u32(ops.reduce_sum_i32(x_local))[:1]
+        return ops.scan_inclusive_i32(x_local, out, carry=carry)
     totals = exchange(ops.reduce_sum_i32(x_local), group).reshape(-1)
     carry = ops.fold(totals, count=rank)  # exclusive prefix of earlier shards
     return ops.scan_inclusive_i32(x_local, out, carry=carry)
 
 
-def compact_gt0_i32(x_local: torch.Tensor, out: torch.Tensor | None = None, group=None):
+def compact_gt0_i32(x_local: torch.Tensor, out: torch.Tensor | None = None, group=None,
+                    peer=None):
     """Returns (out_local, count_local, offset, total) as device int64 scalars
     for count/offset/total; rank r's selected elements belong at
     [offset, offset + count) of the global a[a > 0]."""
@@ -98,15 +107,20 @@ def compact_gt0_i32(x_local: torch.Tensor, out: torch.Tensor | None = None, grou
     if world == 1:
         zero = torch.zeros(1, dtype=torch.int64, device=count.device)
         return out, count, zero, count
+    if peer is not None:
+        r = peer.exscan_u64(count)
+        return out, count, r[:1], r[1:]
     counts = exchange(count, group).reshape(-1)
     offset = ops.fold(counts, count=rank)
     total = ops.fold(counts)
     return out, count, offset, total
 
 
-def histogram256_u8(x_local: torch.Tensor, group=None) -> torch.Tensor:
+def histogram256_u8(x_local: torch.Tensor, group=None, peer=None) -> torch.Tensor:
     bins = ops.histogram256_u8(x_local)
     rank, world = _world(group)
     if world > 1:
+        if peer is not None:
+            return peer.allreduce_u64(bins)
         dist.all_reduce(bins, op=dist.ReduceOp.SUM, group=group)
     return bins

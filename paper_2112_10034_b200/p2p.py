@@ -44,8 +44,17 @@ class Mailboxes:
         self._opened = opened
         self._owned = owned
 
+    @staticmethod
+    def _alloc(world: int, cap: int | None, out: C.c_void_p) -> None:
+        lib = _lib.load()
+        if cap is None:  # the fused-K2 layout: one epoch-tagged word per rank and bank
+            _check(lib.wf_mailbox_alloc(world, C.byref(out)), "wf_mailbox_alloc")
+        else:            # wf_peer_exchange layout: `cap` payload words + flag per rank and bank
+            _check(lib.wf_peer_mailbox_alloc(world, cap, C.byref(out)), "wf_peer_mailbox_alloc")
+
     @classmethod
-    def from_process_group(cls, device: torch.device, group=None) -> "Mailboxes":
+    def from_process_group(cls, device: torch.device, group=None,
+                           cap: int | None = None) -> "Mailboxes":
         """Collective: every rank of `group` must call it.  Failures on any
         rank (no IPC, no peer access) make every rank raise, after the same
         sequence of collectives, so no rank is left waiting in one."""
@@ -53,7 +62,7 @@ class Mailboxes:
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         mine, handle, err = C.c_void_p(), (C.c_char * 64)(), None
         try:
-            _check(lib.wf_mailbox_alloc(world, C.byref(mine)), "wf_mailbox_alloc")
+            cls._alloc(world, cap, mine)
             _check(lib.wf_ipc_handle(mine, handle), "wf_ipc_handle")
         except LaunchError as e:
             err = str(e)
@@ -84,14 +93,13 @@ class Mailboxes:
         return box
 
     @classmethod
-    def local(cls, world: int, device: torch.device) -> list["Mailboxes"]:
+    def local(cls, world: int, device: torch.device, cap: int | None = None) -> list["Mailboxes"]:
         """In-process stand-in for `world` ranks on one GPU (tests): every
         rank's view shares the same pointer array."""
-        lib = _lib.load()
         own = []
         for _ in range(world):
             p = C.c_void_p()
-            _check(lib.wf_mailbox_alloc(world, C.byref(p)), "wf_mailbox_alloc")
+            cls._alloc(world, cap, p)
             own.append(p.value)
         views = [cls(own[r], own, [], device, []) for r in range(world)]
         views[0]._owned = own  # freed once
@@ -138,6 +146,54 @@ class PeerReducer:
         self.boxes.close()
 
 
+class PeerCollectives:
+    """The small exchanges of the sharded C3-C5 paths over peer memory
+    (`wf_peer_exchange`): one single-block kernel per call and rank, results
+    identical on every rank.  Every rank must issue the same sequence of calls."""
+
+    EXSCAN, ALLREDUCE, EXSCAN_U32 = 1, 2, 3
+
+    def __init__(self, boxes: Mailboxes, rank: int, world: int, cap: int, device: torch.device):
+        self.boxes, self.rank, self.world, self.cap = boxes, rank, world, cap
+        self.epoch = 0
+        self.err = torch.zeros(1, dtype=torch.int32, device=device)
+
+    @classmethod
+    def for_process_group(cls, device: torch.device, group=None, cap: int = 256):
+        boxes = Mailboxes.from_process_group(device, group, cap=cap)
+        return cls(boxes, dist.get_rank(group), dist.get_world_size(group), cap, device)
+
+    def _run(self, mode: int, vals: torch.Tensor, count: int, out: torch.Tensor, stream=None):
+        self.epoch += 1
+        _check(_lib.load().wf_peer_exchange(mode, vals.data_ptr(), count, self.cap, out.data_ptr(),
+                                            self.boxes.peers.data_ptr(), self.boxes.own,
+                                            self.rank, self.world, self.epoch,
+                                            self.err.data_ptr(), ops._stream_handle(stream)),
+               "wf_peer_exchange")
+        return out
+
+    def exscan_u32(self, v: torch.Tensor, stream=None) -> torch.Tensor:
+        """int32[1] per rank -> int32[2] = (sum over lower ranks, sum over all), mod 2^32."""
+        out = torch.empty(2, dtype=torch.int32, device=v.device)
+        return self._run(self.EXSCAN_U32, v, 1, out, stream)
+
+    def exscan_u64(self, v: torch.Tensor, stream=None) -> torch.Tensor:
+        """int64[1] per rank -> int64[2] = (sum over lower ranks, sum over all)."""
+        out = torch.empty(2, dtype=torch.int64, device=v.device)
+        return self._run(self.EXSCAN, v, 1, out, stream)
+
+    def allreduce_u64(self, v: torch.Tensor, stream=None) -> torch.Tensor:
+        """int64[count] per rank -> elementwise sum over ranks (wrapping)."""
+        out = torch.empty_like(v)
+        return self._run(self.ALLREDUCE, v, v.numel(), out, stream)
+
+    def failed(self) -> bool:
+        return bool(self.err.item())
+
+    def close(self) -> None:
+        self.boxes.close()
+
+
 def try_peer_reducer(device: torch.device, x_probe: torch.Tensor, group=None):
     """Collective.  Build a PeerReducer and check it bit-for-bit against the
     NCCL path on `x_probe` (this rank's shard of a probe input).  Returns
@@ -156,3 +212,30 @@ def try_peer_reducer(device: torch.device, x_probe: torch.Tensor, group=None):
         pr.close()
         return None, "peer-memory result differs from the NCCL path"
     return pr, "ok"
+
+
+def try_peer_collectives(device: torch.device, group=None, cap: int = 256):
+    """Collective.  PeerCollectives checked against NCCL on a probe (an
+    exclusive scan of rank+1 and an all-reduce of a rank-dependent vector).
+    Returns (collectives, "ok") or (None, reason) — the same on every rank."""
+    from . import distributed as wd
+    try:
+        pc = PeerCollectives.for_process_group(device, group, cap)
+    except Exception as e:
+        return None, f"{type(e).__name__}: {e}"
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    v = torch.tensor([rank + 1], dtype=torch.int64, device=device)
+    got = pc.exscan_u64(v)
+    vec = torch.arange(cap, dtype=torch.int64, device=device) * (rank + 3)
+    red = pc.allreduce_u64(vec)
+    gathered = wd.exchange(v, group).reshape(-1)
+    want_red = vec.clone()
+    dist.all_reduce(want_red, group=group)
+    same = (not pc.failed() and int(got[0]) == int(gathered[:rank].sum())
+            and int(got[1]) == int(gathered.sum()) and torch.equal(red, want_red))
+    ok = torch.tensor([1 if same else 0], dtype=torch.int32, device=device)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+    if int(ok.item()) != 1:
+        pc.close()
+        return None, "peer-memory collectives differ from NCCL"
+    return pc, "ok"

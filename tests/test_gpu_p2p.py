@@ -12,6 +12,8 @@ process through the CUDA IPC handle path the multi-process code uses."""
 
 import multiprocessing as mp
 
+import numpy as np
+
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -123,10 +125,23 @@ def _rank_main(rank: int, world: int, port: int, n: int, q) -> None:
         want = ops.fold(T.cat([ops.reduce_sum_f32(x) for x in xs]))  # NCCL-path combine, locally
         pr = p2p.PeerReducer.for_process_group(dev)
         got = [pr.reduce_sum_f32(xs[rank]).clone() for _ in range(3)]
+        pc = p2p.PeerCollectives.for_process_group(dev, cap=256)
+        xi = ops.fill_synthetic("i32_full", 5000 + rank, seed=rank, device=dev)
+        carry = pc.exscan_u32(ops.reduce_sum_i32(xi))
+        bins = pc.allreduce_u64(ops.histogram256_u8(ops.fill_synthetic("u8_uniform", 777, seed=rank,
+                                                                        device=dev)))
         T.cuda.synchronize()
-        q.put((rank, [bool(T.equal(g.view(T.int32), want.view(T.int32))) for g in got]))
+        res = [bool(T.equal(g.view(T.int32), want.view(T.int32))) for g in got]
+        res.append(not pc.failed())
+        res.append(int(bins.sum().item()) == 777 * world)
+        totals = [int(ops.reduce_sum_i32(ops.fill_synthetic("i32_full", 5000 + r, seed=r,
+                                                              device=dev)).item()) & 0xFFFFFFFF
+                  for r in range(world)]
+        res.append((int(carry[0].item()) & 0xFFFFFFFF) == (sum(totals[:rank]) & 0xFFFFFFFF))
+        q.put((rank, res))
         D.barrier()
         pr.close()
+        pc.close()
     except Exception as e:  # reported to the parent
         q.put((rank, f"{type(e).__name__}: {e}"))
     finally:
@@ -150,4 +165,47 @@ def test_peer_reducer_two_processes_one_gpu(mods):
     res = dict(q.get(timeout=240) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    assert res[0] == [True] * 3 and res[1] == [True] * 3, res
+    assert res[0] == [True] * 6 and res[1] == [True] * 6, res
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_peer_collectives_in_process(mods, world):
+    """wf_peer_exchange with `world` ranks as concurrent single-block kernels
+    on one GPU: scan carries (u32, wrapping), compaction offsets (u64) and the
+    bin all-reduce, over several epochs (both mailbox banks), results
+    identical on every rank and equal to the host-side combine."""
+    ops, p2p, wd = mods
+    dev = torch.device("cuda", 0)
+    cap = 256
+    boxes = p2p.Mailboxes.local(world, dev, cap=cap)
+    pcs = [p2p.PeerCollectives(boxes[r], r, world, cap, dev) for r in range(world)]
+    streams = [torch.cuda.Stream(dev) for _ in range(world)]
+    rng = np.random.default_rng(world)
+    try:
+        for step in range(4):
+            u32 = rng.integers(-2**31, 2**31, size=world, dtype=np.int64).astype(np.int32)
+            u64 = rng.integers(0, 2**40, size=world, dtype=np.int64)
+            vec = rng.integers(0, 2**33, size=(world, cap), dtype=np.int64)
+            ins = [(torch.tensor(u32[r:r + 1], device=dev), torch.tensor(u64[r:r + 1], device=dev),
+                    torch.tensor(vec[r], device=dev)) for r in range(world)]
+            torch.cuda.synchronize()
+            outs = [None] * world
+            order = range(world) if step % 2 == 0 else reversed(range(world))
+            for r in order:
+                with torch.cuda.stream(streams[r]):
+                    a, b, c = ins[r]
+                    outs[r] = (pcs[r].exscan_u32(a, stream=streams[r]),
+                               pcs[r].exscan_u64(b, stream=streams[r]),
+                               pcs[r].allreduce_u64(c, stream=streams[r]))
+            torch.cuda.synchronize()
+            w32 = u32.astype(np.uint32).astype(np.uint64)
+            for r in range(world):
+                assert not pcs[r].failed()
+                e32, e64, red = (t.cpu().numpy() for t in outs[r])
+                assert e32.view(np.uint32).tolist() == [int(w32[:r].sum()) & 0xFFFFFFFF,
+                                                        int(w32.sum()) & 0xFFFFFFFF]
+                assert e64.tolist() == [int(u64[:r].sum()), int(u64.sum())]
+                assert np.array_equal(red, vec.sum(0))
+    finally:
+        torch.cuda.synchronize()
+        boxes[0].close()
