@@ -338,7 +338,15 @@ def run_ours(args, rank, world, local) -> dict | None:
             float(ops.fold(wd.exchange(part).reshape(-1)).item())
     e2e_ms = (time.perf_counter() - t) * 1e3 / e2e_steps
     e2e_ms_max = max_over_ranks(e2e_ms, world)
-    del host
+    # the link's own ceiling on this box: plain pinned H2D copy of the same bytes
+    dst = torch.empty_like(x)
+    dst.copy_(host, non_blocking=True)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    dst.copy_(host, non_blocking=True)
+    torch.cuda.synchronize()
+    h2d_gbs = 4.0 * n_local / (time.perf_counter() - t) / 1e9
+    del host, dst
 
     # ---- per-kernel lines for the other BASELINE configs -------------------
     per = {}
@@ -389,7 +397,9 @@ def run_ours(args, rank, world, local) -> dict | None:
         "e2e": {"value": round(N_C2 / (e2e_ms_max * 1e-3) / 1e9, 4), "unit": "Gelem/s",
                 "h2d_bytes_per_step": 4 * n_local, "d2h_bytes_per_step": 4,
                 "path": "wf_reduce_sum_f32_host (pinned host -> chunked H2D overlapped with K2 "
-                        "-> D2H of the result)", "steps": e2e_steps},
+                        "-> D2H of the result)", "steps": e2e_steps,
+                "pcie_h2d_gbs": round(h2d_gbs, 2),
+                "frac_of_h2d_copy": round(4.0 * n_local / (e2e_ms * 1e-3) / 1e9 / h2d_gbs, 4)},
         "gpu_launches": gpu_launches,
         "clocks": clk.summary(),
         "per_kernel": per,
