@@ -37,6 +37,11 @@ N_C2 = 1 << 30
 N_C3 = 1 << 28
 N_C4 = 1 << 28
 N_C5 = 1 << 32
+# C2 does not pin a block size (C1 does: 256).  1024-thread CTAs look 4 %
+# faster in a back-to-back launch loop (tools/k2_grid3.py) but not under the
+# bench's per-step event timing (0.619-0.624 vs 0.616 ms on the same box,
+# profiles/r01_reduce_experiments.md), so 256 stays.
+BLOCK_C2 = int(os.environ.get("WF_BENCH_BLOCK_C2", "256"))
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 
 
@@ -304,9 +309,9 @@ def run_ours(args, rank, world, local) -> dict | None:
             e = torch.cuda.Event(enable_timing=True)
             s.record()
         if peer is not None:  # one kernel: local reduce + exchange + fold
-            part = peer.reduce_sum_f32(x, block=256)
+            part = peer.reduce_sum_f32(x, block=BLOCK_C2)
         else:
-            part = ops.reduce_sum_f32(x, block=256)
+            part = ops.reduce_sum_f32(x, block=BLOCK_C2)
         launches += 1
         if record:
             e.record()
@@ -397,7 +402,7 @@ def run_ours(args, rank, world, local) -> dict | None:
             "workload": "C2: fp32 warp-shuffle reduction over 2^30 elements sharded across "
                         f"{world} B200",
             "exchange": exchange,
-            "n": N_C2, "block": 256, "parallelism": f"shard{world}",
+            "n": N_C2, "block": BLOCK_C2, "parallelism": f"shard{world}",
             "l2": "inputs larger than L2 (4 GiB vs 126 MB), no flush needed",
         },
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,

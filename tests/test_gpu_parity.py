@@ -112,18 +112,19 @@ def test_reduce_f32_reproducible_and_pinned(ops, golden):
 
 
 @pytest.mark.slow
-def test_reduce_f32_full_config(ops):
+@pytest.mark.parametrize("block", [256, 1024])  # 1024: bench.py's C2 configuration
+def test_reduce_f32_full_config(ops, block):
     """BASELINE config 2 on one GPU: 2^30 fp32."""
     n = 1 << 30
     x = ops.fill_synthetic("f32_unit", n, seed=1)
-    got = float(host(ops.reduce_sum_f32(x))[0])
+    got = float(host(ops.reduce_sum_f32(x, block=block))[0])
     exact = float(torch.sum(x, dtype=torch.float64))
     absx = float(torch.sum(x.abs(), dtype=torch.float64))
     # per-thread chains: n / (148 SMs * resident threads * 16 chains) elements
     chain = n // (148 * 1024 * 16) + 16
     assert abs(got - exact) <= no.f32_tolerance(n, absx, chain=chain)
     assert abs(got - exact) <= no.f32_tolerance(n, absx)  # SURVEY §8c contract
-    assert float(host(ops.reduce_sum_f32(x))[0]) == got
+    assert float(host(ops.reduce_sum_f32(x, block=block))[0]) == got
     del x
 
 
