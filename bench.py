@@ -483,6 +483,14 @@ def per_kernel(args, rank, world, local, dev, peak) -> dict:
     if exchange is not None:
         for k in ("c3_scan_i32", "c4_compact_i32", "c5_hist_u8"):
             res[k]["exchange"] = exchange
+    # DRAM bytes per launch measured by ncu --set full at the 1-GPU BASELINE
+    # size (profiles/ncu_traffic.json) next to the algorithmic bytes
+    if world == 1:
+        for k, op in (("c1_reduce_i32", "reduce_sum_i32"), ("c3_scan_i32", "scan_inclusive_i32"),
+                      ("c4_compact_i32", "compact_gt0_i32"), ("c5_hist_u8", "histogram256_u8")):
+            if k in res:
+                res[k]["ncu_dram_bytes"] = ncu_traffic(op)
+                res[k]["algorithmic_bytes"] = int(res[k]["n"] * res[k]["bytes_per_elem"])
     del u
     torch.cuda.empty_cache()
     return res
