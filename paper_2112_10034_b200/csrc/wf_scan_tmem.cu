@@ -190,7 +190,10 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
     tile_tmem_kernel(const int32_t *__restrict__ in, int32_t *__restrict__ out, uint64_t n,
                      uint32_t ntiles, const int32_t *__restrict__ carry_in,
                      uint64_t *__restrict__ count, uint64_t *__restrict__ desc,
-                     TileHeader *__restrict__ hdr) {
+                     TileHeader *__restrict__ hdr, uint32_t head) {
+  // `head` (0-3): the buffers were rounded down to 16 B, so virtual elements
+  // [0, head) precede the caller's data; they read as 0 (neutral for the sum,
+  // never selected) and are never stored.  Only tile 0 is affected.
   extern __shared__ __align__(128) uint8_t dyn_smem[];
   __shared__ TmShared sh;
   int32_t *stages = reinterpret_cast<int32_t *>(dyn_smem);
@@ -242,7 +245,7 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       t = __shfl_sync(kFull, t, 0);
       int32_t *stage = stages + s * TM_TILE;
       const uint64_t tbase = uint64_t(t) * TM_TILE;
-      if (t != kNoTileTm && tbase + TM_TILE <= n) {
+      if (t != kNoTileTm && tbase + TM_TILE <= n) {  // (tile 0's masked head: aggregator)
         if (lane == 0) {
           sh.stage_tile[s] = t;
           TM_STAMP(t, 0);
@@ -251,7 +254,8 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
         }
       } else {
         if (t != kNoTileTm)  // ragged last tile: guarded copy, zero padding
-          for (uint32_t e = lane; e < TM_TILE; e += 32) stage[e] = tbase + e < n ? in[tbase + e] : 0;
+          for (uint32_t e = lane; e < TM_TILE; e += 32)
+            stage[e] = (tbase + e < n && tbase + e >= head) ? in[tbase + e] : 0;
         __syncwarp();
         if (lane == 0) {
           sh.stage_tile[s] = t;
@@ -296,7 +300,14 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
           uint32_t v[32], sum = 0;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const uint4 x = *reinterpret_cast<const uint4 *>(stage + (8 * (TMUL * h + m) + j) * 128);
+            uint4 x = *reinterpret_cast<const uint4 *>(stage + (8 * (TMUL * h + m) + j) * 128);
+            if (head && t == 0 && q == 0 && h == 0 && m == 0 && j == 0 && lane == 0) {
+              // the 0-3 virtual elements before the caller's data (the TMA
+              // loaded the whole 16-byte-aligned tile)
+              if (head > 0) x.x = 0;
+              if (head > 1) x.y = 0;
+              if (head > 2) x.z = 0;
+            }
             v[4 * j] = x.x; v[4 * j + 1] = x.y; v[4 * j + 2] = x.z; v[4 * j + 3] = x.w;
             if (COMPACT)
               sum += (int32_t(x.x) > 0) + (int32_t(x.y) > 0) + (int32_t(x.z) > 0) + (int32_t(x.w) > 0);
@@ -365,7 +376,7 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive1(&sh.freed[p]);
-      const bool full = uint64_t(t + 1) * TM_TILE <= n;
+      const bool full = uint64_t(t + 1) * TM_TILE <= n && (t > 0 || head == 0);
       const uint64_t base0 = uint64_t(t) * TM_TILE + q * (QVEC * 128) + (8 * TMUL * h) * 128 + lane * 4;
       uint32_t loc[TMUL][8];  // scan: chunk add (local); compaction: chunk write position (local)
       uint32_t run = 0;
@@ -432,7 +443,7 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
             } else {
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                if (e + k < n) out[e + k] = int32_t(x[k] + add);
+                if (e + k < n && e + k >= head) out[e + k] = int32_t(x[k] + add);
             }
           } else {
             uint32_t pos = off + loc[m][j];
@@ -515,13 +526,17 @@ bool tmem_scan_enabled() {
   return e == nullptr || e[0] != '0';
 }
 
+// `in` / `out` need only 4-byte alignment: they are rounded down to 16 B and
+// the 0-3 leading elements masked (scan: in and out must share the offset).
 cudaError_t launch_scan_tmem_i32(const int32_t *in, int32_t *out, uint64_t n,
                                  const int32_t *carry, void *ws, cudaStream_t s) {
   auto *hdr = reinterpret_cast<TileHeader *>(ws);
   auto *desc = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + kTileWsHeader);
-  const uint32_t nt = uint32_t((n + TM_TILE - 1) / TM_TILE);
+  const uint32_t head = uint32_t((reinterpret_cast<uintptr_t>(in) & 15u) / 4u);
+  const uint64_t nv = n + head;
+  const uint32_t nt = uint32_t((nv + TM_TILE - 1) / TM_TILE);
   tile_tmem_kernel<false><<<tmem_grid<false>(nt), TM_THREADS, tm_smem<false>(), s>>>(
-      in, out, n, nt, carry, nullptr, desc, hdr);
+      in - head, out - head, nv, nt, carry, nullptr, desc, hdr, head);
   return cudaGetLastError();
 }
 
@@ -529,9 +544,11 @@ cudaError_t launch_compact_tmem_i32(const int32_t *in, uint64_t n, int32_t *out,
                                     void *ws, cudaStream_t s) {
   auto *hdr = reinterpret_cast<TileHeader *>(ws);
   auto *desc = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + kTileWsHeader);
-  const uint32_t nt = uint32_t((n + TM_TILE - 1) / TM_TILE);
+  const uint32_t head = uint32_t((reinterpret_cast<uintptr_t>(in) & 15u) / 4u);
+  const uint64_t nv = n + head;
+  const uint32_t nt = uint32_t((nv + TM_TILE - 1) / TM_TILE);
   tile_tmem_kernel<true><<<tmem_grid<true>(nt), TM_THREADS, tm_smem<true>(), s>>>(
-      in, out, n, nt, nullptr, count, desc, hdr);
+      in - head, out, nv, nt, nullptr, count, desc, hdr, head);
   return cudaGetLastError();
 }
 

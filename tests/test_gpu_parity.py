@@ -544,3 +544,30 @@ def test_c4_c5_reference_pins_on_gpu(ops, golden, monkeypatch, tmem):
         else:
             bins = host(ops.histogram256_u8(dev(a))).view(np.uint64)
             assert np.array_equal(bins.astype(np.int64), g[f"{tag}_bins"].astype(np.int64)), tag
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+@pytest.mark.parametrize("n", [1, 3, 5, 8189, 8192, 8195, 3 * 8192 + 1, (1 << 20) + 3])
+def test_tmem_kernel_misaligned_views(ops, k, n):
+    """4-byte-aligned views (x[k:]) take the TMEM kernel with the first 0-3
+    virtual elements masked: nothing before the view is stored, results equal
+    the oracle; the scan also in place and with a carry."""
+    a = synthetic.generate("i32_full", n + 8, seed=n + k)
+    x = dev(a)
+    y = torch.zeros(n + 8, dtype=torch.int32, device="cuda")
+    got = ops.scan_inclusive_i32(x[k:k + n], out=y[k:k + n])
+    assert np.array_equal(host(got), no.scan_inclusive_i32(a[k:k + n]))
+    assert not host(y[:k]).any() and not host(y[k + n:]).any()  # no stray stores
+    carry = torch.tensor([99], dtype=torch.int32, device="cuda")
+    z = dev(a)
+    ops.scan_inclusive_i32(z[k:k + n], out=z[k:k + n], carry=carry)
+    zz = host(z)
+    assert np.array_equal(zz[k:k + n], no.scan_inclusive_i32(a[k:k + n], carry=99))
+    assert np.array_equal(zz[:k], a[:k]) and np.array_equal(zz[k + n:], a[k + n:])
+    for ko in (0, 1, 3):  # compaction: any output offset
+        buf = torch.full((n + 8,), -7, dtype=torch.int32, device="cuda")
+        out, cnt = ops.compact_gt0_i32(x[k:k + n], out=buf[ko:ko + n])
+        want = no.compact_gt0_i32(a[k:k + n])
+        m = int(host(cnt)[0])
+        assert m == len(want) and np.array_equal(host(out)[:m], want)
+        assert (host(buf[:ko]) == -7).all()
