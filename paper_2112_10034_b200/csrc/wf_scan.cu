@@ -525,9 +525,9 @@ cudaError_t launch_scan_i32(const int32_t *in, int32_t *out, uint64_t n,
   auto *desc = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + kTileWsHeader);
   const bool aligned = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u) == 0;
   if (aligned && two_pass_usable(n)) return launch_scan2p_i32(in, out, n, carry, ws, s);
-  // the TMEM kernel masks a common 16-byte misalignment of in and out
-  const bool same_offset = ((reinterpret_cast<uintptr_t>(in) ^ reinterpret_cast<uintptr_t>(out)) & 15u) == 0;
-  if (same_offset && tmem_scan_enabled()) return launch_scan_tmem_i32(in, out, n, carry, ws, s);
+  // the TMEM kernel takes any 4-byte-aligned in/out (masked head, scalar
+  // stores when the output's 16-byte offset differs)
+  if (tmem_scan_enabled()) return launch_scan_tmem_i32(in, out, n, carry, ws, s);
   if (aligned && persistent_enabled()) {
     const uint64_t pt = (n + PTILE - 1) / PTILE;
     const int grid = persistent_grid<false>(uint32_t(pt));

@@ -190,10 +190,12 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
     tile_tmem_kernel(const int32_t *__restrict__ in, int32_t *__restrict__ out, uint64_t n,
                      uint32_t ntiles, const int32_t *__restrict__ carry_in,
                      uint64_t *__restrict__ count, uint64_t *__restrict__ desc,
-                     TileHeader *__restrict__ hdr, uint32_t head) {
+                     TileHeader *__restrict__ hdr, uint32_t head, bool vec_out) {
   // `head` (0-3): the buffers were rounded down to 16 B, so virtual elements
   // [0, head) precede the caller's data; they read as 0 (neutral for the sum,
   // never selected) and are never stored.  Only tile 0 is affected.
+  // `vec_out` false (scan output at a different 16-byte offset than the
+  // input): every tile is stored with scalar stores.
   extern __shared__ __align__(128) uint8_t dyn_smem[];
   __shared__ TmShared sh;
   int32_t *stages = reinterpret_cast<int32_t *>(dyn_smem);
@@ -376,7 +378,7 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive1(&sh.freed[p]);
-      const bool full = uint64_t(t + 1) * TM_TILE <= n && (t > 0 || head == 0);
+      const bool full = vec_out && uint64_t(t + 1) * TM_TILE <= n && (t > 0 || head == 0);
       const uint64_t base0 = uint64_t(t) * TM_TILE + q * (QVEC * 128) + (8 * TMUL * h) * 128 + lane * 4;
       uint32_t loc[TMUL][8];  // scan: chunk add (local); compaction: chunk write position (local)
       uint32_t run = 0;
@@ -526,8 +528,9 @@ bool tmem_scan_enabled() {
   return e == nullptr || e[0] != '0';
 }
 
-// `in` / `out` need only 4-byte alignment: they are rounded down to 16 B and
-// the 0-3 leading elements masked (scan: in and out must share the offset).
+// `in` / `out` need only 4-byte alignment: the input is rounded down to 16 B
+// and its 0-3 leading elements masked; a scan output at another 16-byte
+// offset is written with scalar stores.
 cudaError_t launch_scan_tmem_i32(const int32_t *in, int32_t *out, uint64_t n,
                                  const int32_t *carry, void *ws, cudaStream_t s) {
   auto *hdr = reinterpret_cast<TileHeader *>(ws);
@@ -536,7 +539,8 @@ cudaError_t launch_scan_tmem_i32(const int32_t *in, int32_t *out, uint64_t n,
   const uint64_t nv = n + head;
   const uint32_t nt = uint32_t((nv + TM_TILE - 1) / TM_TILE);
   tile_tmem_kernel<false><<<tmem_grid<false>(nt), TM_THREADS, tm_smem<false>(), s>>>(
-      in - head, out - head, nv, nt, carry, nullptr, desc, hdr, head);
+      in - head, out - head, nv, nt, carry, nullptr, desc, hdr, head,
+      ((reinterpret_cast<uintptr_t>(in) ^ reinterpret_cast<uintptr_t>(out)) & 15u) == 0);
   return cudaGetLastError();
 }
 
@@ -548,7 +552,7 @@ cudaError_t launch_compact_tmem_i32(const int32_t *in, uint64_t n, int32_t *out,
   const uint64_t nv = n + head;
   const uint32_t nt = uint32_t((nv + TM_TILE - 1) / TM_TILE);
   tile_tmem_kernel<true><<<tmem_grid<true>(nt), TM_THREADS, tm_smem<true>(), s>>>(
-      in - head, out, nv, nt, nullptr, count, desc, hdr, head);
+      in - head, out, nv, nt, nullptr, count, desc, hdr, head, false);
   return cudaGetLastError();
 }
 

@@ -17,7 +17,7 @@ def t(fn):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(); fn(); e.record(); torch.cuda.synchronize(); ts.append(s.elapsed_time(e) * 1e3)
     return round(statistics.median(ts), 1)
-for off in (0, 1):
-    xv, yv = x[off:off + n], y[off:off + n]
-    print(json.dumps({"offset_elems": off, "scan_us": t(lambda: ops.scan_inclusive_i32(xv, yv)),
+for off, yoff in ((0, 0), (1, 1), (1, 2)):
+    xv, yv = x[off:off + n], y[yoff:yoff + n]
+    print(json.dumps({"offset_elems": off, "out_offset": yoff, "scan_us": t(lambda: ops.scan_inclusive_i32(xv, yv)),
                       "compact_us": t(lambda: ops.compact_gt0_i32(xv, yv))}))
