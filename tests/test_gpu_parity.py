@@ -228,12 +228,18 @@ def test_compact_full_config(ops):
 
 @pytest.mark.parametrize("n", [1, 4097, 8192 * 5 + 3, (1 << 20) + 3, (1 << 22) + 13])
 def test_smem_stage_kernel_scan_compact(ops, monkeypatch, n):
-    """The pre-TMEM persistent kernel stays selectable (A/B baseline)."""
+    """The pre-TMEM kernels stay selectable (A/B baseline): the smem-stage
+    persistent kernel (aligned) and the register-tile kernel (4-byte views)."""
     monkeypatch.setenv("WF_SCAN_TMEM", "0")
     a = synthetic.generate("i32_full", n, seed=n + 9)
     assert np.array_equal(host(ops.scan_inclusive_i32(dev(a))), no.scan_inclusive_i32(a))
     out, cnt = ops.compact_gt0_i32(dev(a))
     want = no.compact_gt0_i32(a)
+    assert int(host(cnt)[0]) == len(want) and np.array_equal(host(out)[:len(want)], want)
+    # 4-byte-aligned views: the register-tile single-pass kernels
+    b = dev(np.concatenate([[5], a]).astype(np.int32))
+    assert np.array_equal(host(ops.scan_inclusive_i32(b[1:])), no.scan_inclusive_i32(a))
+    out, cnt = ops.compact_gt0_i32(b[1:])
     assert int(host(cnt)[0]) == len(want) and np.array_equal(host(out)[:len(want)], want)
 
 
