@@ -278,7 +278,7 @@ def time_launches(fn, steps: int, warmup: int, flush=None):
 
 def run_ours(args, rank, world, local) -> dict | None:
     import torch
-    from paper_2112_10034_b200 import _lib, distributed as wd, ops
+    from paper_2112_10034_b200 import distributed as wd, ops
 
     peak, peak_src = measured_peak()
     dev = torch.device("cuda", local)

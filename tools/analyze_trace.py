@@ -2,7 +2,6 @@
 R_{i-W} (the window chain) and the latest aggregate in the window."""
 import sys
 import numpy as np
-from numpy.lib.stride_tricks import sliding_window_view
 
 for f in sys.argv[1:]:
     W = int(f.split("=")[1]) if "=" in f else 32

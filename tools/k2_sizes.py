@@ -1,7 +1,6 @@
 """K2 time vs shard size (the per-GPU work at 1/2/4/8 GPUs under strong
 scaling of the 2^30 job), plain and with the fused exchange (world 1)."""
 import json
-import statistics
 import sys
 from pathlib import Path
 

@@ -1,4 +1,4 @@
-import sys, time, threading, subprocess
+import time, threading, subprocess
 import faulthandler; faulthandler.enable()
 import pynvml as nv
 nv.nvmlInit()

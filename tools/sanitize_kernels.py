@@ -5,7 +5,6 @@ import sys
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2112_10034_b200 import ops  # noqa: E402
