@@ -37,11 +37,11 @@ N_C2 = 1 << 30
 N_C3 = 1 << 28
 N_C4 = 1 << 28
 N_C5 = 1 << 32
-# C2 does not pin a block size (C1 does: 256).  1024-thread CTAs look 4 %
-# faster in a back-to-back launch loop (tools/k2_grid3.py) but not under the
-# bench's per-step event timing (0.619-0.624 vs 0.616 ms on the same box,
-# profiles/r01_reduce_experiments.md), so 256 stays.
-BLOCK_C2 = int(os.environ.get("WF_BENCH_BLOCK_C2", "256"))
+# C2 does not pin a block size (C1 does: 256).  Back-to-back steps at 2^30:
+# 256-thread CTAs 615 us, 512 598 us from the first steps on, 1024 587 us but
+# only after ~25 launches (606-612 before; tools/bench_loop_probe2.py,
+# profiles/r01_reduce_experiments.md) — 512 is the robust choice.
+BLOCK_C2 = int(os.environ.get("WF_BENCH_BLOCK_C2", "512"))
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 
 
@@ -299,30 +299,27 @@ def run_ours(args, rank, world, local) -> dict | None:
         log(f"rank {rank}: partial exchange = {exchange}")
 
     # ---- headline: K2 step over the 2^30 job, device-resident inputs ------
-    kern = []
+    # The timed region is K back-to-back steps bracketed by two events (no
+    # per-step events: they would serialise kernel boundaries that a real
+    # stream of steps overlaps).  When a step is one kernel (1 GPU, or the
+    # fused peer-memory exchange) the kernel's average duration IS the step
+    # time; with the NCCL fallback the kernel alone is timed in a second loop.
     launches = 0
 
-    def step(record):
+    def step():
         nonlocal launches
-        if record:
-            s = torch.cuda.Event(enable_timing=True)
-            e = torch.cuda.Event(enable_timing=True)
-            s.record()
         if peer is not None:  # one kernel: local reduce + exchange + fold
             part = peer.reduce_sum_f32(x, block=BLOCK_C2)
         else:
             part = ops.reduce_sum_f32(x, block=BLOCK_C2)
         launches += 1
-        if record:
-            e.record()
-            kern.append((s, e))
         if world > 1 and peer is None:
             ops.fold(wd.exchange(part).reshape(-1))
             launches += 1
         return part
 
     for _ in range(args.warmup):
-        step(False)
+        step()
     launches = 0
     barrier_sync(world)
     with ClockSampler(local) as clk:
@@ -330,11 +327,20 @@ def run_ours(args, rank, world, local) -> dict | None:
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()
         for _ in range(args.steps):
-            step(True)
+            step()
         t1.record()
         barrier_sync(world)
     step_ms = t0.elapsed_time(t1) / args.steps
-    kern_ms = statistics.mean(s.elapsed_time(e) for s, e in kern)
+    if world == 1 or peer is not None:
+        kern_ms, kern_timing = step_ms, "timed region / steps (one kernel per step)"
+    else:
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(args.steps):
+            ops.reduce_sum_f32(x, block=BLOCK_C2)
+        s1.record()
+        torch.cuda.synchronize()
+        kern_ms, kern_timing = s0.elapsed_time(s1) / args.steps, "separate back-to-back K2 loop"
     step_ms_max = max_over_ranks(step_ms, world)
     value = N_C2 / (step_ms_max * 1e-3) / 1e9
     achieved = 4.0 * n_local / (kern_ms * 1e-3) / 1e9
@@ -408,6 +414,7 @@ def run_ours(args, rank, world, local) -> dict | None:
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                      "kernel": "reduce_sum_f32 (K2)", "peak_source": peak_src,
+                     "kernel_timing": kern_timing,
                      "algorithmic_bytes_per_launch": 4 * n_local},
         "cpu_baseline": cpu,
         "e2e": {"value": round(N_C2 / (e2e_ms_max * 1e-3) / 1e9, 4), "unit": "Gelem/s",
