@@ -257,18 +257,29 @@ def cpu_baseline_kernel(kind: str, budget_s: float) -> dict:
 
 # ---- GPU timing helpers -----------------------------------------------------
 def time_launches(fn, steps: int, warmup: int, flush=None):
-    """Per-launch CUDA-event times (ms) on the current stream."""
+    """Per-launch times (ms) on the current stream.  Without a flush the
+    `steps` launches run back to back between two events (the steady state of
+    a stream of calls; inputs larger than L2 need no flush) and the average
+    is returned for each; with a flush (C1) every launch is bracketed by its
+    own events right after the L2 flush."""
     import torch
     for _ in range(warmup):
         if flush is not None:
             flush()
         fn()
     torch.cuda.synchronize()
+    if flush is None:
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(steps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        return [s.elapsed_time(e) / steps] * steps
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(steps)]
     for s, e in evs:
-        if flush is not None:
-            flush()
+        flush()
         s.record()
         fn()
         e.record()
