@@ -23,6 +23,10 @@ the reference's own code paths:
     thread per bin counting i32-widened bytes), run through run_oracle and
     launch(hybrid_transform(...)) — reference-produced vectors that pin the
     results K4 / K5 must reproduce
+  - random_kernels.json: 200 kernels from the reference's own fuzzer
+    (randgen.generate_kernel, the inputs of tests/test_random_diff.py:17-27)
+    with their run_oracle outputs — cross-checked against the transformed
+    path, as the reference's differential test does
   - corpus.npz: all 17 corpus kernels (corpus.py) through run_oracle
   - corpus_traces.json: run_oracle ExecTrace counts for the same runs and the
     cfg/build.py uid -> IR-class catalogue of every kernel (--traces-only
@@ -231,6 +235,28 @@ def c4c5_pin() -> dict:
     return out
 
 
+def random_kernels() -> dict:
+    """tests/test_random_diff.py:13-43 restated: seeds 0-149 (grid 1), 150-179
+    (specialized: same outputs), 180-199 (grid 3); warp 4, block 8."""
+    from warpfold.randgen import generate_kernel
+    warp, block = 4, 8
+    out = []
+    for seed in range(200):
+        grid = 3 if seed >= 180 else 1
+        src = generate_kernel(seed, warp_size=warp, block_size=block)
+        n = grid * block
+        gin = (np.arange(n) * 3 - 7).astype(np.int32)
+        o1 = _run("oracle", src, grid, block, [("i32", gin), ("i32", np.zeros(n))], [2], warp=warp)
+        o2 = _run("launch", src, grid, block, [("i32", gin), ("i32", np.zeros(n))], [2], warp=warp)
+        assert all(np.array_equal(a, b) for a, b in zip(o1, o2)), seed
+        out.append({"seed": seed, "grid": grid, "block": block, "warp": warp, "scalar": 2,
+                    "source": src, "gin": gin.tolist(),
+                    "gin_out": o1[0].astype(np.int32).tolist(),
+                    "gout": o1[1].astype(np.int32).tolist()})
+    return {"source": "warpfold randgen.generate_kernel + run_oracle (cross-checked with "
+                      "launch(hybrid_transform(...)))", "kernels": out}
+
+
 def corpus_golden() -> tuple[dict, dict]:
     arrays, manifest = {}, {}
     for k in corpus.ALL:
@@ -286,6 +312,9 @@ def corpus_traces() -> dict:
 
 
 def main() -> None:
+    if "--random-only" in sys.argv:
+        (HERE / "random_kernels.json").write_text(json.dumps(random_kernels()))
+        return
     if "--c4c5-only" in sys.argv:
         np.savez_compressed(HERE / "c4c5_pin.npz", **c4c5_pin())
         (HERE / "C4_COMPACT_SERIAL.spk").write_text(C4_COMPACT_SERIAL)
@@ -300,6 +329,7 @@ def main() -> None:
     np.savez_compressed(HERE / "c1c2_pin.npz", **c1c2_pin())
     np.savez_compressed(HERE / "c3_pin.npz", **c3_pin())
     np.savez_compressed(HERE / "c4c5_pin.npz", **c4c5_pin())
+    (HERE / "random_kernels.json").write_text(json.dumps(random_kernels()))
     arrays, manifest = corpus_golden()
     np.savez_compressed(HERE / "corpus.npz", **arrays)
     (HERE / "corpus_manifest.json").write_text(json.dumps(manifest, indent=1))

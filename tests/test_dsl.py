@@ -149,3 +149,20 @@ def test_cli_transform_emits_cuda(tmp_path):
     bad = tmp_path / "bad.spk"
     bad.write_text("__global__ void k(global i32* a) { a[0] = 1 }")
     assert main(["transform", str(bad)]) == 3  # parse error -> EXIT_TRANSFORM
+
+
+def test_reference_fuzzer_kernels_parse_check_and_generate():
+    """Every kernel of the reference's fuzzer (tests/golden/random_kernels.json)
+    goes through this front end: parse, check, CUDA codegen at warp size 4."""
+    import json
+    from pathlib import Path
+    from paper_2112_10034_b200.dsl import codegen, parse_module
+    from paper_2112_10034_b200.dsl.checker import check_kernel
+    cases = json.loads((Path(__file__).resolve().parent / "golden" / "random_kernels.json")
+                       .read_text())["kernels"]
+    assert len(cases) == 200
+    for c in cases:
+        kernel = parse_module(c["source"]).kernel()
+        table = check_kernel(kernel)
+        src, _ = codegen.generate(kernel, table, warp_size=c["warp"])
+        assert "__global__" in src

@@ -179,3 +179,20 @@ def test_masked_collectives_and_dynamic_smem(wf):
     bal = semantics.collective("ballot", (a * 2 > 0).astype(np.int32), None, 0, 32, 32, mask)
     want = np.where(np.arange(32) % 2 == 0, sh + 1000 * bal, 0)
     assert np.array_equal(o, want)
+
+
+RANDOM = json.loads((GOLDEN / "random_kernels.json").read_text())["kernels"]
+
+
+@pytest.mark.parametrize("case", RANDOM, ids=lambda c: f"seed{c['seed']}")
+def test_reference_fuzzer_kernels_bit_exact(wf, case):
+    """The reference's own fuzzer kernels (randgen.generate_kernel, the inputs
+    of its tests/test_random_diff.py) compiled natively at warp size 4:
+    gin and gout equal run_oracle's (tests/golden/random_kernels.json)."""
+    cfg = wf.LaunchConfig(grid_size=case["grid"], block_size=case["block"], warp_size=case["warp"])
+    n = case["grid"] * case["block"]
+    gin, gout = _run(wf, case["source"], cfg,
+                     [("i32", np.array(case["gin"], dtype=np.int32)), ("i32", np.zeros(n))],
+                     [case["scalar"]], specialize=case["seed"] >= 150 and case["seed"] < 180)
+    assert gin.view(np.int32).tolist() == case["gin_out"], case["source"]
+    assert gout.view(np.int32).tolist() == case["gout"], case["source"]
