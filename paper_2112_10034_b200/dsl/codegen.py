@@ -259,10 +259,15 @@ class CudaGen:
         return f"{fn}({a}, {b})", I32
 
     def mask(self, e) -> str:
+        # a collective synchronises its LOGICAL warp only (the W-lane segment
+        # of the hardware warp): at W < 32 one segment may execute it inside a
+        # branch its neighbour skips (legal in the reference, whose aligned-
+        # barrier rule is per logical warp), so the other segment's lanes must
+        # not be named in the *_sync mask
         if e is None:
-            return "wf_present()"
+            return "(wf_present() & wf_segbits())"
         m, _ = self.expr(e)
-        return f"((unsigned)({m}) & wf_present())"
+        return f"((unsigned)({m}) & wf_present() & wf_segbits())"
 
     def collective(self, e: n.CollectiveCall) -> tuple[str, str]:
         # operands first, then the collective's own uid (cfg/build.py:153-159)

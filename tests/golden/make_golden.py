@@ -27,6 +27,8 @@ the reference's own code paths:
     (randgen.generate_kernel, the inputs of tests/test_random_diff.py:17-27)
     with their run_oracle outputs — cross-checked against the transformed
     path, as the reference's differential test does
+  - acceptance_fuzz.json: the 1000 fuzzer kernels of the reference's
+    acceptance criterion 5 with their run_oracle outputs
   - corpus.npz: all 17 corpus kernels (corpus.py) through run_oracle
   - corpus_traces.json: run_oracle ExecTrace counts for the same runs and the
     cfg/build.py uid -> IR-class catalogue of every kernel (--traces-only
@@ -257,6 +259,20 @@ def random_kernels() -> dict:
                       "launch(hybrid_transform(...)))", "kernels": out}
 
 
+def acceptance_fuzz() -> dict:
+    """The reference's acceptance criterion 5 (tests/test_acceptance.py:
+    218-236): 1000 fuzzer kernels at warp 4, block 8, gin = 5*i - 9."""
+    from warpfold.randgen import generate_kernel
+    out = []
+    for seed in range(1000):
+        src = generate_kernel(seed, warp_size=4, block_size=8)
+        gin = (np.arange(8) * 5 - 9).astype(np.int32)
+        o = _run("oracle", src, 1, 8, [("i32", gin), ("i32", np.zeros(8))], [2], warp=4)
+        out.append([seed, src, o[0].astype(np.int32).tolist(), o[1].astype(np.int32).tolist()])
+    return {"source": "warpfold tests/test_acceptance.py criterion 5 inputs; outputs from "
+                      "run_oracle", "cases": out}
+
+
 def corpus_golden() -> tuple[dict, dict]:
     arrays, manifest = {}, {}
     for k in corpus.ALL:
@@ -314,6 +330,7 @@ def corpus_traces() -> dict:
 def main() -> None:
     if "--random-only" in sys.argv:
         (HERE / "random_kernels.json").write_text(json.dumps(random_kernels()))
+        (HERE / "acceptance_fuzz.json").write_text(json.dumps(acceptance_fuzz()))
         return
     if "--c4c5-only" in sys.argv:
         np.savez_compressed(HERE / "c4c5_pin.npz", **c4c5_pin())
@@ -330,6 +347,7 @@ def main() -> None:
     np.savez_compressed(HERE / "c3_pin.npz", **c3_pin())
     np.savez_compressed(HERE / "c4c5_pin.npz", **c4c5_pin())
     (HERE / "random_kernels.json").write_text(json.dumps(random_kernels()))
+    (HERE / "acceptance_fuzz.json").write_text(json.dumps(acceptance_fuzz()))
     arrays, manifest = corpus_golden()
     np.savez_compressed(HERE / "corpus.npz", **arrays)
     (HERE / "corpus_manifest.json").write_text(json.dumps(manifest, indent=1))

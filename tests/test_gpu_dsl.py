@@ -196,3 +196,20 @@ def test_reference_fuzzer_kernels_bit_exact(wf, case):
                      [case["scalar"]], specialize=case["seed"] >= 150 and case["seed"] < 180)
     assert gin.view(np.int32).tolist() == case["gin_out"], case["source"]
     assert gout.view(np.int32).tolist() == case["gout"], case["source"]
+
+
+@pytest.mark.slow
+def test_reference_acceptance_fuzz_1000_kernels(wf):
+    """The reference's acceptance criterion 5 (tests/test_acceptance.py:218-236)
+    on the GPU: 1000 fuzzer kernels at warp size 4, zero divergences from
+    run_oracle (tests/golden/acceptance_fuzz.json)."""
+    cases = json.loads((GOLDEN / "acceptance_fuzz.json").read_text())["cases"]
+    assert len(cases) == 1000
+    cfg = wf.LaunchConfig(grid_size=1, block_size=8, warp_size=4)
+    gin0 = (np.arange(8) * 5 - 9).astype(np.int32)
+    bad = []
+    for seed, src, want_gin, want_gout in cases:
+        gin, gout = _run(wf, src, cfg, [("i32", gin0), ("i32", np.zeros(8))], [2])
+        if gin.view(np.int32).tolist() != want_gin or gout.view(np.int32).tolist() != want_gout:
+            bad.append(seed)
+    assert not bad, f"{len(bad)} of 1000 kernels diverge, first seeds {bad[:10]}"
