@@ -491,6 +491,18 @@ def per_kernel(args, rank, world, local, dev, peak) -> dict:
     t = time_launches(lambda: wd.compact_gt0_i32(x, out, peer=pc), steps, warm)
     res["c4_compact_i32"] = stats(t, hi - lo, 6, N_C4)
     res["c4_compact_i32"]["bytes_per_elem_note"] = "4 B read + 4 B x selectivity (~0.5) written"
+    # also 0 %, 1 % and 100 % selectivity (same n, i32_select)
+    variants = {}
+    for permille in (0, 10, 1000):
+        ops.fill_synthetic("i32_select", hi - lo, seed=0, base=lo, param=permille, out=x)
+        t = time_launches(lambda: wd.compact_gt0_i32(x, out, peer=pc), steps, warm)
+        ms = statistics.mean(t)
+        bpe = 4 + 4 * permille / 1000
+        variants[f"{permille / 10:g}%"] = {
+            "kernel_us": round(ms * 1e3, 2),
+            "gbs": round(bpe * (hi - lo) / (ms * 1e-3) / 1e9, 1),
+            "gelem_s": round(N_C4 / (max_over_ranks(ms, world) * 1e-3) / 1e9, 3)}
+    res["c4_compact_i32"]["selectivity_variants"] = variants
     del x, y, out
     torch.cuda.empty_cache()
     # C5 histogram
@@ -498,6 +510,16 @@ def per_kernel(args, rank, world, local, dev, peak) -> dict:
     u = ops.fill_synthetic("u8_uniform", hi - lo, seed=0, base=lo, device=dev)
     t = time_launches(lambda: wd.histogram256_u8(u, peer=pc), steps, warm)
     res["c5_hist_u8"] = stats(t, hi - lo, 1, N_C5)
+    # also all-same-value and skewed (geometric) bytes
+    variants = {}
+    for gen in ("u8_const", "u8_geom"):
+        ops.fill_synthetic(gen, hi - lo, seed=0, base=lo, out=u)
+        t = time_launches(lambda: wd.histogram256_u8(u, peer=pc), steps, warm)
+        ms = statistics.mean(t)
+        variants[gen] = {"kernel_us": round(ms * 1e3, 2),
+                         "gbs": round((hi - lo) / (ms * 1e-3) / 1e9, 1),
+                         "gelem_s": round(N_C5 / (max_over_ranks(ms, world) * 1e-3) / 1e9, 3)}
+    res["c5_hist_u8"]["data_variants"] = variants
     if exchange is not None:
         for k in ("c3_scan_i32", "c4_compact_i32", "c5_hist_u8"):
             res[k]["exchange"] = exchange
