@@ -98,7 +98,13 @@ constexpr int NFG = WF_TM_NFG;
 constexpr int NFIN = 8 * NFG;             // per group: one finisher warp per tile eighth
 constexpr int W_LB = W_FIN + NFIN;        // look-back warps W_LB .. W_LB+NLB-1
 constexpr int W_PROD = W_LB + NLB;        // producer warp
-constexpr int TM_THREADS = (W_PROD + 1) * 32;
+#ifndef WF_TM_NAG
+#define WF_TM_NAG 1  // aggregator groups (4 warps each), taking stage items round-robin
+#endif
+constexpr int NAG = WF_TM_NAG;
+constexpr int W_AGG2 = ((W_PROD + 1 + 3) / 4) * 4;  // 2nd group: warp % 4 = TMEM lane quarter
+constexpr int TM_THREADS = (NAG == 2 ? W_AGG2 + 4 : W_PROD + 1) * 32;
+constexpr uint32_t kExitOnly = 0xfffffffdu;  // second stop item (NAG = 2): just leave
 #ifndef WF_TM_TMUL
 #define WF_TM_TMUL 1  // tile = 32 KiB x TMUL
 #endif
@@ -164,7 +170,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 }
 
 // named barrier over the 128 aggregator threads (id 1; id 0 is __syncthreads)
-__device__ __forceinline__ void agg_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void agg_sync(uint32_t grp) {
+  asm volatile("bar.sync %0, 128;" ::"r"(1u + grp) : "memory");
+}
 
 __device__ __forceinline__ void mbar_arrive1(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -264,20 +272,34 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
           mbar_arrive1(&sh.full[s]);
         }
       }
-      if (t == kNoTileTm) break;
+      if (t == kNoTileTm) {
+        if (NAG == 2) {  // the other aggregator group's stop item
+          const int s2 = int((i + 1) % S);
+          const uint32_t k2 = (i + 1) / S;
+          if (k2 > 0) mbar_wait(&sh.empty[s2], (k2 - 1) & 1u);
+          if (lane == 0) {
+            sh.stage_tile[s2] = kExitOnly;
+            mbar_arrive1(&sh.full[s2]);
+          }
+        }
+        break;
+      }
     }
-  } else if (warp < W_FIN) {
+  } else if (warp < W_FIN || (NAG == 2 && warp >= W_AGG2)) {
     // ----------------------------- aggregators ----------------------------
-    const uint32_t q = warp;  // tile quarter and TMEM lane quarter
+    const uint32_t q = warp & 3u;  // tile quarter and TMEM lane quarter
+    const uint32_t grp = (NAG == 2 && warp >= W_AGG2) ? 1u : 0u;
+    const bool leader = warp == (grp ? uint32_t(W_AGG2) : 0u) && lane == 0;
     const uint32_t tcol = sh.tmem_base + ((32u * q) << 16);
-    for (uint32_t i = 0;; ++i) {
+    for (uint32_t i = grp;; i += NAG) {
       const int s = int(i % S), p = int(i % P);
       const uint32_t kp = i / P;
       mbar_wait(&sh.full[s], (i / S) & 1u);
       const uint32_t t = sh.stage_tile[s];
+      if (t == kExitOnly) break;
       if (kp > 0) mbar_wait(&sh.freed[p], (kp - 1) & 1u);
       tc_fence_after();
-      if (threadIdx.x == 0 && t != kNoTileTm) TM_STAMP(t, 1);
+      if (leader && t != kNoTileTm) TM_STAMP(t, 1);
       if (t == kNoTileTm) {
         // one stop item per look-back warp (items i .. i+NLB-1); the finishers
         // stop at the first.  Slot p is free (waited above); the next NLB-1
@@ -286,7 +308,7 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
           const uint32_t ie = i + e;
           const int pe = int(ie % P);
           if (e > 0 && ie / P > 0) mbar_wait(&sh.freed[pe], (ie / P - 1) & 1u);
-          if (threadIdx.x == 0) {
+          if (leader) {
             sh.slot_tile[pe] = kNoTileTm;
             mbar_arrive1(&sh.parked[pe]);
           }
@@ -330,8 +352,8 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       }
       tmem_wait_st();
       tc_fence_before();
-      agg_sync();
-      if (threadIdx.x == 0) {
+      agg_sync(grp);
+      if (leader) {
         uint32_t a = 0;
 #pragma unroll
         for (int w = 0; w < 4; ++w) a += sh.slot_wtot[p][w][0] + sh.slot_wtot[p][w][1];
@@ -458,7 +480,7 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       if (COMPACT && t == ntiles - 1 && q == 0 && h == 0 && lane == 0) *count = uint64_t(prefix) + agg;
       if (q == 0 && h == 0 && lane == 0) TM_STAMP(t, 4);
     }
-  } else {
+  } else if (warp < W_PROD) {
     // ----------------------------- look-back ------------------------------
     const uint32_t me = warp - W_LB;
     for (uint32_t i = me;; i += NLB) {
