@@ -43,6 +43,7 @@ N_C5 = 1 << 32
 # profiles/r01_reduce_experiments.md) — 512 is the robust choice.
 BLOCK_C2 = int(os.environ.get("WF_BENCH_BLOCK_C2", "512"))
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+NOMINAL_HBM_GBS = 8000.0   # north_star / BASELINE.md §4: % of peak also vs 8.0 TB/s
 
 
 def log(*a):
@@ -387,6 +388,7 @@ def run_ours(args, rank, world, local) -> dict | None:
         per = per_kernel(args, rank, world, local, dev, peak)
     per["c2_reduce_f32"] = {"gelem_s": round(value, 3), "gbs": round(achieved, 1),
                             "frac_of_peak": round(achieved / peak, 4),
+                            "frac_of_8tbs": round(achieved / NOMINAL_HBM_GBS, 4),
                             "kernel_us": round(kern_ms * 1e3, 2), "n": N_C2,
                             "bytes_per_elem": 4}
     del x
@@ -424,6 +426,7 @@ def run_ours(args, rank, world, local) -> dict | None:
         },
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "frac_of_nominal_8tbs": round(achieved / NOMINAL_HBM_GBS, 4),
                      "kernel": "reduce_sum_f32 (K2)", "peak_source": peak_src,
                      "kernel_timing": kern_timing,
                      "algorithmic_bytes_per_launch": 4 * n_local},
@@ -458,7 +461,9 @@ def per_kernel(args, rank, world, local, dev, peak) -> dict:
         ms_max = max_over_ranks(ms, world)
         gbs = bytes_per_elem * n_elems / (ms * 1e-3) / 1e9
         return {"gelem_s": round(n_total / (ms_max * 1e-3) / 1e9, 3), "gbs": round(gbs, 1),
-                "frac_of_peak": round(gbs / peak, 4), "kernel_us": round(ms * 1e3, 2),
+                "frac_of_peak": round(gbs / peak, 4),
+                "frac_of_8tbs": round(gbs / NOMINAL_HBM_GBS, 4),
+                "kernel_us": round(ms * 1e3, 2),
                 "n": n_total, "bytes_per_elem": bytes_per_elem}
 
     # C1 (single GPU by definition): 2^20 int32, block 256, L2 flushed
@@ -469,6 +474,8 @@ def per_kernel(args, rank, world, local, dev, peak) -> dict:
                           flush=lambda: flush_buf.fill_(1))
         res["c1_reduce_i32"] = stats(t, N_C1, 4, N_C1)
         res["c1_reduce_i32"]["l2"] = "flushed (256 MiB write) before every launch"
+        res["c1_reduce_i32"]["bound"] = ("latency: 4 MiB is 0.6 us of HBM time; see "
+                                         "latency_context_us for the launch + atomic floor")
         # latency context for this 4 MiB (0.6 us of HBM time) kernel, same
         # flushed methodology: K1 on 4 elements (launch + one atomic) and the
         # library reduction torch.sum of the same input
