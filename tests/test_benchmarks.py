@@ -1,0 +1,53 @@
+"""The GPU mode-comparison bench (`python -m paper_2112_10034_b200 bench`,
+the reference's cli.py:128-151 / bench.py:53-126 analogue)."""
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+from paper_2112_10034_b200 import benchmarks as bm
+from paper_2112_10034_b200.__main__ import build_parser
+from paper_2112_10034_b200.config import LaunchConfig
+from paper_2112_10034_b200.dsl import hybrid_transform, specialize
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_parser_accepts_reference_bench_flags():
+    a = build_parser().parse_args(["bench", "--suite", "modes", "--iters", "10",
+                                   "--repeats", "2", "--json"])
+    assert (a.suite, a.iters, a.repeats, a.json) == ("modes", 10, 2, True)
+
+
+@pytest.mark.parametrize("name", bm.MODE_KERNELS)
+def test_mode_kernels_translate_both_ways(name):
+    k = bm._kernel(bm.MODE_SOURCES[name])
+    cfg = LaunchConfig(grid_size=1, block_size=32)
+    for mode in ("flat", "hier"):
+        assert "__global__" in hybrid_transform(k, cfg, mode=mode).cuda_source(cfg)
+
+
+def test_jit_kernel_specializes():
+    cfg = LaunchConfig(grid_size=1, block_size=32)
+    prog = specialize(hybrid_transform(bm._kernel(bm.JIT_SOURCE), cfg, mode="hier"), cfg)
+    assert prog.specialized == {"block_size": 32, "grid_size": 1}
+
+
+@pytest.mark.gpu
+def test_bench_cli_all_suites():
+    env = dict(os.environ, PYTHONPATH=str(ROOT))
+    r = subprocess.run([sys.executable, "-m", "paper_2112_10034_b200", "bench", "--json",
+                        "--iters", "20", "--repeats", "2", "--op-iters", "3"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert [row["kernel"] for row in res["modes"]] == list(bm.MODE_KERNELS)
+    assert all(row["flat_ms"] > 0 and row["hier_ms"] > 0 for row in res["modes"])
+    assert res["jit"]["specialized_ms"] > 0
+    assert len(res["ops"]) == sum(len(v[2]) for v in bm.OPS.values())
+    assert all(row["gelem_s"] > 0 for row in res["ops"])
+    assert [row["n_gpus"] for row in res["scaling"]] == [1] * 4

@@ -577,3 +577,17 @@ def test_tmem_kernel_misaligned_views(ops, k, n):
         m = int(host(cnt)[0])
         assert m == len(want) and np.array_equal(host(out)[:m], want)
         assert (host(buf[:ko]) == -7).all()
+
+
+@pytest.mark.gpu
+def test_ops_follow_the_current_torch_stream(ops):
+    """ops.* enqueue on the current stream (fast raw-handle lookup), including
+    inside a `torch.cuda.stream` context."""
+    side = torch.cuda.Stream()
+    assert ops._stream_handle() == torch.cuda.current_stream().cuda_stream
+    with torch.cuda.stream(side):
+        assert ops._stream_handle() == side.cuda_stream
+        x = torch.arange(1 << 20, dtype=torch.int32, device="cuda") % 7 - 3
+        out = ops.reduce_sum_i32(x)
+    side.synchronize()
+    assert int(out.item()) == int(x.long().sum())
