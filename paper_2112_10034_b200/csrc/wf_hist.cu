@@ -31,24 +31,55 @@ constexpr int BLOCK = kHistBlock;
 #endif
 constexpr int UNROLL = WF_HIST_UNROLL;
 
-__device__ __forceinline__ void count_word(uint32_t *col, uint32_t w) {
-  atomicAdd(col + ((w & 0xffu) << 5), 1u);
-  atomicAdd(col + (((w >> 8) & 0xffu) << 5), 1u);
-  atomicAdd(col + (((w >> 16) & 0xffu) << 5), 1u);
-  atomicAdd(col + ((w >> 24) << 5), 1u);
+#if WF_HIST_PRMT
+// Bin stride 256 B ([bin][64 words], lanes use the first 32): the byte
+// offset of (bin, lane) is (bin << 8) | (lane << 2), which ONE byte permute
+// assembles from the data word and lane*4 — PRMT + ATOMS per input byte
+// instead of SHF + LOP3 + IADD + ATOMS (the 32 KiB layout).  Measured
+// slower (686 vs 644 us at 2^32): the loop is bound by shared-atomic
+// wavefronts, not issue, and the 256 B stride costs ~9 % extra wavefronts
+// (146 M vs 134 M; the same 32 KiB code at WF_HIST_BINW=64 is as slow).
+// Kept as the documented negative result (profiles/r01_hist_experiments.md).
+constexpr uint32_t kBinWords = 64;
+__device__ __forceinline__ void count_word(uint32_t *sh, uint32_t lane4, uint32_t w) {
+  char *base = reinterpret_cast<char *>(sh);
+  atomicAdd(reinterpret_cast<uint32_t *>(base + __byte_perm(w, lane4, 0x5504)), 1u);
+  atomicAdd(reinterpret_cast<uint32_t *>(base + __byte_perm(w, lane4, 0x5514)), 1u);
+  atomicAdd(reinterpret_cast<uint32_t *>(base + __byte_perm(w, lane4, 0x5524)), 1u);
+  atomicAdd(reinterpret_cast<uint32_t *>(base + __byte_perm(w, lane4, 0x5534)), 1u);
 }
+__device__ __forceinline__ void count_byte(uint32_t *sh, uint32_t lane4, uint32_t b) {
+  atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(sh) + ((b << 8) | lane4)), 1u);
+}
+#else
+constexpr uint32_t kBinWords = WF_HIST_BINW;
+constexpr uint32_t kBinShift = WF_HIST_BINW == 64 ? 6 : 5;
+__device__ __forceinline__ void count_word(uint32_t *col, uint32_t w) {
+  atomicAdd(col + ((w & 0xffu) << kBinShift), 1u);
+  atomicAdd(col + (((w >> 8) & 0xffu) << kBinShift), 1u);
+  atomicAdd(col + (((w >> 16) & 0xffu) << kBinShift), 1u);
+  atomicAdd(col + ((w >> 24) << kBinShift), 1u);
+}
+#endif
 
 __global__ void __launch_bounds__(BLOCK, 2048 / BLOCK)
     hist256_kernel(const uint8_t *__restrict__ in, uint64_t n,
                    unsigned long long *__restrict__ bins, bool accumulate,
                    unsigned long long *__restrict__ accum,
                    uint32_t *__restrict__ ticket) {
-  extern __shared__ uint32_t sh[];  // [256][32]
-  for (uint32_t i = threadIdx.x; i < 256 * 32; i += BLOCK) sh[i] = 0u;
+  extern __shared__ uint32_t sh[];  // [256][kBinWords], lane l counts in word l
+  for (uint32_t i = threadIdx.x; i < 256 * kBinWords; i += BLOCK) sh[i] = 0u;
   __syncthreads();
 
-  const uint32_t lane = threadIdx.x & 31;
-  uint32_t *col = sh + lane;
+#if WF_HIST_PRMT
+  const uint32_t lane4 = (threadIdx.x & 31) << 2;
+#define WF_CNT4(w) count_word(sh, lane4, (w))
+#define WF_CNT1(b) count_byte(sh, lane4, (b))
+#else
+  uint32_t *col = sh + (threadIdx.x & 31);
+#define WF_CNT4(w) count_word(col, (w))
+#define WF_CNT1(b) atomicAdd(col + (uint32_t(b) << kBinShift), 1u)
+#endif
   const uint64_t gtid = uint64_t(blockIdx.x) * BLOCK + threadIdx.x;
   const uint64_t nthreads = uint64_t(gridDim.x) * BLOCK;
 
@@ -66,21 +97,23 @@ __global__ void __launch_bounds__(BLOCK, 2048 / BLOCK)
     for (int u = 0; u < UNROLL; ++u) q[u] = ldg_stream(vin + i + u * nthreads);
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
-      count_word(col, q[u].x);
-      count_word(col, q[u].y);
-      count_word(col, q[u].z);
-      count_word(col, q[u].w);
+      WF_CNT4(q[u].x);
+      WF_CNT4(q[u].y);
+      WF_CNT4(q[u].z);
+      WF_CNT4(q[u].w);
     }
   }
   for (; i < nvec; i += nthreads) {
     const uint4 q = ldg_stream(vin + i);
-    count_word(col, q.x);
-    count_word(col, q.y);
-    count_word(col, q.z);
-    count_word(col, q.w);
+    WF_CNT4(q.x);
+    WF_CNT4(q.y);
+    WF_CNT4(q.z);
+    WF_CNT4(q.w);
   }
-  if (gtid < head) atomicAdd(col + (uint32_t(in[gtid]) << 5), 1u);
-  if (tail0 + gtid < n) atomicAdd(col + (uint32_t(in[tail0 + gtid]) << 5), 1u);
+  if (gtid < head) WF_CNT1(in[gtid]);
+  if (tail0 + gtid < n) WF_CNT1(in[tail0 + gtid]);
+#undef WF_CNT4
+#undef WF_CNT1
   __syncthreads();
 
   // fold the 32 lane columns of each bin; rotation keeps the reads of a warp
@@ -89,7 +122,7 @@ __global__ void __launch_bounds__(BLOCK, 2048 / BLOCK)
     const uint32_t b = threadIdx.x;
     uint32_t s = 0;
 #pragma unroll 8
-    for (uint32_t l = 0; l < 32; ++l) s += sh[b * 32 + ((l + b) & 31u)];
+    for (uint32_t l = 0; l < 32; ++l) s += sh[b * kBinWords + ((l + b) & 31u)];
     if (s) atomicAdd(accum + b, (unsigned long long)s);
   }
   __shared__ bool am_last;

@@ -30,7 +30,13 @@ constexpr uint64_t kScanTile = uint64_t(kScanBlock) * kScanVec * 4;  // 4096
 #define WF_HIST_BLOCK 1024
 #endif
 constexpr int kHistBlock = WF_HIST_BLOCK;
-constexpr size_t kHistSmem = 256 * 32 * sizeof(uint32_t);  // 32 KiB
+#ifndef WF_HIST_PRMT
+#define WF_HIST_PRMT 0  // 1: 256 B bin stride, one PRMT per address (slower, wf_hist.cu)
+#endif
+#ifndef WF_HIST_BINW
+#define WF_HIST_BINW 32  // words per bin row in the non-PRMT layout (32 or 64)
+#endif
+constexpr size_t kHistSmem = 256 * (WF_HIST_PRMT ? 64 : WF_HIST_BINW) * sizeof(uint32_t);
 
 int sm_count(int device);
 int current_device();
