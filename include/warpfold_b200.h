@@ -217,7 +217,9 @@ int wf_fill_synthetic(int gen, void *out, uint64_t n, uint64_t seed,
  * caller-provided device staging buffer in double-buffered chunks, each
  * chunk's copy overlapping the previous chunk's kernel; the scalar result is
  * copied back into *host_out.  Synchronous (returns after the result is in
- * host memory).  staging_bytes >= 2 MiB. */
+ * host memory).  staging_bytes >= 2 MiB.  Concurrent calls on one device
+ * are serialised (they share the device's copy streams); calls on different
+ * devices run concurrently. */
 int wf_reduce_sum_f32_host(const float *host_in, uint64_t n, float *host_out,
                            void *staging, size_t staging_bytes, void *ws,
                            size_t ws_bytes, wf_stream_t stream);

@@ -95,6 +95,14 @@ struct CopyStreams {
 };
 static std::mutex g_streams_mu;
 static CopyStreams g_streams[64];
+// Host-buffer calls on one device share its copy streams and events, so they
+// are serialised per device (each call is synchronous and PCIe-bound anyway);
+// calls on different devices run concurrently.
+static std::mutex g_host_mu[64];
+static std::unique_lock<std::mutex> host_call_lock() {
+  const int dev = current_device();
+  return std::unique_lock<std::mutex>(g_host_mu[dev >= 0 && dev < 64 ? dev : 0]);
+}
 
 static int get_copy_streams(CopyStreams *&cs) {
   const int dev = current_device();
@@ -399,6 +407,7 @@ static int reduce_host(int op, const T *host_in, uint64_t n, T *host_out, void *
     return fail(WF_ERR_ARG, "staging buffer too small for n=%llu", (unsigned long long)n);
   int rc = check_ws(op, n, ws, ws_bytes);
   if (rc) return rc;
+  auto lk = host_call_lock();
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   uint64_t nchunks = 0;
   rc = stream_chunks(host_in, n, sizeof(T), staging, body, s,
@@ -445,6 +454,7 @@ int wf_histogram256_u8_host(const uint8_t *host_in, uint64_t n, uint64_t *host_b
     return fail(WF_ERR_ARG, "staging buffer must be at least 2 MiB");
   int rc = check_ws(WF_OP_HISTOGRAM256_U8, n, ws, ws_bytes);
   if (rc) return rc;
+  auto lk = host_call_lock();
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t body = (staging_bytes - 4096) & ~size_t(511);
   uint64_t *dbins = reinterpret_cast<uint64_t *>(static_cast<char *>(staging) + body);

@@ -484,6 +484,28 @@ def test_host_entry_points(ops):
     assert np.array_equal(ops.histogram256_u8_host(u), no.histogram256_u8(u))
 
 
+def test_host_entry_points_from_concurrent_threads(ops):
+    """Host-buffer calls from several threads on one device share the copy
+    streams (and, through ops, the staging buffer); the library serialises
+    them, so every thread gets its own exact result."""
+    from concurrent.futures import ThreadPoolExecutor
+    n = (40 << 20) + 3
+    arrays = [synthetic.generate("i32_full", n, seed=100 + t) for t in range(4)]
+    bytes_ = [synthetic.generate("u8_uniform", n, seed=200 + t) for t in range(4)]
+    want = [no.reduce_sum_i32(a) for a in arrays]
+    want_h = [no.histogram256_u8(u) for u in bytes_]
+
+    def work(t):
+        torch.cuda.set_device(0)
+        for _ in range(3):
+            assert ops.reduce_sum_i32_host(arrays[t]) == want[t]
+            assert np.array_equal(ops.histogram256_u8_host(bytes_[t]), want_h[t])
+        return True
+
+    with ThreadPoolExecutor(4) as ex:
+        assert all(ex.map(work, range(4)))
+
+
 @pytest.mark.slow
 def test_scan_beyond_2p32_elements(ops):
     """Maximum-size check: > 2^32 elements (16 GiB in + 16 GiB out), so tile
