@@ -36,6 +36,7 @@ from .config import LaunchConfig
 from .memory import DeviceMemory
 
 NOMINAL_HBM_GBS = 8000.0  # north_star's 8 TB/s
+L2_BYTES = 126 << 20      # B200 L2: inputs at or below this stay resident across repeats
 
 # Barrier-free kernels for the modes suite (the reference uses the same four
 # names, bench.py:24); written here for the GPU bench.
@@ -244,7 +245,8 @@ def bench_ops(ops_=tuple(OPS), log2_sizes=None, iters: int = 20, repeats: int = 
             gbs = n * bpe / t / 1e9
             rows.append({"op": op, "n": n, "us": t * 1e6, "gelem_s": n / t / 1e9,
                          "gbs": gbs, "frac_of_8tbs": gbs / NOMINAL_HBM_GBS,
-                         "bytes_per_elem": bpe})
+                         "bytes_per_elem": bpe,
+                         "l2_resident": x.numel() * x.element_size() <= L2_BYTES})
             del x, outs
     torch.cuda.empty_cache()
     return rows
