@@ -26,6 +26,22 @@ from .checker import SymbolTable, check_kernel
 from .codegen import generate, generate_traced
 
 _cache_lock = threading.Lock()
+_fault_bufs: dict = {}
+
+
+def _fault_buffers(device):
+    """Per (device, thread) fault record: a zeroed device int64[6] the
+    kernels write only on a fault, and a pinned host mirror.  Reused across
+    launches (re-zeroed after a fault), so a launch costs one kernel, one
+    6-word D2H copy and one synchronise."""
+    import torch
+    key = (device.index, threading.get_ident())
+    bufs = _fault_bufs.get(key)
+    if bufs is None:
+        bufs = (torch.zeros(6, dtype=torch.int64, device=device),
+                torch.zeros(6, dtype=torch.int64).pin_memory())
+        _fault_bufs[key] = bufs
+    return bufs
 _module_cache: dict = {}
 
 
@@ -130,7 +146,7 @@ class JitProgram:
                 keep.append(C.c_int32(int(bound[p.name])))
             else:
                 keep.append(C.c_float(float(np.float32(bound[p.name]))))
-        err = torch.zeros(6, dtype=torch.int64, device=memory.device)
+        err, err_host = _fault_buffers(memory.device)
         dyn = [s for s, (_, ln) in self.table.shared.items() if ln is None]
         elem = 4
         dyn_len = config.shared_bytes // elem if dyn else 0
@@ -138,14 +154,16 @@ class JitProgram:
         if trace is not None:
             counts = torch.zeros(self.layout.max_uid + 1, dtype=torch.int64, device=memory.device)
             keep.append(C.c_void_p(counts.data_ptr()))
-        argv = (C.c_void_p * len(keep))(*[C.cast(C.pointer(k), C.c_void_p) for k in keep])
-        stream = torch.cuda.current_stream(memory.device).cuda_stream
+        argv = (C.c_void_p * len(keep))(*[C.addressof(k) for k in keep])
+        stream = torch.cuda.current_stream(memory.device)
         rc = _lib.load().wf_jit_launch(mod, config.grid_size, config.block_size,
-                                       config.shared_bytes, argv, stream)
+                                       config.shared_bytes, argv, stream.cuda_stream)
         _lib.check(rc, f"launch of {self.name}")
-        torch.cuda.current_stream(memory.device).synchronize()
-        code, arg, idx, length = (int(v) for v in err.cpu().tolist()[:4])
+        err_host.copy_(err, non_blocking=True)
+        stream.synchronize()
+        code, arg, idx, length = (int(v) for v in err_host.tolist()[:4])
         if code:
+            err.zero_()
             raise ExecutionError(self._message(code, arg, idx, length))
         if trace is not None:
             c = counts.cpu().tolist()
