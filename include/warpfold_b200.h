@@ -158,6 +158,26 @@ int wf_reduce_sum_f32_mg(const float *in, uint64_t n, float *out, int block,
 #define WF_PEER_ALLREDUCE 2
 #define WF_PEER_EXSCAN_U32 3
 size_t wf_peer_mailbox_bytes(int world, uint32_t cap);
+/* The same exchange fused into the last block of the producing kernel (one
+ * kernel per rank and step instead of kernel + exchange kernel), on a
+ * wf_peer_mailbox_alloc mailbox and the same epoch sequence as
+ * wf_peer_exchange:
+ *   wf_reduce_sum_i32_exscan_mg: K1 over the rank's shard, then
+ *     d_out2 = {sum of the shards of ranks < rank, sum of all shards}
+ *     (int32, wrapping) — the carry-in and total of the sharded C3 scan.
+ *   wf_histogram256_u8_mg: K5 over the rank's shard, then d_bins = the
+ *     element-wise sum of every rank's 256 bins (cap >= 256).
+ * Every rank must issue the same sequence of exchange calls. */
+int wf_reduce_sum_i32_exscan_mg(const int32_t *in, uint64_t n, int32_t *d_out2,
+                                int block, int grid, void *ws, size_t ws_bytes,
+                                void *const *d_peers, const void *d_mailbox,
+                                uint32_t cap, int rank, int world, uint32_t epoch,
+                                uint32_t *d_err, wf_stream_t stream);
+int wf_histogram256_u8_mg(const uint8_t *in, uint64_t n, uint64_t *d_bins,
+                          void *ws, size_t ws_bytes, void *const *d_peers,
+                          const void *d_mailbox, uint32_t cap, int rank,
+                          int world, uint32_t epoch, uint32_t *d_err,
+                          wf_stream_t stream);
 int wf_peer_mailbox_alloc(int world, uint32_t cap, void **d_mailbox);
 int wf_peer_exchange(int mode, const void *d_vals, uint32_t count, uint32_t cap,
                      void *d_out, void *const *d_peers, const void *d_mailbox,

@@ -60,6 +60,10 @@ SIGNATURES = {
     "wf_peer_mailbox_alloc": (C.c_int, [C.c_int, _u32, C.POINTER(_vp)]),
     "wf_peer_exchange": (C.c_int, [C.c_int, _vp, _u32, _u32, _vp, _vp, _vp, C.c_int, C.c_int,
                                    _u32, _vp, _vp]),
+    "wf_reduce_sum_i32_exscan_mg": (C.c_int, [_vp, _u64, _vp, C.c_int, C.c_int, _vp, _sz, _vp,
+                                              _vp, _u32, C.c_int, C.c_int, _u32, _vp, _vp]),
+    "wf_histogram256_u8_mg": (C.c_int, [_vp, _u64, _vp, _vp, _sz, _vp, _vp, _u32, C.c_int,
+                                        C.c_int, _u32, _vp, _vp]),
     "wf_reduce_sum_f32_mg": (C.c_int, [_vp, _u64, _vp, C.c_int, C.c_int, _vp, _sz, _vp, _vp,
                                        C.c_int, C.c_int, _u32, _vp]),
     "wf_fold_i32": (C.c_int, [_vp, _u32, _vp, _vp]),

@@ -282,6 +282,48 @@ int wf_peer_mailbox_alloc(int world, uint32_t cap, void **d_mailbox) {
   return cuda_status(cudaMemset(*d_mailbox, 0, b), "peer mailbox zero");
 }
 
+static int check_peer(void *const *d_peers, const void *d_mailbox, uint32_t cap, uint32_t need,
+                      int rank, int world, uint32_t epoch, uint32_t *d_err) {
+  if (d_peers == nullptr || d_mailbox == nullptr || d_err == nullptr)
+    return fail(WF_ERR_ARG, "NULL pointer");
+  if (world < 1 || world > 256 || rank < 0 || rank >= world)
+    return fail(WF_ERR_ARG, "rank %d / world %d out of range", rank, world);
+  if (cap < need) return fail(WF_ERR_ARG, "peer mailbox cap %u < %u payload words", cap, need);
+  if (epoch == 0) return fail(WF_ERR_ARG, "epoch must start at 1");
+  return WF_OK;
+}
+
+int wf_reduce_sum_i32_exscan_mg(const int32_t *in, uint64_t n, int32_t *d_out2, int block,
+                                int grid, void *ws, size_t ws_bytes, void *const *d_peers,
+                                const void *d_mailbox, uint32_t cap, int rank, int world,
+                                uint32_t epoch, uint32_t *d_err, wf_stream_t stream) {
+  int rc = reduce_common(WF_OP_REDUCE_SUM_I32, in, n, d_out2, block, grid, ws, ws_bytes);
+  if (rc) return rc;
+  rc = check_peer(d_peers, d_mailbox, cap, 1, rank, world, epoch, d_err);
+  if (rc) return rc;
+  if (grid == 0) grid = auto_reduce_grid(false, block, n);
+  return cuda_status(launch_reduce_i32_exscan_mg(in, n, d_out2, block, grid, ws, d_peers,
+                                                 d_mailbox, cap, rank, world, epoch, d_err,
+                                                 static_cast<cudaStream_t>(stream)),
+                     "reduce_sum_i32_exscan_mg");
+}
+
+int wf_histogram256_u8_mg(const uint8_t *in, uint64_t n, uint64_t *d_bins, void *ws,
+                          size_t ws_bytes, void *const *d_peers, const void *d_mailbox,
+                          uint32_t cap, int rank, int world, uint32_t epoch, uint32_t *d_err,
+                          wf_stream_t stream) {
+  if (d_bins == nullptr) return fail(WF_ERR_ARG, "bins pointer is NULL");
+  if (n && in == nullptr) return fail(WF_ERR_ARG, "input pointer is NULL");
+  int rc = check_ws(WF_OP_HISTOGRAM256_U8, n, ws, ws_bytes);
+  if (rc) return rc;
+  rc = check_peer(d_peers, d_mailbox, cap, 256, rank, world, epoch, d_err);
+  if (rc) return rc;
+  return cuda_status(launch_hist256_mg(in, n, d_bins, auto_hist_grid(n), ws, d_peers, d_mailbox,
+                                       cap, rank, world, epoch, d_err,
+                                       static_cast<cudaStream_t>(stream)),
+                     "histogram256_u8_mg");
+}
+
 int wf_peer_exchange(int mode, const void *d_vals, uint32_t count, uint32_t cap, void *d_out,
                      void *const *d_peers, const void *d_mailbox, int rank, int world,
                      uint32_t epoch, uint32_t *d_err, wf_stream_t stream) {

@@ -21,6 +21,7 @@
 // Roofline: HBM, 1 B/elem read.
 #include "wf_device.cuh"
 #include "wf_internal.h"
+#include "wf_peer.cuh"
 
 namespace wf {
 namespace {
@@ -62,11 +63,15 @@ __device__ __forceinline__ void count_word(uint32_t *col, uint32_t w) {
 }
 #endif
 
+// PX: the last block runs the peer all-reduce of wf_peer.cuh on the rank's
+// 256 bins, so `bins` receives the sum over all ranks — the sharded
+// histogram and its bin exchange in ONE kernel (wf_histogram256_u8_mg).
+template <bool PX>
 __global__ void __launch_bounds__(BLOCK, 2048 / BLOCK)
     hist256_kernel(const uint8_t *__restrict__ in, uint64_t n,
                    unsigned long long *__restrict__ bins, bool accumulate,
                    unsigned long long *__restrict__ accum,
-                   uint32_t *__restrict__ ticket) {
+                   uint32_t *__restrict__ ticket, PeerArgs pa) {
   extern __shared__ uint32_t sh[];  // [256][kBinWords], lane l counts in word l
   for (uint32_t i = threadIdx.x; i < 256 * kBinWords; i += BLOCK) sh[i] = 0u;
   __syncthreads();
@@ -130,6 +135,14 @@ __global__ void __launch_bounds__(BLOCK, 2048 / BLOCK)
   if (threadIdx.x == 0) am_last = atom_add_acq_rel_gpu(ticket, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!am_last) return;
+  if constexpr (PX) {
+    __shared__ uint64_t s_bins[256];
+    if (threadIdx.x < 256) s_bins[threadIdx.x] = atomicExch(accum + threadIdx.x, 0ull);
+    if (threadIdx.x == 0) *ticket = 0u;
+    __syncthreads();
+    peer_exchange_block(kPeerAllreduce, s_bins, nullptr, 256, bins, pa);
+    return;
+  }
   if (threadIdx.x < 256) {
     const unsigned long long v = atomicExch(accum + threadIdx.x, 0ull);
     bins[threadIdx.x] = accumulate ? bins[threadIdx.x] + v : v;
@@ -142,10 +155,10 @@ __global__ void __launch_bounds__(BLOCK, 2048 / BLOCK)
 int auto_hist_grid(uint64_t n) {
   static int per_sm = 0;
   if (per_sm == 0) {
-    cudaFuncSetAttribute(hist256_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(hist256_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(kHistSmem));
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, hist256_kernel, BLOCK, kHistSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, hist256_kernel<false>, BLOCK, kHistSmem);
     per_sm = b > 0 ? b : 1;
   }
   const uint64_t full = uint64_t(per_sm) * uint64_t(sm_count(current_device()));
@@ -155,20 +168,41 @@ int auto_hist_grid(uint64_t n) {
   return int(need < full ? need : full);
 }
 
+static void configure_hist(bool px) {
+  static uint64_t configured[2] = {0, 0};  // one bit per device
+  const int dev = current_device();
+  if (dev < 64 && !(configured[px] >> dev & 1)) {
+    if (px)
+      cudaFuncSetAttribute(hist256_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(kHistSmem));
+    else
+      cudaFuncSetAttribute(hist256_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(kHistSmem));
+    configured[px] |= 1ull << dev;
+  }
+}
+
 cudaError_t launch_hist256(const uint8_t *in, uint64_t n, uint64_t *bins,
                            bool accumulate, int grid, void *ws,
                            cudaStream_t s) {
   auto *ticket = reinterpret_cast<uint32_t *>(ws);
   auto *accum = reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + kWsHeader);
-  static uint64_t configured = 0;  // one bit per device
-  const int dev = current_device();
-  if (dev < 64 && !(configured >> dev & 1)) {
-    cudaFuncSetAttribute(hist256_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(kHistSmem));
-    configured |= 1ull << dev;
-  }
-  hist256_kernel<<<grid, BLOCK, kHistSmem, s>>>(
-      in, n, reinterpret_cast<unsigned long long *>(bins), accumulate, accum, ticket);
+  configure_hist(false);
+  hist256_kernel<false><<<grid, BLOCK, kHistSmem, s>>>(
+      in, n, reinterpret_cast<unsigned long long *>(bins), accumulate, accum, ticket, PeerArgs{});
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hist256_mg(const uint8_t *in, uint64_t n, uint64_t *bins, int grid, void *ws,
+                              void *const *peers, const void *mine, uint32_t cap, int rank,
+                              int world, uint32_t epoch, uint32_t *err, cudaStream_t s) {
+  auto *ticket = reinterpret_cast<uint32_t *>(ws);
+  auto *accum = reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + kWsHeader);
+  configure_hist(true);
+  PeerArgs pa{reinterpret_cast<uint64_t *const *>(peers), static_cast<const uint64_t *>(mine),
+              cap, rank, world, epoch, err};
+  hist256_kernel<true><<<grid, BLOCK, kHistSmem, s>>>(
+      in, n, reinterpret_cast<unsigned long long *>(bins), false, accum, ticket, pa);
   return cudaGetLastError();
 }
 

@@ -51,6 +51,13 @@ int auto_reduce_grid(bool is_f32, int block, uint64_t n);
 cudaError_t launch_reduce_f32_mg(const float *in, uint64_t n, float *out, int block, int grid,
                                  void *ws, void *const *peers, const void *mine, int rank,
                                  int world, uint32_t epoch, cudaStream_t s);
+cudaError_t launch_reduce_i32_exscan_mg(const int32_t *in, uint64_t n, int32_t *out2, int block,
+                                        int grid, void *ws, void *const *peers, const void *mine,
+                                        uint32_t cap, int rank, int world, uint32_t epoch,
+                                        uint32_t *err, cudaStream_t s);
+cudaError_t launch_hist256_mg(const uint8_t *in, uint64_t n, uint64_t *bins, int grid, void *ws,
+                              void *const *peers, const void *mine, uint32_t cap, int rank,
+                              int world, uint32_t epoch, uint32_t *err, cudaStream_t s);
 size_t peer_mailbox_bytes(int world, uint32_t count);
 cudaError_t launch_peer_exchange(int mode, const void *vals, uint32_t count, uint32_t cap,
                                  void *out, void *const *peers, const void *mine, int rank,

@@ -20,6 +20,7 @@
 // result is bitwise reproducible run to run.  Roofline: HBM read, 4 B/elem.
 #include "wf_device.cuh"
 #include "wf_internal.h"
+#include "wf_peer.cuh"
 
 #ifndef WF_RED_PDL
 #define WF_RED_PDL 0  // programmatic dependent launch between consecutive K2 launches
@@ -107,12 +108,17 @@ __device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long
   return v;
 }
 
-template <class Op, int BLOCK, int UNROLL, bool MG = false>
+// PX (i32 only): the last block also runs the peer exchange of wf_peer.cuh on
+// the rank total (exclusive scan over ranks, mod 2^32), so out = {carry of
+// this rank's shard, global total} — the sharded scan's pass 1 and its carry
+// exchange in ONE kernel (wf_reduce_sum_i32_exscan_mg).
+template <class Op, int BLOCK, int UNROLL, bool MG = false, bool PX = false>
 __global__ void __launch_bounds__(BLOCK)
     reduce_kernel(const typename Op::elem_t *__restrict__ in, uint64_t n,
                   typename Op::elem_t *__restrict__ out,
                   typename Op::acc_t *__restrict__ partials,
-                  uint32_t *__restrict__ ticket, MgArgs mg = MgArgs{}) {
+                  uint32_t *__restrict__ ticket, MgArgs mg = MgArgs{},
+                  PeerArgs pa = PeerArgs{}) {
   using acc_t = typename Op::acc_t;
   using elem_t = typename Op::elem_t;
   const uint64_t gtid = uint64_t(blockIdx.x) * BLOCK + threadIdx.x;
@@ -185,6 +191,23 @@ __global__ void __launch_bounds__(BLOCK)
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
 
+  if constexpr (PX) {
+    __shared__ bool s_last;
+    __shared__ uint32_t s_total;
+    if (threadIdx.x == 0) {
+      auto *word = reinterpret_cast<unsigned long long *>(ticket);
+      const unsigned long long mine = (1ull << 48) | Op::bits(bsum);
+      const unsigned long long old = atomicAdd(word, mine);
+      s_last = (old >> 48) == gridDim.x - 1;
+      if (s_last) {
+        s_total = uint32_t(old + mine);
+        *word = 0ull;
+      }
+    }
+    __syncthreads();
+    if (s_last) peer_exchange_block(kPeerExscanU32, nullptr, &s_total, 1, out, pa);
+    return;
+  }
   if (Op::kOrderFree) {
     // integer Σ is order-independent: ONE 64-bit atomic per block carries both
     // the block sum (low 48 bits: 32 bits of sum + up to 2^16 wraps) and an
@@ -301,7 +324,7 @@ cudaError_t launch_block(const typename Op::elem_t *in, uint64_t n,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, reduce_kernel<Op, BLOCK, kUnroll, false>, in, n, out, partials,
-                            ticket, MgArgs{});
+                            ticket, MgArgs{}, PeerArgs{});
 #else
   reduce_kernel<Op, BLOCK, kUnroll>
       <<<grid, BLOCK, 0, s>>>(in, n, out, partials, ticket);
@@ -350,7 +373,32 @@ cudaError_t launch_mg_block(const float *in, uint64_t n, float *out, int grid, v
   return cudaGetLastError();
 }
 
+template <int BLOCK>
+cudaError_t launch_px_block(const int32_t *in, uint64_t n, int32_t *out2, int grid, void *ws,
+                            const PeerArgs &pa, cudaStream_t s) {
+  auto *ticket = reinterpret_cast<uint32_t *>(ws);
+  auto *partials = reinterpret_cast<uint32_t *>(static_cast<char *>(ws) + kWsHeader);
+  reduce_kernel<SumI32, BLOCK, kUnroll, false, true>
+      <<<grid, BLOCK, 0, s>>>(in, n, out2, partials, ticket, MgArgs{}, pa);
+  return cudaGetLastError();
+}
+
 }  // namespace
+
+cudaError_t launch_reduce_i32_exscan_mg(const int32_t *in, uint64_t n, int32_t *out2, int block,
+                                        int grid, void *ws, void *const *peers, const void *mine,
+                                        uint32_t cap, int rank, int world, uint32_t epoch,
+                                        uint32_t *err, cudaStream_t s) {
+  PeerArgs pa{reinterpret_cast<uint64_t *const *>(peers), static_cast<const uint64_t *>(mine),
+              cap, rank, world, epoch, err};
+  switch (block) {
+    case 128: return launch_px_block<128>(in, n, out2, grid, ws, pa, s);
+    case 256: return launch_px_block<256>(in, n, out2, grid, ws, pa, s);
+    case 512: return launch_px_block<512>(in, n, out2, grid, ws, pa, s);
+    case 1024: return launch_px_block<1024>(in, n, out2, grid, ws, pa, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 cudaError_t launch_reduce_f32_mg(const float *in, uint64_t n, float *out, int block, int grid,
                                  void *ws, void *const *peers, const void *mine, int rank,

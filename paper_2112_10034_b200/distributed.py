@@ -21,9 +21,10 @@ one small collective:
 The exchange helpers are backend-agnostic (NCCL on GPUs, gloo in the CPU
 tests) and the carries/offsets are computed by the device kernels, so a step
 needs no host round trip.  With a ``p2p.PeerCollectives`` (``peer=``) the
-scan carries, compaction offsets and bin sums instead travel over peer memory
-(NVLink, CUDA IPC mailboxes) in one single-block kernel per rank; the fp32
-reduction has its own fused form (``p2p.PeerReducer``).
+exchanges travel over peer memory (NVLink, CUDA IPC mailboxes) instead: the
+scan's pass 1 and the histogram run their exchange in their own last block
+(one kernel each), the compaction offsets take one single-block kernel; the
+fp32 reduction has its own fused form (``p2p.PeerReducer``).
 """
 
 from __future__ import annotations
@@ -89,8 +90,8 @@ def scan_inclusive_i32(x_local: torch.Tensor, out: torch.Tensor | None = None,
     rank, world = _world(group)
     if world == 1:
         return ops.scan_inclusive_i32(x_local, out)
-    if peer is not None:
-        carry = peer.exscan_u32(ops.reduce_sum_i32(x_local))[:1]
+    if peer is not None:  # pass 1 + carry exchange in one kernel
+        carry = peer.reduce_exscan_i32(x_local)[:1]
         return ops.scan_inclusive_i32(x_local, out, carry=carry)
     totals = exchange(ops.reduce_sum_i32(x_local), group).reshape(-1)
     carry = ops.fold(totals, count=rank)  # exclusive prefix of earlier shards
@@ -117,10 +118,10 @@ def compact_gt0_i32(x_local: torch.Tensor, out: torch.Tensor | None = None, grou
 
 
 def histogram256_u8(x_local: torch.Tensor, group=None, peer=None) -> torch.Tensor:
-    bins = ops.histogram256_u8(x_local)
     rank, world = _world(group)
+    if world > 1 and peer is not None:  # histogram + bin all-reduce in one kernel
+        return peer.histogram256_u8(x_local)
+    bins = ops.histogram256_u8(x_local)
     if world > 1:
-        if peer is not None:
-            return peer.allreduce_u64(bins)
         dist.all_reduce(bins, op=dist.ReduceOp.SUM, group=group)
     return bins

@@ -147,9 +147,12 @@ class PeerReducer:
 
 
 class PeerCollectives:
-    """The small exchanges of the sharded C3-C5 paths over peer memory
-    (`wf_peer_exchange`): one single-block kernel per call and rank, results
-    identical on every rank.  Every rank must issue the same sequence of calls."""
+    """The exchanges of the sharded C3-C5 paths over peer memory, results
+    identical on every rank: fused into the producing kernel's last block
+    where the exchange directly follows one (`reduce_exscan_i32` for the scan
+    carry, `histogram256_u8` for the bins), else one single-block kernel
+    (`wf_peer_exchange`: the compaction offsets).  All share one mailbox and
+    epoch sequence; every rank must issue the same sequence of calls."""
 
     EXSCAN, ALLREDUCE, EXSCAN_U32 = 1, 2, 3
 
@@ -187,6 +190,41 @@ class PeerCollectives:
         out = torch.empty_like(v)
         return self._run(self.ALLREDUCE, v, v.numel(), out, stream)
 
+    def reduce_exscan_i32(self, x_local: torch.Tensor, out: torch.Tensor | None = None,
+                          block: int = 256, stream=None) -> torch.Tensor:
+        """K1 over this rank's shard with the carry exchange fused into its
+        last block (``wf_reduce_sum_i32_exscan_mg``): int32[2] = (wrapping sum
+        of the shards of lower ranks, wrapping sum of all shards) — the
+        sharded scan's pass 1 + exchange in one kernel."""
+        ops._require_cuda(x_local, torch.int32, "x")
+        if out is None:
+            out = torch.empty(2, dtype=torch.int32, device=x_local.device)
+        self.epoch += 1
+        ws = ops.workspace(_lib.OP_REDUCE_SUM_I32, x_local.numel(), x_local.device, stream)
+        _check(_lib.load().wf_reduce_sum_i32_exscan_mg(
+            x_local.data_ptr(), x_local.numel(), out.data_ptr(), block, 0, ws.data_ptr(),
+            ws.numel(), self.boxes.peers.data_ptr(), self.boxes.own, self.cap, self.rank,
+            self.world, self.epoch, self.err.data_ptr(), ops._stream_handle(stream)),
+            "wf_reduce_sum_i32_exscan_mg")
+        return out
+
+    def histogram256_u8(self, x_local: torch.Tensor, bins: torch.Tensor | None = None,
+                        stream=None) -> torch.Tensor:
+        """K5 over this rank's shard with the bin all-reduce fused into its
+        last block (``wf_histogram256_u8_mg``): the global int64[256] bins on
+        every rank."""
+        ops._require_cuda(x_local, torch.uint8, "x")
+        if bins is None:
+            bins = torch.empty(256, dtype=torch.int64, device=x_local.device)
+        self.epoch += 1
+        ws = ops.workspace(_lib.OP_HISTOGRAM256_U8, x_local.numel(), x_local.device, stream)
+        _check(_lib.load().wf_histogram256_u8_mg(
+            x_local.data_ptr(), x_local.numel(), bins.data_ptr(), ws.data_ptr(), ws.numel(),
+            self.boxes.peers.data_ptr(), self.boxes.own, self.cap, self.rank, self.world,
+            self.epoch, self.err.data_ptr(), ops._stream_handle(stream)),
+            "wf_histogram256_u8_mg")
+        return bins
+
     def failed(self) -> bool:
         return bool(self.err.item())
 
@@ -216,7 +254,8 @@ def try_peer_reducer(device: torch.device, x_probe: torch.Tensor, group=None):
 
 def try_peer_collectives(device: torch.device, group=None, cap: int = 256):
     """Collective.  PeerCollectives checked against NCCL on a probe (an
-    exclusive scan of rank+1 and an all-reduce of a rank-dependent vector).
+    exclusive scan of rank+1, an all-reduce of a rank-dependent vector, and
+    the two fused kernels: scan pass 1 + carry, histogram + bin all-reduce).
     Returns (collectives, "ok") or (None, reason) — the same on every rank."""
     from . import distributed as wd
     try:
@@ -231,8 +270,18 @@ def try_peer_collectives(device: torch.device, group=None, cap: int = 256):
     gathered = wd.exchange(v, group).reshape(-1)
     want_red = vec.clone()
     dist.all_reduce(want_red, group=group)
+    xi = ops.fill_synthetic("i32_full", 100003 + 17 * rank, seed=rank, device=device)
+    carry = pc.reduce_exscan_i32(xi)
+    totals = wd.exchange(ops.reduce_sum_i32(xi), group).reshape(-1).to(torch.int64) & 0xFFFFFFFF
+    xu = ops.fill_synthetic("u8_uniform", 300007 + 5 * rank, seed=rank, device=device)
+    bins = pc.histogram256_u8(xu)
+    want_bins = ops.histogram256_u8(xu)
+    dist.all_reduce(want_bins, group=group)
     same = (not pc.failed() and int(got[0]) == int(gathered[:rank].sum())
-            and int(got[1]) == int(gathered.sum()) and torch.equal(red, want_red))
+            and int(got[1]) == int(gathered.sum()) and torch.equal(red, want_red)
+            and int(carry[0]) & 0xFFFFFFFF == int(totals[:rank].sum()) & 0xFFFFFFFF
+            and int(carry[1]) & 0xFFFFFFFF == int(totals.sum()) & 0xFFFFFFFF
+            and torch.equal(bins, want_bins))
     ok = torch.tensor([1 if same else 0], dtype=torch.int32, device=device)
     dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
     if int(ok.item()) != 1:

@@ -128,8 +128,10 @@ def _rank_main(rank: int, world: int, port: int, n: int, q) -> None:
         pc = p2p.PeerCollectives.for_process_group(dev, cap=256)
         xi = ops.fill_synthetic("i32_full", 5000 + rank, seed=rank, device=dev)
         carry = pc.exscan_u32(ops.reduce_sum_i32(xi))
-        bins = pc.allreduce_u64(ops.histogram256_u8(ops.fill_synthetic("u8_uniform", 777, seed=rank,
-                                                                        device=dev)))
+        xu = ops.fill_synthetic("u8_uniform", 777, seed=rank, device=dev)
+        bins = pc.allreduce_u64(ops.histogram256_u8(xu))
+        carry_fused = pc.reduce_exscan_i32(xi)     # K1 + exchange in one kernel
+        bins_fused = pc.histogram256_u8(xu)        # K5 + all-reduce in one kernel
         T.cuda.synchronize()
         res = [bool(T.equal(g.view(T.int32), want.view(T.int32))) for g in got]
         res.append(not pc.failed())
@@ -138,6 +140,8 @@ def _rank_main(rank: int, world: int, port: int, n: int, q) -> None:
                                                               device=dev)).item()) & 0xFFFFFFFF
                   for r in range(world)]
         res.append((int(carry[0].item()) & 0xFFFFFFFF) == (sum(totals[:rank]) & 0xFFFFFFFF))
+        res.append(bool(T.equal(carry_fused, carry)) and bool(T.equal(bins_fused, bins))
+                   and not pc.failed())
         q.put((rank, res))
         D.barrier()
         pr.close()
@@ -165,7 +169,7 @@ def test_peer_reducer_two_processes_one_gpu(mods):
     res = dict(q.get(timeout=240) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    assert res[0] == [True] * 6 and res[1] == [True] * 6, res
+    assert res[0] == [True] * 7 and res[1] == [True] * 7, res
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
@@ -206,6 +210,53 @@ def test_peer_collectives_in_process(mods, world):
                                                         int(w32.sum()) & 0xFFFFFFFF]
                 assert e64.tolist() == [int(u64[:r].sum()), int(u64.sum())]
                 assert np.array_equal(red, vec.sum(0))
+    finally:
+        torch.cuda.synchronize()
+        boxes[0].close()
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_fused_peer_kernels_in_process(mods, world):
+    """K1 + scan-carry exchange and K5 + bin all-reduce fused into one kernel
+    per rank (wf_reduce_sum_i32_exscan_mg, wf_histogram256_u8_mg): `world`
+    concurrent ranks on one GPU, several epochs interleaved with the
+    stand-alone exchange on the same mailbox, results identical on every rank
+    and equal to the per-rank kernels combined on the host."""
+    ops, p2p, wd = mods
+    dev = torch.device("cuda", 0)
+    cap = 256
+    boxes = p2p.Mailboxes.local(world, dev, cap=cap)
+    pcs = [p2p.PeerCollectives(boxes[r], r, world, cap, dev) for r in range(world)]
+    streams = [torch.cuda.Stream(dev) for _ in range(world)]
+    n_i, n_u = (1 << 22) * world + 977, (1 << 24) * world + 33
+    si = [wd.shard_range(n_i, r, world) for r in range(world)]
+    su = [wd.shard_range(n_u, r, world) for r in range(world)]
+    xs = [ops.fill_synthetic("i32_full", hi - lo, seed=5, base=lo) for lo, hi in si]
+    us = [ops.fill_synthetic("u8_uniform", hi - lo, seed=6, base=lo) for lo, hi in su]
+    totals = [int(ops.reduce_sum_i32(x).item()) & 0xFFFFFFFF for x in xs]
+    want_bins = sum(ops.histogram256_u8(u) for u in us)
+    # created up front: a pageable H2D copy inside the loop would block the
+    # host behind this rank's spinning kernel before the next rank launches
+    offs_in = [torch.tensor([r + 1], device=dev) for r in range(world)]
+    torch.cuda.synchronize()
+    try:
+        for step in range(4):
+            outs = [None] * world
+            order = range(world) if step % 2 == 0 else reversed(range(world))
+            for r in order:
+                with torch.cuda.stream(streams[r]):
+                    c = pcs[r].reduce_exscan_i32(xs[r], stream=streams[r])
+                    off = pcs[r].exscan_u64(offs_in[r], stream=streams[r])
+                    b = pcs[r].histogram256_u8(us[r], stream=streams[r])
+                    outs[r] = (c, off, b)
+            torch.cuda.synchronize()
+            for r in range(world):
+                c, off, b = outs[r]
+                assert not pcs[r].failed(), (step, r)
+                assert (int(c[0]) & 0xFFFFFFFF, int(c[1]) & 0xFFFFFFFF) == (
+                    sum(totals[:r]) & 0xFFFFFFFF, sum(totals) & 0xFFFFFFFF), (step, r)
+                assert off.tolist() == [r * (r + 1) // 2, world * (world + 1) // 2]
+                assert torch.equal(b, want_bins), (step, r)
     finally:
         torch.cuda.synchronize()
         boxes[0].close()
