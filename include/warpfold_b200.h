@@ -167,12 +167,21 @@ size_t wf_peer_mailbox_bytes(int world, uint32_t cap);
  *     (int32, wrapping) — the carry-in and total of the sharded C3 scan.
  *   wf_histogram256_u8_mg: K5 over the rank's shard, then d_bins = the
  *     element-wise sum of every rank's 256 bins (cap >= 256).
+ *   wf_compact_gt0_i32_mg: K4 over the rank's shard (output stays local),
+ *     d_counts3 = {this rank's count, its global offset, the global total}
+ *     (u64); the exchange runs in the compaction kernel's last finisher warp
+ *     on the default (TMEM) path, as a second kernel otherwise.
  * Every rank must issue the same sequence of exchange calls. */
 int wf_reduce_sum_i32_exscan_mg(const int32_t *in, uint64_t n, int32_t *d_out2,
                                 int block, int grid, void *ws, size_t ws_bytes,
                                 void *const *d_peers, const void *d_mailbox,
                                 uint32_t cap, int rank, int world, uint32_t epoch,
                                 uint32_t *d_err, wf_stream_t stream);
+int wf_compact_gt0_i32_mg(const int32_t *in, uint64_t n, int32_t *out,
+                          uint64_t *d_counts3, void *ws, size_t ws_bytes,
+                          void *const *d_peers, const void *d_mailbox,
+                          uint32_t cap, int rank, int world, uint32_t epoch,
+                          uint32_t *d_err, wf_stream_t stream);
 int wf_histogram256_u8_mg(const uint8_t *in, uint64_t n, uint64_t *d_bins,
                           void *ws, size_t ws_bytes, void *const *d_peers,
                           const void *d_mailbox, uint32_t cap, int rank,

@@ -62,6 +62,8 @@ SIGNATURES = {
                                    _u32, _vp, _vp]),
     "wf_reduce_sum_i32_exscan_mg": (C.c_int, [_vp, _u64, _vp, C.c_int, C.c_int, _vp, _sz, _vp,
                                               _vp, _u32, C.c_int, C.c_int, _u32, _vp, _vp]),
+    "wf_compact_gt0_i32_mg": (C.c_int, [_vp, _u64, _vp, _vp, _vp, _sz, _vp, _vp, _u32, C.c_int,
+                                        C.c_int, _u32, _vp, _vp]),
     "wf_histogram256_u8_mg": (C.c_int, [_vp, _u64, _vp, _vp, _sz, _vp, _vp, _u32, C.c_int,
                                         C.c_int, _u32, _vp, _vp]),
     "wf_reduce_sum_f32_mg": (C.c_int, [_vp, _u64, _vp, C.c_int, C.c_int, _vp, _sz, _vp, _vp,

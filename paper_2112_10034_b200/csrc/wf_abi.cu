@@ -308,6 +308,26 @@ int wf_reduce_sum_i32_exscan_mg(const int32_t *in, uint64_t n, int32_t *d_out2, 
                      "reduce_sum_i32_exscan_mg");
 }
 
+int wf_compact_gt0_i32_mg(const int32_t *in, uint64_t n, int32_t *out, uint64_t *d_counts3,
+                          void *ws, size_t ws_bytes, void *const *d_peers, const void *d_mailbox,
+                          uint32_t cap, int rank, int world, uint32_t epoch, uint32_t *d_err,
+                          wf_stream_t stream) {
+  if (d_counts3 == nullptr) return fail(WF_ERR_ARG, "counts pointer is NULL");
+  if (n > 0 && (in == nullptr || out == nullptr)) return fail(WF_ERR_ARG, "NULL buffer pointer");
+  if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 3u)
+    return fail(WF_ERR_ARG, "buffers must be 4-byte aligned");
+  if (n > 0xffffffffull)
+    return fail(WF_ERR_ARG, "compaction takes n < 2^32 per call, got %llu", (unsigned long long)n);
+  int rc = check_ws(WF_OP_COMPACT_GT0_I32, n, ws, ws_bytes);
+  if (rc) return rc;
+  rc = check_peer(d_peers, d_mailbox, cap, 1, rank, world, epoch, d_err);
+  if (rc) return rc;
+  return cuda_status(launch_compact_gt0_i32_mg(in, n, out, d_counts3, ws, d_peers, d_mailbox, cap,
+                                               rank, world, epoch, d_err,
+                                               static_cast<cudaStream_t>(stream)),
+                     "compact_gt0_i32_mg");
+}
+
 int wf_histogram256_u8_mg(const uint8_t *in, uint64_t n, uint64_t *d_bins, void *ws,
                           size_t ws_bytes, void *const *d_peers, const void *d_mailbox,
                           uint32_t cap, int rank, int world, uint32_t epoch, uint32_t *d_err,

@@ -82,6 +82,14 @@ cudaError_t launch_scan_tmem_i32(const int32_t *in, int32_t *out, uint64_t n,
                                  const int32_t *carry, void *ws, cudaStream_t s);
 cudaError_t launch_compact_tmem_i32(const int32_t *in, uint64_t n, int32_t *out,
                                     uint64_t *count, void *ws, cudaStream_t s);
+struct PeerArgs;  // wf_peer.cuh
+cudaError_t launch_compact_tmem_i32_mg(const int32_t *in, uint64_t n, int32_t *out,
+                                       uint64_t *counts3, void *ws, const PeerArgs &pa,
+                                       cudaStream_t s);
+cudaError_t launch_compact_gt0_i32_mg(const int32_t *in, uint64_t n, int32_t *out,
+                                      uint64_t *counts3, void *ws, void *const *peers,
+                                      const void *mine, uint32_t cap, int rank, int world,
+                                      uint32_t epoch, uint32_t *err, cudaStream_t s);
 
 // L2-streamed two-pass scan / compaction (wf_scan2p.cu), 16 B aligned buffers
 bool two_pass_usable(uint64_t n);

@@ -123,4 +123,53 @@ static __device__ __noinline__ bool peer_exchange_block(int mode, const uint64_t
   return true;
 }
 
+// One warp's form of mode 1 (exclusive scan + total of one u64 per rank),
+// for kernels where only one warp holds the value when it becomes known (the
+// compaction's last finisher warp).  Lane p handles peer p (p, p+32, ...):
+// payload store, release fence, flag store — per-thread program order, so no
+// barrier cumulativity is needed.  out2 = {sum_{r<rank} v_r, sum_r v_r}.
+static __device__ __noinline__ bool peer_exscan_warp(uint64_t v, uint64_t *out2,
+                                                     const PeerArgs pa) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t world = uint32_t(pa.world);
+  const uint32_t stride = pa.cap + 1;
+  const uint64_t bank_off = uint64_t(pa.epoch & 1u) * world * stride;
+  const uint64_t my_slot = bank_off + uint64_t(pa.rank) * stride;
+  for (uint32_t p = lane; p < world; p += 32) {
+    peer_st_relaxed_sys(pa.peers[p] + my_slot, v);
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    peer_st_relaxed_sys(pa.peers[p] + my_slot + pa.cap, uint64_t(pa.epoch));
+  }
+  bool fail = false;
+  uint64_t excl = 0, total = 0;
+  for (uint32_t p = lane; p < world; p += 32) {
+    const uint64_t *slot = pa.mine + bank_off + uint64_t(p) * stride;
+    uint32_t spins = 0;
+    while (peer_ld_acquire_sys(slot + pa.cap) != uint64_t(pa.epoch)) {
+      if (++spins > (1u << 25)) {  // ~4 s: a peer never arrived
+        fail = true;
+        break;
+      }
+      __nanosleep(128);
+    }
+    const uint64_t x = fail ? 0 : peer_ld_relaxed_sys(slot);
+    if (int(p) < pa.rank) excl += x;
+    total += x;
+  }
+  if (__any_sync(0xffffffffu, fail)) {
+    if (lane == 0) *pa.err = 1u;
+    return false;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    excl += __shfl_xor_sync(0xffffffffu, excl, o);
+    total += __shfl_xor_sync(0xffffffffu, total, o);
+  }
+  if (lane == 0) {
+    out2[0] = excl;
+    out2[1] = total;
+  }
+  return true;
+}
+
 }  // namespace wf

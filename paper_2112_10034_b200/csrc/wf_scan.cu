@@ -35,6 +35,7 @@
 // 4 B per selected element written.
 #include "wf_device.cuh"
 #include "wf_internal.h"
+#include "wf_peer.cuh"
 
 #include <cstdlib>
 
@@ -559,6 +560,24 @@ cudaError_t launch_compact_gt0_i32(const int32_t *in, uint64_t n, int32_t *out,
   compact_gt0_kernel<<<uint32_t(ntiles), BLOCK, 0, s>>>(in, n, uint32_t(ntiles), aligned, out,
                                                          count, desc, hdr);
   return cudaGetLastError();
+}
+
+// Sharded compaction + offset exchange: fused into the TMEM kernel's last
+// finisher warp on the default path, else the selected compaction kernel
+// followed by the stand-alone exchange kernel.  counts3 = {count, offset, total}.
+cudaError_t launch_compact_gt0_i32_mg(const int32_t *in, uint64_t n, int32_t *out,
+                                      uint64_t *counts3, void *ws, void *const *peers,
+                                      const void *mine, uint32_t cap, int rank, int world,
+                                      uint32_t epoch, uint32_t *err, cudaStream_t s) {
+  const bool aligned = (reinterpret_cast<uintptr_t>(in) & 15u) == 0;
+  PeerArgs pa{reinterpret_cast<uint64_t *const *>(peers), static_cast<const uint64_t *>(mine),
+              cap, rank, world, epoch, err};
+  if (n > 0 && tmem_scan_enabled() && !(aligned && two_pass_usable(n)))
+    return launch_compact_tmem_i32_mg(in, n, out, counts3, ws, pa, s);
+  cudaError_t e = launch_compact_gt0_i32(in, n, out, counts3, ws, s);
+  if (e != cudaSuccess) return e;
+  return launch_peer_exchange(kPeerExscan, counts3, 1, cap, counts3 + 1, peers, mine, rank, world,
+                              epoch, err, s);
 }
 
 }  // namespace wf

@@ -45,6 +45,7 @@
 // runtime/hostdesc.py:109-129; compaction not expressible, dsl/lexer.py:18-25).
 #include "wf_device.cuh"
 #include "wf_internal.h"
+#include "wf_peer.cuh"
 
 #include <cstdlib>
 
@@ -193,12 +194,17 @@ struct TmShared {
   uint32_t epoch;
 };
 
-template <bool COMPACT>
+// PX (compaction only): the finisher warp of the last tile also runs the
+// offset exchange of wf_peer.cuh (peer_exscan_warp): count = {this rank's
+// count, its global offset, the global total} — the sharded compaction and
+// its exchange in ONE kernel (wf_compact_gt0_i32_mg).
+template <bool COMPACT, bool PX = false>
 __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
     tile_tmem_kernel(const int32_t *__restrict__ in, int32_t *__restrict__ out, uint64_t n,
                      uint32_t ntiles, const int32_t *__restrict__ carry_in,
                      uint64_t *__restrict__ count, uint64_t *__restrict__ desc,
-                     TileHeader *__restrict__ hdr, uint32_t head, bool vec_out) {
+                     TileHeader *__restrict__ hdr, uint32_t head, bool vec_out,
+                     PeerArgs pa) {
   // `head` (0-3): the buffers were rounded down to 16 B, so virtual elements
   // [0, head) precede the caller's data; they read as 0 (neutral for the sum,
   // never selected) and are never stored.  Only tile 0 is affected.
@@ -477,7 +483,11 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
           }
         }
       }
-      if (COMPACT && t == ntiles - 1 && q == 0 && h == 0 && lane == 0) *count = uint64_t(prefix) + agg;
+      if (COMPACT && t == ntiles - 1 && q == 0 && h == 0) {
+        const uint64_t total = uint64_t(prefix) + agg;
+        if (lane == 0) *count = total;
+        if constexpr (PX) peer_exscan_warp(total, count + 1, pa);
+      }
       if (q == 0 && h == 0 && lane == 0) TM_STAMP(t, 4);
     }
   } else if (warp < W_PROD) {
@@ -562,7 +572,8 @@ cudaError_t launch_scan_tmem_i32(const int32_t *in, int32_t *out, uint64_t n,
   const uint32_t nt = uint32_t((nv + TM_TILE - 1) / TM_TILE);
   tile_tmem_kernel<false><<<tmem_grid<false>(nt), TM_THREADS, tm_smem<false>(), s>>>(
       in - head, out - head, nv, nt, carry, nullptr, desc, hdr, head,
-      ((reinterpret_cast<uintptr_t>(in) ^ reinterpret_cast<uintptr_t>(out)) & 15u) == 0);
+      ((reinterpret_cast<uintptr_t>(in) ^ reinterpret_cast<uintptr_t>(out)) & 15u) == 0,
+      PeerArgs{});
   return cudaGetLastError();
 }
 
@@ -574,7 +585,28 @@ cudaError_t launch_compact_tmem_i32(const int32_t *in, uint64_t n, int32_t *out,
   const uint64_t nv = n + head;
   const uint32_t nt = uint32_t((nv + TM_TILE - 1) / TM_TILE);
   tile_tmem_kernel<true><<<tmem_grid<true>(nt), TM_THREADS, tm_smem<true>(), s>>>(
-      in - head, out, nv, nt, nullptr, count, desc, hdr, head, false);
+      in - head, out, nv, nt, nullptr, count, desc, hdr, head, false, PeerArgs{});
+  return cudaGetLastError();
+}
+
+// n >= 1.  counts3 = {count, global offset, global total}.
+cudaError_t launch_compact_tmem_i32_mg(const int32_t *in, uint64_t n, int32_t *out,
+                                       uint64_t *counts3, void *ws, const PeerArgs &pa,
+                                       cudaStream_t s) {
+  auto *hdr = reinterpret_cast<TileHeader *>(ws);
+  auto *desc = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + kTileWsHeader);
+  const uint32_t head = uint32_t((reinterpret_cast<uintptr_t>(in) & 15u) / 4u);
+  const uint64_t nv = n + head;
+  const uint32_t nt = uint32_t((nv + TM_TILE - 1) / TM_TILE);
+  static bool configured[64] = {};
+  const int dev = current_device();
+  if (dev >= 0 && dev < 64 && !configured[dev]) {
+    cudaFuncSetAttribute(tile_tmem_kernel<true, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(tm_smem<true>()));
+    configured[dev] = true;
+  }
+  tile_tmem_kernel<true, true><<<tmem_grid<true>(nt), TM_THREADS, tm_smem<true>(), s>>>(
+      in - head, out, nv, nt, nullptr, counts3, desc, hdr, head, false, pa);
   return cudaGetLastError();
 }
 

@@ -21,10 +21,10 @@ one small collective:
 The exchange helpers are backend-agnostic (NCCL on GPUs, gloo in the CPU
 tests) and the carries/offsets are computed by the device kernels, so a step
 needs no host round trip.  With a ``p2p.PeerCollectives`` (``peer=``) the
-exchanges travel over peer memory (NVLink, CUDA IPC mailboxes) instead: the
-scan's pass 1 and the histogram run their exchange in their own last block
-(one kernel each), the compaction offsets take one single-block kernel; the
-fp32 reduction has its own fused form (``p2p.PeerReducer``).
+exchanges travel over peer memory (NVLink, CUDA IPC mailboxes) instead, each
+inside the kernel that produces its input (scan pass 1, compaction,
+histogram: one kernel per rank and op); the fp32 reduction has its own fused
+form (``p2p.PeerReducer``).
 """
 
 from __future__ import annotations
@@ -103,14 +103,14 @@ def compact_gt0_i32(x_local: torch.Tensor, out: torch.Tensor | None = None, grou
     """Returns (out_local, count_local, offset, total) as device int64 scalars
     for count/offset/total; rank r's selected elements belong at
     [offset, offset + count) of the global a[a > 0]."""
-    out, count = ops.compact_gt0_i32(x_local, out)
     rank, world = _world(group)
+    if world > 1 and peer is not None:  # compaction + offset exchange in one kernel
+        out, c3 = peer.compact_gt0_i32(x_local, out)
+        return out, c3[:1], c3[1:2], c3[2:]
+    out, count = ops.compact_gt0_i32(x_local, out)
     if world == 1:
         zero = torch.zeros(1, dtype=torch.int64, device=count.device)
         return out, count, zero, count
-    if peer is not None:
-        r = peer.exscan_u64(count)
-        return out, count, r[:1], r[1:]
     counts = exchange(count, group).reshape(-1)
     offset = ops.fold(counts, count=rank)
     total = ops.fold(counts)

@@ -148,11 +148,12 @@ class PeerReducer:
 
 class PeerCollectives:
     """The exchanges of the sharded C3-C5 paths over peer memory, results
-    identical on every rank: fused into the producing kernel's last block
-    where the exchange directly follows one (`reduce_exscan_i32` for the scan
-    carry, `histogram256_u8` for the bins), else one single-block kernel
-    (`wf_peer_exchange`: the compaction offsets).  All share one mailbox and
-    epoch sequence; every rank must issue the same sequence of calls."""
+    identical on every rank, each fused into the kernel that produces its
+    input (`reduce_exscan_i32`: scan pass 1 + carry; `compact_gt0_i32`:
+    compaction + offsets; `histogram256_u8`: bins + all-reduce); the
+    stand-alone single-block exchanges (`exscan_u32`, `exscan_u64`,
+    `allreduce_u64`) serve any other value.  All share one mailbox and epoch
+    sequence; every rank must issue the same sequence of calls."""
 
     EXSCAN, ALLREDUCE, EXSCAN_U32 = 1, 2, 3
 
@@ -207,6 +208,24 @@ class PeerCollectives:
             self.world, self.epoch, self.err.data_ptr(), ops._stream_handle(stream)),
             "wf_reduce_sum_i32_exscan_mg")
         return out
+
+    def compact_gt0_i32(self, x_local: torch.Tensor, out: torch.Tensor | None = None,
+                        stream=None):
+        """K4 over this rank's shard with the offset exchange fused into the
+        compaction kernel (``wf_compact_gt0_i32_mg``): returns (out_local,
+        int64[3] = (count, global offset, global total))."""
+        ops._require_cuda(x_local, torch.int32, "x")
+        if out is None:
+            out = torch.empty_like(x_local)
+        counts = torch.empty(3, dtype=torch.int64, device=x_local.device)
+        self.epoch += 1
+        ws = ops.workspace(_lib.OP_COMPACT_GT0_I32, x_local.numel(), x_local.device, stream)
+        _check(_lib.load().wf_compact_gt0_i32_mg(
+            x_local.data_ptr(), x_local.numel(), out.data_ptr(), counts.data_ptr(), ws.data_ptr(),
+            ws.numel(), self.boxes.peers.data_ptr(), self.boxes.own, self.cap, self.rank,
+            self.world, self.epoch, self.err.data_ptr(), ops._stream_handle(stream)),
+            "wf_compact_gt0_i32_mg")
+        return out, counts
 
     def histogram256_u8(self, x_local: torch.Tensor, bins: torch.Tensor | None = None,
                         stream=None) -> torch.Tensor:
@@ -277,11 +296,14 @@ def try_peer_collectives(device: torch.device, group=None, cap: int = 256):
     bins = pc.histogram256_u8(xu)
     want_bins = ops.histogram256_u8(xu)
     dist.all_reduce(want_bins, group=group)
+    _, cnt3 = pc.compact_gt0_i32(xi)
+    counts = wd.exchange(ops.compact_gt0_i32(xi)[1], group).reshape(-1)
     same = (not pc.failed() and int(got[0]) == int(gathered[:rank].sum())
             and int(got[1]) == int(gathered.sum()) and torch.equal(red, want_red)
             and int(carry[0]) & 0xFFFFFFFF == int(totals[:rank].sum()) & 0xFFFFFFFF
             and int(carry[1]) & 0xFFFFFFFF == int(totals.sum()) & 0xFFFFFFFF
-            and torch.equal(bins, want_bins))
+            and torch.equal(bins, want_bins)
+            and cnt3.tolist() == [int(counts[rank]), int(counts[:rank].sum()), int(counts.sum())])
     ok = torch.tensor([1 if same else 0], dtype=torch.int32, device=device)
     dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
     if int(ok.item()) != 1:

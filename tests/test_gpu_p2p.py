@@ -132,6 +132,7 @@ def _rank_main(rank: int, world: int, port: int, n: int, q) -> None:
         bins = pc.allreduce_u64(ops.histogram256_u8(xu))
         carry_fused = pc.reduce_exscan_i32(xi)     # K1 + exchange in one kernel
         bins_fused = pc.histogram256_u8(xu)        # K5 + all-reduce in one kernel
+        _, c3 = pc.compact_gt0_i32(xi)             # K4 + offsets in one kernel
         T.cuda.synchronize()
         res = [bool(T.equal(g.view(T.int32), want.view(T.int32))) for g in got]
         res.append(not pc.failed())
@@ -142,6 +143,9 @@ def _rank_main(rank: int, world: int, port: int, n: int, q) -> None:
         res.append((int(carry[0].item()) & 0xFFFFFFFF) == (sum(totals[:rank]) & 0xFFFFFFFF))
         res.append(bool(T.equal(carry_fused, carry)) and bool(T.equal(bins_fused, bins))
                    and not pc.failed())
+        cnts = [int((ops.fill_synthetic("i32_full", 5000 + r, seed=r, device=dev) > 0).sum())
+                for r in range(world)]
+        res.append(c3.tolist() == [cnts[rank], sum(cnts[:rank]), sum(cnts)])
         q.put((rank, res))
         D.barrier()
         pr.close()
@@ -169,7 +173,7 @@ def test_peer_reducer_two_processes_one_gpu(mods):
     res = dict(q.get(timeout=240) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    assert res[0] == [True] * 7 and res[1] == [True] * 7, res
+    assert res[0] == [True] * 8 and res[1] == [True] * 8, res
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
@@ -217,8 +221,9 @@ def test_peer_collectives_in_process(mods, world):
 
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
 def test_fused_peer_kernels_in_process(mods, world):
-    """K1 + scan-carry exchange and K5 + bin all-reduce fused into one kernel
-    per rank (wf_reduce_sum_i32_exscan_mg, wf_histogram256_u8_mg): `world`
+    """K1 + scan-carry exchange, K4 + offset exchange and K5 + bin all-reduce
+    fused into one kernel per rank (wf_reduce_sum_i32_exscan_mg,
+    wf_compact_gt0_i32_mg, wf_histogram256_u8_mg): `world`
     concurrent ranks on one GPU, several epochs interleaved with the
     stand-alone exchange on the same mailbox, results identical on every rank
     and equal to the per-rank kernels combined on the host."""
@@ -235,6 +240,8 @@ def test_fused_peer_kernels_in_process(mods, world):
     us = [ops.fill_synthetic("u8_uniform", hi - lo, seed=6, base=lo) for lo, hi in su]
     totals = [int(ops.reduce_sum_i32(x).item()) & 0xFFFFFFFF for x in xs]
     want_bins = sum(ops.histogram256_u8(u) for u in us)
+    want_sel = [x[x > 0] for x in xs]
+    counts = [int(w.numel()) for w in want_sel]
     # created up front: a pageable H2D copy inside the loop would block the
     # host behind this rank's spinning kernel before the next rank launches
     offs_in = [torch.tensor([r + 1], device=dev) for r in range(world)]
@@ -248,15 +255,18 @@ def test_fused_peer_kernels_in_process(mods, world):
                     c = pcs[r].reduce_exscan_i32(xs[r], stream=streams[r])
                     off = pcs[r].exscan_u64(offs_in[r], stream=streams[r])
                     b = pcs[r].histogram256_u8(us[r], stream=streams[r])
-                    outs[r] = (c, off, b)
+                    co, c3 = pcs[r].compact_gt0_i32(xs[r], stream=streams[r])
+                    outs[r] = (c, off, b, co, c3)
             torch.cuda.synchronize()
             for r in range(world):
-                c, off, b = outs[r]
+                c, off, b, co, c3 = outs[r]
                 assert not pcs[r].failed(), (step, r)
                 assert (int(c[0]) & 0xFFFFFFFF, int(c[1]) & 0xFFFFFFFF) == (
                     sum(totals[:r]) & 0xFFFFFFFF, sum(totals) & 0xFFFFFFFF), (step, r)
                 assert off.tolist() == [r * (r + 1) // 2, world * (world + 1) // 2]
                 assert torch.equal(b, want_bins), (step, r)
+                assert c3.tolist() == [counts[r], sum(counts[:r]), sum(counts)], (step, r)
+                assert torch.equal(co[:counts[r]], want_sel[r]), (step, r)
     finally:
         torch.cuda.synchronize()
         boxes[0].close()
