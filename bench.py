@@ -451,7 +451,8 @@ def per_kernel(args, rank, world, local, dev, peak) -> dict:
     if world > 1:  # C3-C5 exchanges over peer memory when every rank can map every mailbox
         from paper_2112_10034_b200 import p2p
         pc, why = p2p.try_peer_collectives(dev)
-        exchange = ("peer-memory kernel (wf_peer_exchange)" if pc
+        exchange = ("peer memory, fused into the producing kernel (C3: scan pass 1, "
+                    "C4: compaction, C5: histogram)" if pc
                     else f"NCCL (peer path unavailable: {why})")
         log(f"rank {rank}: C3-C5 exchange = {exchange}")
     steps, warm = max(5, args.steps), max(3, args.warmup)
