@@ -20,5 +20,18 @@ r = [ops.reduce_sum_i32(x), ops.reduce_sum_f32(f), ops.scan_inclusive_i32(x),
 a = torch.arange(96, dtype=torch.int32, device="cuda")
 for kind in ("shfl_down", "shfl_up", "shfl_xor", "shfl_idx", "vote_all", "vote_any", "ballot", "reduce_add"):
     r.append(ops.warp_collective(kind, a, operand=3, block=96))
+# the fused multi-GPU forms (world 1: own mailbox; the peer stores and the
+# flag/epoch protocol still run)
+from paper_2112_10034_b200 import p2p  # noqa: E402
+dev = torch.device("cuda", 0)
+boxes = p2p.Mailboxes.local(1, dev, cap=256)
+pc = p2p.PeerCollectives(boxes[0], 0, 1, 256, dev)
+r += [pc.reduce_exscan_i32(x), pc.compact_gt0_i32(x)[1], pc.histogram256_u8(u),
+      pc.exscan_u64(torch.ones(1, dtype=torch.int64, device=dev))]
+kboxes = p2p.Mailboxes.local(1, dev)
+r.append(p2p.PeerReducer(kboxes[0], 0, 1).reduce_sum_f32(f))
 torch.cuda.synchronize()
+assert not pc.failed()
+boxes[0].close()
+kboxes[0].close()
 print("ok", [int(t.reshape(-1)[0].item()) if t.dtype != torch.float32 else float(t[0]) for t in r[:5]])
