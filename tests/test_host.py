@@ -143,6 +143,32 @@ def test_abi_argument_errors_map_to_reference_exceptions(lib):
     assert rc == _lib.WF_ERR_UNSUPPORTED
 
 
+def test_fused_exchange_entry_points_validate_before_launch(lib):
+    """The *_mg entry points reject bad mailbox arguments before any CUDA
+    call (fake, aligned device addresses; no GPU needed)."""
+    ws, wsb, ptr = 256, 1 << 20, 64
+    # (in, n, out2, block, grid, ws, ws_bytes, peers, mailbox, cap, rank, world, epoch, err, stream)
+    rc = lib.wf_reduce_sum_i32_exscan_mg(ptr, 10, ptr, 256, 0, ws, wsb, None, ptr, 1, 0, 1, 1, ptr, None)
+    assert rc == _lib.WF_ERR_ARG and "NULL" in _lib.last_error()
+    rc = lib.wf_reduce_sum_i32_exscan_mg(ptr, 10, ptr, 256, 0, ws, wsb, ptr, ptr, 0, 0, 1, 1, ptr, None)
+    assert rc == _lib.WF_ERR_ARG and "cap 0 < 1" in _lib.last_error()
+    rc = lib.wf_reduce_sum_i32_exscan_mg(ptr, 10, ptr, 256, 0, ws, wsb, ptr, ptr, 1, 0, 1, 0, ptr, None)
+    assert rc == _lib.WF_ERR_ARG and "epoch" in _lib.last_error()
+    rc = lib.wf_reduce_sum_i32_exscan_mg(ptr, 10, ptr, 256, 0, ws, wsb, ptr, ptr, 1, 3, 2, 1, ptr, None)
+    assert rc == _lib.WF_ERR_ARG and "out of range" in _lib.last_error()
+    rc = lib.wf_reduce_sum_i32_exscan_mg(ptr, 10, ptr, 100, 0, ws, wsb, ptr, ptr, 1, 0, 1, 1, ptr, None)
+    assert rc == _lib.WF_ERR_CONFIG
+    # (in, n, bins, ws, ws_bytes, peers, mailbox, cap, rank, world, epoch, err, stream)
+    rc = lib.wf_histogram256_u8_mg(ptr, 10, ptr, ws, wsb, ptr, ptr, 255, 0, 1, 1, ptr, None)
+    assert rc == _lib.WF_ERR_ARG and "cap 255 < 256" in _lib.last_error()
+    # (in, n, out, counts3, ws, ws_bytes, peers, mailbox, cap, rank, world, epoch, err, stream)
+    rc = lib.wf_compact_gt0_i32_mg(ptr, 1 << 33, ptr, ptr, ws, 1 << 40, ptr, ptr, 1, 0, 1, 1, ptr,
+                                   None)
+    assert rc == _lib.WF_ERR_ARG and "2^32" in _lib.last_error()
+    rc = lib.wf_compact_gt0_i32_mg(ptr, 10, ptr, None, ws, wsb, ptr, ptr, 1, 0, 1, 1, ptr, None)
+    assert rc == _lib.WF_ERR_ARG and "counts" in _lib.last_error()
+
+
 def test_cuda_error_codes_map_to_execution_error():
     with pytest.raises(errors.ExecutionError, match="CUDA error 700"):
         _lib.check(700, "illegal address")
