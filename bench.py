@@ -343,6 +343,13 @@ def run_ours(args, rank, world, local) -> dict | None:
         t1.record()
         barrier_sync(world)
     step_ms = t0.elapsed_time(t1) / args.steps
+    if peer is not None:  # the timed exchange must still agree with the NCCL path, bit for bit
+        got = peer.reduce_sum_f32(x, block=BLOCK_C2)
+        want = ops.fold(wd.exchange(ops.reduce_sum_f32(x, block=BLOCK_C2)).reshape(-1))
+        if not torch.equal(got.view(torch.int32), want.view(torch.int32)):
+            log(f"rank {rank}: fused K2 exchange disagrees with NCCL after timing: "
+                f"{float(got.item())} vs {float(want.item())}")
+            exchange += " — FAILED post-timing check"
     if world == 1 or peer is not None:
         kern_ms, kern_timing = step_ms, "timed region / steps (one kernel per step)"
     else:
@@ -549,6 +556,9 @@ def per_kernel(args, rank, world, local, dev, peak) -> dict:
                          "gelem_s": round(N_C5 / (max_over_ranks(ms, world) * 1e-3) / 1e9, 3)}
     res["c5_hist_u8"]["data_variants"] = variants
     if exchange is not None:
+        if pc is not None and pc.failed():  # a peer never arrived in some call: results invalid
+            log(f"rank {rank}: a peer-memory exchange timed out during the C3-C5 runs")
+            exchange += " — FAILED (peer timeout)"
         for k in ("c3_scan_i32", "c4_compact_i32", "c5_hist_u8"):
             res[k]["exchange"] = exchange
     # DRAM bytes per launch measured by ncu --set full at the 1-GPU BASELINE
