@@ -142,9 +142,14 @@ def init_dist(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test-only: every rank on GPU 0 over gloo, to run the N>1 code path
+    # (IPC mailboxes, fused exchanges) as real processes on a 1-GPU box
+    if os.environ.get("WF_BENCH_SAME_GPU") == "1":
+        local = 0
     if world > 1:
         torch.cuda.set_device(local) if args.impl == "ours" else None
         backend = "nccl" if args.impl == "ours" else "gloo"
+        backend = os.environ.get("WF_BENCH_BACKEND", backend)
         dist.init_process_group(backend=backend,
                                 device_id=torch.device("cuda", local) if backend == "nccl" else None)
     elif args.impl == "ours":
@@ -365,6 +370,7 @@ def run_ours(args, rank, world, local) -> dict | None:
     achieved = 4.0 * n_local / (kern_ms * 1e-3) / 1e9
     gpu_launches = launches
 
+    log(f"rank {rank}: headline done ({step_ms:.3f} ms/step)")
     # ---- e2e through the C-ABI host entry point ---------------------------
     host = torch.empty(n_local, dtype=torch.float32, pin_memory=True)
     host.copy_(x)
@@ -389,6 +395,7 @@ def run_ours(args, rank, world, local) -> dict | None:
     h2d_gbs = 4.0 * n_local / (time.perf_counter() - t) / 1e9
     del host, dst
 
+    log(f"rank {rank}: e2e done")
     # ---- per-kernel lines for the other BASELINE configs -------------------
     per = {}
     if not args.headline_only:
@@ -464,9 +471,11 @@ def per_kernel(args, rank, world, local, dev, peak) -> dict:
         log(f"rank {rank}: C3-C5 exchange = {exchange}")
     steps, warm = max(5, args.steps), max(3, args.warmup)
 
-    def stats(times_ms, n_elems, bytes_per_elem, n_total):
+    def stats(times_ms, n_elems, bytes_per_elem, n_total, all_ranks=True):
+        # all_ranks=False for legs only rank 0 runs (C1): a collective there
+        # would pair with another leg's collective on the other ranks
         ms = statistics.mean(times_ms)
-        ms_max = max_over_ranks(ms, world)
+        ms_max = max_over_ranks(ms, world) if all_ranks else ms
         gbs = bytes_per_elem * n_elems / (ms * 1e-3) / 1e9
         return {"gelem_s": round(n_total / (ms_max * 1e-3) / 1e9, 3), "gbs": round(gbs, 1),
                 "frac_of_peak": round(gbs / peak, 4),
@@ -480,7 +489,7 @@ def per_kernel(args, rank, world, local, dev, peak) -> dict:
         flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
         t = time_launches(lambda: ops.reduce_sum_i32(x1, block=256), steps, warm,
                           flush=lambda: flush_buf.fill_(1))
-        res["c1_reduce_i32"] = stats(t, N_C1, 4, N_C1)
+        res["c1_reduce_i32"] = stats(t, N_C1, 4, N_C1, all_ranks=False)
         res["c1_reduce_i32"]["l2"] = "flushed (256 MiB write) before every launch"
         res["c1_reduce_i32"]["bound"] = ("latency: 4 MiB is 0.6 us of HBM time; see "
                                          "latency_context_us for the launch + atomic floor")
@@ -515,12 +524,14 @@ def per_kernel(args, rank, world, local, dev, peak) -> dict:
             "how": f"{per_graph} launches per CUDA graph replay, input L2-resident"}
         del graph
         del x1, flush_buf, tiny
+    log(f"rank {rank}: C3")
     # C3 scan
     lo, hi = wd.shard_range(N_C3, rank, world)
     x = ops.fill_synthetic("i32_full", hi - lo, seed=0, base=lo, device=dev)
     y = torch.empty_like(x)
     t = time_launches(lambda: wd.scan_inclusive_i32(x, y, peer=pc), steps, warm)
     res["c3_scan_i32"] = stats(t, hi - lo, 8 if world == 1 else 12, N_C3)
+    log(f"rank {rank}: C4")
     # C4 compaction
     out = torch.empty_like(x)
     t = time_launches(lambda: wd.compact_gt0_i32(x, out, peer=pc), steps, warm)
@@ -540,6 +551,7 @@ def per_kernel(args, rank, world, local, dev, peak) -> dict:
     res["c4_compact_i32"]["selectivity_variants"] = variants
     del x, y, out
     torch.cuda.empty_cache()
+    log(f"rank {rank}: C5")
     # C5 histogram
     lo, hi = wd.shard_range(N_C5, rank, world)
     u = ops.fill_synthetic("u8_uniform", hi - lo, seed=0, base=lo, device=dev)

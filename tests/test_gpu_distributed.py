@@ -124,3 +124,37 @@ def test_bench_n2_path_simulated(wd, monkeypatch):
     assert per["c3_scan_i32"]["bytes_per_elem"] == 12  # reduce-then-scan across GPUs
     for k in ("c1_reduce_i32", "c3_scan_i32", "c4_compact_i32", "c5_hist_u8"):
         assert per[k]["gelem_s"] > 0
+
+
+@pytest.mark.slow
+def test_bench_n2_two_processes_one_gpu():
+    """bench.py at N=2 as the driver launches it (torchrun, one process per
+    rank), with both ranks on GPU 0 over gloo (WF_BENCH_SAME_GPU): real
+    process group, IPC mailboxes and fused exchanges, so a collective issued
+    by only some ranks (it once hung the C1 leg's stats) or a mismatched
+    epoch sequence fails here.  Numbers are meaningless (two contexts
+    time-slice one GPU); only completion and the line's shape are checked."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, WF_BENCH_SAME_GPU="1", WF_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                        "--master-port", str(port), "bench.py", "--gpus", "2", "--steps", "3",
+                        "--warmup", "3", "--no-cpu-baseline"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "shard2"
+    assert line["config"]["exchange"].startswith("peer memory"), line["config"]["exchange"]
+    assert line["gpu_launches"] == line["steps"]  # one fused kernel per step
+    for k in ("c3_scan_i32", "c4_compact_i32", "c5_hist_u8"):
+        assert "FAILED" not in line["per_kernel"][k]["exchange"], line["per_kernel"][k]
+    assert "FAILED" not in line["config"]["exchange"]
