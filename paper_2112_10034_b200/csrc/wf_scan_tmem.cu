@@ -483,10 +483,14 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
           }
         }
       }
-      if (COMPACT && t == ntiles - 1 && q == 0 && h == 0) {
-        const uint64_t total = uint64_t(prefix) + agg;
-        if (lane == 0) *count = total;
-        if constexpr (PX) peer_exscan_warp(total, count + 1, pa);
+      if constexpr (PX) {
+        if (COMPACT && t == ntiles - 1 && q == 0 && h == 0) {
+          const uint64_t total = uint64_t(prefix) + agg;
+          if (lane == 0) *count = total;
+          peer_exscan_warp(total, count + 1, pa);
+        }
+      } else {
+        if (COMPACT && t == ntiles - 1 && q == 0 && h == 0 && lane == 0) *count = uint64_t(prefix) + agg;
       }
       if (q == 0 && h == 0 && lane == 0) TM_STAMP(t, 4);
     }
