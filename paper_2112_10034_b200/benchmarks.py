@@ -254,10 +254,13 @@ def bench_ops(ops_=tuple(OPS), log2_sizes=None, iters: int = 20, repeats: int = 
 
 def bench_scaling(ops_=("reduce_sum_f32", "scan_inclusive_i32", "compact_gt0_i32",
                         "histogram256_u8"), log2_total=None, iters: int = 20,
-                  repeats: int = 5, group=None) -> list[dict]:
+                  repeats: int = 5, group=None, peer: bool = True) -> list[dict]:
     """Sharded K2-K5 at a fixed total size (strong scaling) on every rank of
-    the process group; time = max over ranks of the device time.  Without a
-    process group it measures one GPU."""
+    the process group; time = max over ranks of the device time.  With
+    `peer` the exchanges run fused into the kernels over peer memory
+    (p2p.PeerReducer / PeerCollectives, set up by consensus; NCCL if any rank
+    cannot map the others' mailboxes).  Without a process group it measures
+    one GPU."""
     import torch.distributed as dist
     from . import distributed as wd
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -265,6 +268,19 @@ def bench_scaling(ops_=("reduce_sum_f32", "scan_inclusive_i32", "compact_gt0_i32
         if dist.is_available() and dist.is_initialized() else (0, 1)
     totals = log2_total or {"reduce_sum_f32": 30, "scan_inclusive_i32": 28,
                             "compact_gt0_i32": 28, "histogram256_u8": 32}
+    pr = pc = None
+    exchange = "none (1 GPU)"
+    if world > 1:
+        exchange = "NCCL"
+        if peer:
+            from . import p2p
+            lo_p, hi_p = wd.shard_range(1 << 20, rank, world)
+            probe = ops.fill_synthetic("f32_unit", hi_p - lo_p, seed=7, base=lo_p, device=dev)
+            pr, _ = p2p.try_peer_reducer(dev, probe, group)
+            pc, _ = p2p.try_peer_collectives(dev, group)
+            exchange = "peer memory (fused)" if pr is not None and pc is not None else "NCCL"
+            if exchange == "NCCL":  # identical decision on every rank (consensus above)
+                pr = pc = None
     rows = []
     for op in ops_:
         gen = OPS[op][0]
@@ -273,13 +289,14 @@ def bench_scaling(ops_=("reduce_sum_f32", "scan_inclusive_i32", "compact_gt0_i32
         x = ops.fill_synthetic(gen, hi - lo, seed=0, base=lo, device=dev)
         outs = _outs(op, hi - lo, dev)
         if op == "reduce_sum_f32":
-            fn = lambda: wd.reduce_sum_f32(x, group=group, block=512)  # noqa: E731
+            fn = (lambda: pr.reduce_sum_f32(x, block=512)) if pr is not None else \
+                (lambda: wd.reduce_sum_f32(x, group=group, block=512))
         elif op == "scan_inclusive_i32":
-            fn = lambda: wd.scan_inclusive_i32(x, outs["out"], group=group)  # noqa: E731
+            fn = lambda: wd.scan_inclusive_i32(x, outs["out"], group=group, peer=pc)  # noqa: E731
         elif op == "compact_gt0_i32":
-            fn = lambda: wd.compact_gt0_i32(x, outs["out"], group=group)  # noqa: E731
+            fn = lambda: wd.compact_gt0_i32(x, outs["out"], group=group, peer=pc)  # noqa: E731
         else:
-            fn = lambda: wd.histogram256_u8(x, group=group)  # noqa: E731
+            fn = lambda: wd.histogram256_u8(x, group=group, peer=pc)  # noqa: E731
         if world > 1:
             dist.barrier(group=group)
         t = torch.tensor([_device_time(fn, iters, repeats)], dtype=torch.float64, device=dev)
@@ -287,7 +304,15 @@ def bench_scaling(ops_=("reduce_sum_f32", "scan_inclusive_i32", "compact_gt0_i32
             dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
         t = float(t.item())
         rows.append({"op": op, "n": n, "n_gpus": world, "scaling": "strong",
-                     "us": t * 1e6, "gelem_s": n / t / 1e9})
+                     "us": t * 1e6, "gelem_s": n / t / 1e9, "exchange": exchange})
         del x, outs
+    failed = pc is not None and pc.failed()
+    for closer in (pr, pc):
+        if closer is not None:
+            torch.cuda.synchronize()
+            closer.close()
+    if failed:
+        for r in rows:
+            r["exchange"] += " — FAILED (peer timeout)"
     torch.cuda.empty_cache()
     return rows

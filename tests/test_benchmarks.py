@@ -51,3 +51,25 @@ def test_bench_cli_all_suites():
     assert len(res["ops"]) == sum(len(v[2]) for v in bm.OPS.values())
     assert all(row["gelem_s"] > 0 for row in res["ops"])
     assert [row["n_gpus"] for row in res["scaling"]] == [1] * 4
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_bench_cli_scaling_two_processes_one_gpu():
+    """`bench --suite scaling` under torchrun with 2 ranks (both on GPU 0
+    over gloo, WF_BENCH_SAME_GPU): the fused peer exchanges are set up by
+    consensus and every rank issues the same collectives."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, PYTHONPATH=str(ROOT), WF_BENCH_SAME_GPU="1", WF_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                        "--master-port", str(port), "-m", "paper_2112_10034_b200", "bench",
+                        "--suite", "scaling", "--json", "--op-iters", "3", "--repeats", "2"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    rows = json.loads(r.stdout.strip().splitlines()[-1])["scaling"]
+    assert [row["n_gpus"] for row in rows] == [2] * 4
+    assert all(row["exchange"] == "peer memory (fused)" for row in rows), rows
