@@ -20,7 +20,11 @@ NAMES = {"reduce_kernel<wf::<unnamed>::SumI32": "reduce_sum_i32",
          "compact_gt0_kernel": "compact_gt0_i32", "hist256_kernel": "histogram256_u8",
          "tile_tmem_kernel<false>": "scan_inclusive_i32", "tile_tmem_kernel<(bool)0>": "scan_inclusive_i32",
          "tile_tmem_kernel<0>": "scan_inclusive_i32", "tile_tmem_kernel<true>": "compact_gt0_i32",
-         "tile_tmem_kernel<(bool)1>": "compact_gt0_i32", "tile_tmem_kernel<1>": "compact_gt0_i32"}
+         "tile_tmem_kernel<(bool)1>": "compact_gt0_i32", "tile_tmem_kernel<1>": "compact_gt0_i32",
+         # two template parameters since the fused multi-GPU form: <COMPACT, PX>
+         "tile_tmem_kernel<0, ": "scan_inclusive_i32", "tile_tmem_kernel<1, ": "compact_gt0_i32",
+         "tile_tmem_kernel<(bool)0, ": "scan_inclusive_i32",
+         "tile_tmem_kernel<(bool)1, ": "compact_gt0_i32"}
 
 
 def op_name(kernel: str) -> str:
