@@ -1,9 +1,9 @@
-// wf_peer.cu — small collectives over peer memory (NVLink 5 / NVSwitch) for
-// the exchange steps of the sharded paths: the shard totals
-// that become scan carries (C3), the compaction counts that become global
-// offsets (C4) and the 256 histogram bins (C5).  Each is ONE single-block
-// kernel per rank instead of an NCCL all-gather / all-reduce plus a fold
-// kernel.
+// wf_peer.cu — the stand-alone form of the peer-memory exchange (NVLink 5 /
+// NVSwitch) of the sharded paths: ONE single-block kernel
+// per rank instead of an NCCL all-gather / all-reduce plus a fold kernel.
+// The default paths run the same exchange inside the producing kernel
+// (K1 -> scan carries, K4 -> compaction offsets, K5 -> bins); this kernel
+// serves any other value and the non-default compaction kernels.
 //
 // The protocol (mailbox layout, banks, fences) lives in wf_peer.cuh, shared
 // with the kernels that run the same exchange in their last block
