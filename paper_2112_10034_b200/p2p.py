@@ -245,7 +245,12 @@ class PeerCollectives:
         return bins
 
     def failed(self) -> bool:
+        """True once any call timed out waiting for a peer (~4 s); sticky
+        until clear_error().  Synchronises with the device."""
         return bool(self.err.item())
+
+    def clear_error(self) -> None:
+        self.err.zero_()
 
     def close(self) -> None:
         self.boxes.close()
