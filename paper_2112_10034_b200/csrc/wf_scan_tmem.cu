@@ -68,7 +68,7 @@
 #define WF_LBK_TM 1  // scan look-back predecessors per lane (window = 32 * K tiles)
 #endif
 #ifndef WF_LBK_COMPACT_TM
-#define WF_LBK_COMPACT_TM 2  // compaction look-back width
+#define WF_LBK_COMPACT_TM 1  // compaction look-back width (1: 277.7 vs 2: 281.6 us, tools/lbk_sweep.sh)
 #endif
 
 #ifndef WF_TM_TRACE
