@@ -56,7 +56,7 @@
 #define WF_TM_SLOTS 8  // TMEM slots per CTA (64 columns each; power of two)
 #endif
 #ifndef WF_TM_NLB
-#define WF_TM_NLB 6  // look-back warps per CTA
+#define WF_TM_NLB 3  // look-back warps per CTA (with 2 aggregator groups; tools/nag_sweep3.sh)
 #endif
 #ifndef WF_TM_NFG
 #define WF_TM_NFG 1  // finisher groups (8 warps each), taking tiles round-robin
@@ -100,7 +100,7 @@ constexpr int NFIN = 8 * NFG;             // per group: one finisher warp per ti
 constexpr int W_LB = W_FIN + NFIN;        // look-back warps W_LB .. W_LB+NLB-1
 constexpr int W_PROD = W_LB + NLB;        // producer warp
 #ifndef WF_TM_NAG
-#define WF_TM_NAG 1  // aggregator groups (4 warps each), taking stage items round-robin
+#define WF_TM_NAG 2  // aggregator groups (4 warps each), taking stage items round-robin
 #endif
 constexpr int NAG = WF_TM_NAG;
 constexpr int W_AGG2 = ((W_PROD + 1 + 3) / 4) * 4;  // 2nd group: warp % 4 = TMEM lane quarter
