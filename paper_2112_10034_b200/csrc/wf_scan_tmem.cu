@@ -118,6 +118,8 @@ constexpr uint32_t kNoTileTm = 0xffffffffu;
 static_assert((P & (P - 1)) == 0 && TM_COLS <= 512, "TMEM slots: power of two, <= 512 cols");
 static_assert(NLB >= 1 && NLB <= P, "look-back warps must not outnumber TMEM slots");
 static_assert(NFG <= NLB, "every finisher group must see one of the NLB stop items");
+static_assert(!(NAG == 2 && NFG > 1), "two aggregator groups with two finisher groups hang "
+              "(tools/sweep_final.sh): not a supported combination");
 
 // ---- TMEM helpers (tcgen05, cta_group::1) --------------------------------
 __device__ __forceinline__ void tmem_alloc(uint32_t *dst_smem, uint32_t ncols) {
