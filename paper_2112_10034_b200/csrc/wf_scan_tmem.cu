@@ -120,6 +120,15 @@ static_assert(NLB >= 1 && NLB <= P, "look-back warps must not outnumber TMEM slo
 static_assert(NFG <= NLB, "every finisher group must see one of the NLB stop items");
 static_assert(!(NAG == 2 && NFG > 1), "two aggregator groups with two finisher groups hang "
               "(tools/sweep_final.sh): not a supported combination");
+// With two aggregator groups taking stage items round-robin, an odd stage
+// count would hand one stage to both groups alternately: a group could then
+// wait on that stage's mbarrier for a phase two ahead of the current one,
+// which a parity wait reports as already complete (S = 5 hung,
+// tools/sweep_final2.sh).  Even S keeps every stage (and, P being a power of
+// two, every slot) with one group, so waiters are never more than one phase
+// ahead.
+static_assert(NAG == 1 || (S % 2 == 0 && P % 2 == 0),
+              "two aggregator groups need an even number of stages and slots");
 
 // ---- TMEM helpers (tcgen05, cta_group::1) --------------------------------
 __device__ __forceinline__ void tmem_alloc(uint32_t *dst_smem, uint32_t ncols) {
