@@ -200,6 +200,13 @@ struct TmShared {
   uint32_t slot_tile[P];
   uint32_t slot_agg[P];
   uint32_t item_prefix[2 * P];  // prefix of item i at i % 2P (outlives the slot's reuse)
+  // look-back copy of the slot metadata, by item (i % 2P): the look-back warp
+  // of item i reads it after the slot may already hold item i + P; entry i is
+  // only rewritten for item i + 2P, which cannot be parked before the
+  // finishers have item i's prefix, i.e. after this warp read its entry
+  uint32_t item_tile[2 * P];
+  uint32_t item_agg[2 * P];
+  uint32_t item_seq[2 * P];
   uint32_t slot_wtot[P][4][2];  // per tile quarter and half
   uint32_t tmem_base;
   uint32_t epoch;
@@ -327,6 +334,8 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
           if (e > 0 && ie / P > 0) mbar_wait(&sh.freed[pe], (ie / P - 1) & 1u);
           if (leader) {
             sh.slot_tile[pe] = kNoTileTm;
+            sh.item_tile[ie % (2 * P)] = kNoTileTm;
+            sh.item_seq[ie % (2 * P)] = ie;
             mbar_arrive1(&sh.parked[pe]);
           }
         }
@@ -376,6 +385,9 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
         for (int w = 0; w < 4; ++w) a += sh.slot_wtot[p][w][0] + sh.slot_wtot[p][w][1];
         sh.slot_tile[p] = t;
         sh.slot_agg[p] = a;
+        sh.item_tile[i % (2 * P)] = t;
+        sh.item_agg[i % (2 * P)] = a;
+        sh.item_seq[i % (2 * P)] = i;
         // publish the aggregate right here, not in the look-back warp: a
         // look-back warp busy with an older tile must never delay it
         if (t == 0) {
@@ -512,9 +524,18 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       const int p = int(i % P);
       const uint32_t kp = i / P;
       mbar_wait(&sh.parked[p], kp & 1u);
-      const uint32_t t = sh.slot_tile[p];
+      // Look-back warps take items round-robin (NLB need not divide P), so the
+      // previous use of this slot belonged to another warp; a parity wait
+      // issued while that phase is still open passes early.  The item ring
+      // entry carries the item index, written before the arrive: wait for it.
+      const int ri = int(i % (2 * P));
+      if (ld_volatile_u32(&sh.item_seq[ri]) != i) {
+        while (ld_volatile_u32(&sh.item_seq[ri]) != i) __nanosleep(32);
+      }
+      __threadfence_block();
+      const uint32_t t = sh.item_tile[ri];
       if (t == kNoTileTm) break;
-      const uint32_t agg = sh.slot_agg[p];
+      const uint32_t agg = sh.item_agg[ri];
       uint32_t excl;
       if (t == 0) {  // its prefix descriptor was published by the aggregator
         excl = (!COMPACT && carry_in != nullptr) ? uint32_t(*carry_in) : 0u;
