@@ -242,13 +242,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 }
 
 // 1-D bulk copy global -> shared, completion reported on `bar` (UBLKCP)
+#ifndef WF_TMA_EVICT_FIRST
+#define WF_TMA_EVICT_FIRST 0  // 1: streamed tiles marked evict-first in L2
+#endif
 __device__ __forceinline__ void tma_load_1d(void *dst_smem, const void *src, uint32_t bytes,
                                             uint64_t *bar) {
+#if WF_TMA_EVICT_FIRST
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+#else
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst_smem)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+#endif
 }
 
 // 1-D bulk copy shared -> global, tracked by bulk groups

@@ -71,6 +71,10 @@
 #define WF_LBK_COMPACT_TM 1  // compaction look-back width (1: 277.7 vs 2: 281.6 us, tools/lbk_sweep.sh)
 #endif
 
+#ifndef WF_CMP_STCS
+#define WF_CMP_STCS 0  // 1: compaction stores with the streaming (.cs) hint
+#endif
+
 #ifndef WF_TM_TRACE
 #define WF_TM_TRACE 0
 #endif
@@ -502,7 +506,13 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
             uint32_t pos = off + loc[m][j];
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              if (int32_t(x[k]) > 0) out[pos++] = int32_t(x[k]);
+              if (int32_t(x[k]) > 0) {
+#if WF_CMP_STCS
+                __stcs(out + pos++, int32_t(x[k]));
+#else
+                out[pos++] = int32_t(x[k]);
+#endif
+              }
           }
         }
       }
