@@ -260,6 +260,25 @@ int wf_histogram256_u8_host(const uint8_t *host_in, uint64_t n,
                             uint64_t *host_bins, void *staging,
                             size_t staging_bytes, void *ws, size_t ws_bytes,
                             wf_stream_t stream);
+/* Scan and compaction from host memory into host memory: a three-slot ring
+ * in the staging buffer overlaps chunk c's H2D, chunk c-1's kernel and chunk
+ * c-2's D2H (PCIe is full duplex).  The scan continues each chunk from the
+ * previous chunk's last output (one carry chain, identical to one device
+ * scan); `host_carry_in` may be NULL (carry 0).  The compaction writes the
+ * selected elements of every chunk behind those of the previous ones
+ * (== a[a > 0]) and their number into *host_count.  `ws` is sized for one
+ * chunk (wf_workspace_bytes(op, staging_bytes / 4, 0) always suffices).
+ * staging: 256-byte aligned, >= 3 MiB (scan) / 6 MiB (compaction).
+ * Replaces the reference's copy-in / launch / copy-out of host buffers
+ * (runtime/launch.py:105-134, runtime/memory.py:62-81). */
+int wf_scan_inclusive_i32_host(const int32_t *host_in, int32_t *host_out,
+                               uint64_t n, const int32_t *host_carry_in,
+                               void *staging, size_t staging_bytes, void *ws,
+                               size_t ws_bytes, wf_stream_t stream);
+int wf_compact_gt0_i32_host(const int32_t *host_in, uint64_t n,
+                            int32_t *host_out, uint64_t *host_count,
+                            void *staging, size_t staging_bytes, void *ws,
+                            size_t ws_bytes, wf_stream_t stream);
 
 /* ---- DSL kernels compiled natively (replaces hybrid_transform + run_mpmd)
  * passes/pipeline.py:103-179 / interp/mpmd.py:237-255: the Python front end

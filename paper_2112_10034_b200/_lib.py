@@ -78,6 +78,8 @@ SIGNATURES = {
     "wf_fill_synthetic": (C.c_int, [C.c_int, _vp, _u64, _u64, _u64, _u32, _vp]),
     "wf_reduce_sum_f32_host": (C.c_int, [_vp, _u64, _vp, _vp, _sz, _vp, _sz, _vp]),
     "wf_reduce_sum_i32_host": (C.c_int, [_vp, _u64, _vp, _vp, _sz, _vp, _sz, _vp]),
+    "wf_scan_inclusive_i32_host": (C.c_int, [_vp, _vp, _u64, _vp, _vp, _sz, _vp, _sz, _vp]),
+    "wf_compact_gt0_i32_host": (C.c_int, [_vp, _u64, _vp, _vp, _vp, _sz, _vp, _sz, _vp]),
     "wf_histogram256_u8_host": (C.c_int, [_vp, _u64, _vp, _vp, _sz, _vp, _sz, _vp]),
     "wf_jit_compile": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p),
                                  C.c_char_p, _sz]),

@@ -92,6 +92,11 @@ struct CopyStreams {
   cudaStream_t copy[2] = {nullptr, nullptr};
   cudaEvent_t copied[2] = {nullptr, nullptr};
   cudaEvent_t consumed[2] = {nullptr, nullptr};
+  // three-slot ring of the scan / compaction host paths (H2D in, kernel,
+  // D2H out, all overlapped): landed / computed / drained per slot
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t landed[3] = {}, computed[3] = {}, drained[3] = {};
+  uint64_t *pinned = nullptr;  // per-slot compaction counts read by the host
 };
 static std::mutex g_streams_mu;
 static CopyStreams g_streams[64];
@@ -116,6 +121,15 @@ static int get_copy_streams(CopyStreams *&cs) {
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.consumed[k], cudaEventDisableTiming);
       if (e != cudaSuccess) return cuda_status(e, "creating copy streams");
     }
+    cudaError_t e = cudaStreamCreateWithFlags(&c.h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.d2h, cudaStreamNonBlocking);
+    for (int k = 0; k < 3 && e == cudaSuccess; ++k) {
+      e = cudaEventCreateWithFlags(&c.landed[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.computed[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.drained[k], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaHostAlloc(&c.pinned, 64, cudaHostAllocDefault);
+    if (e != cudaSuccess) return cuda_status(e, "creating copy streams");
   }
   cs = &c;
   return WF_OK;
@@ -186,6 +200,17 @@ void wf_shutdown(void) {
       c.copy[k] = nullptr;
       c.copied[k] = c.consumed[k] = nullptr;
     }
+    if (c.h2d) cudaStreamDestroy(c.h2d);
+    if (c.d2h) cudaStreamDestroy(c.d2h);
+    for (int k = 0; k < 3; ++k) {
+      if (c.landed[k]) cudaEventDestroy(c.landed[k]);
+      if (c.computed[k]) cudaEventDestroy(c.computed[k]);
+      if (c.drained[k]) cudaEventDestroy(c.drained[k]);
+      c.landed[k] = c.computed[k] = c.drained[k] = nullptr;
+    }
+    if (c.pinned) cudaFreeHost(c.pinned);
+    c.h2d = c.d2h = nullptr;
+    c.pinned = nullptr;
   }
 }
 
@@ -415,6 +440,7 @@ int wf_histogram256_u8(const uint8_t *in, uint64_t n, uint64_t *bins, int grid, 
   int rc = check_ws(WF_OP_HISTOGRAM256_U8, n, ws, ws_bytes);
   if (rc) return rc;
   if (grid == 0) grid = auto_hist_grid(n);
+  if (grid < min_hist_grid(n)) grid = min_hist_grid(n);  // u32 lane counters stay < 2^32
   return cuda_status(
       launch_hist256(in, n, bins, false, grid, ws, static_cast<cudaStream_t>(stream)),
       "histogram256_u8");
@@ -493,7 +519,7 @@ int wf_reduce_sum_f32_host(const float *host_in, uint64_t n, float *host_out, vo
   return reduce_host<float>(
       WF_OP_REDUCE_SUM_F32, host_in, n, host_out, staging, staging_bytes, ws, ws_bytes, stream,
       [&](const float *d, uint64_t cnt, float *o, cudaStream_t s) {
-        return launch_reduce_f32(d, cnt, o, 256, auto_reduce_grid(true, 256, cnt), ws, s);
+        return launch_reduce_f32(d, cnt, o, 512, auto_reduce_grid(true, 512, cnt), ws, s);
       },
       [](const float *v, uint32_t c, float *o, cudaStream_t s) { return launch_fold_f32(v, c, o, s); });
 }
@@ -530,6 +556,139 @@ int wf_histogram256_u8_host(const uint8_t *host_in, uint64_t n, uint64_t *host_b
   e = cudaMemcpyAsync(host_bins, dbins, 256 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   return cuda_status(e, "host histogram");
+}
+
+}  // extern "C"
+
+// ---- host-buffer scan and compaction: three-slot H2D / kernel / D2H ring ---
+// Reference analog: the reference's memory is host memory and its launch
+// copies every buffer in and out (runtime/launch.py:105-134,
+// runtime/memory.py:62-81).  Here chunk c's H2D (h2d stream), chunk c-1's
+// kernel (caller's stream) and chunk c-2's D2H (d2h stream) run at once; PCIe
+// is full duplex, so the D2H of the result hides under the H2D of the input.
+namespace wf {
+namespace {
+constexpr int kRing = 3;
+
+int host_ring_checks(const void *host_in, const void *host_out, uint64_t n, void *staging,
+                     size_t staging_bytes, size_t min_bytes) {
+  if (n && (host_in == nullptr || host_out == nullptr))
+    return fail(WF_ERR_ARG, "host buffer pointer is NULL");
+  if (staging == nullptr || staging_bytes < min_bytes)
+    return fail(WF_ERR_ARG, "staging buffer must be at least %zu bytes", min_bytes);
+  if (reinterpret_cast<uintptr_t>(staging) & 255u)
+    return fail(WF_ERR_ARG, "staging buffer must be 256-byte aligned");
+  return WF_OK;
+}
+}  // namespace
+}  // namespace wf
+
+extern "C" {
+
+int wf_scan_inclusive_i32_host(const int32_t *host_in, int32_t *host_out, uint64_t n,
+                               const int32_t *host_carry_in, void *staging, size_t staging_bytes,
+                               void *ws, size_t ws_bytes, wf_stream_t stream) {
+  int rc = host_ring_checks(host_in, host_out, n, staging, staging_bytes, size_t(3) << 20);
+  if (rc) return rc;
+  // [0, 256): carry-in slot; then three in-place chunk buffers
+  const size_t buf = ((staging_bytes - 256) / kRing) & ~size_t(255);
+  const uint64_t per_chunk = buf / 4;
+  rc = check_ws(WF_OP_SCAN_INCLUSIVE_I32, per_chunk, ws, ws_bytes);
+  if (rc) return rc;
+  auto lk = host_call_lock();
+  CopyStreams *cs = nullptr;
+  if ((rc = get_copy_streams(cs))) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char *base = static_cast<char *>(staging);
+  int32_t *d_carry = reinterpret_cast<int32_t *>(base);
+  cudaError_t e = cudaSuccess;
+  if (host_carry_in != nullptr)
+    e = cudaMemcpyAsync(d_carry, host_carry_in, 4, cudaMemcpyHostToDevice, s);
+  const int32_t *carry = host_carry_in != nullptr ? d_carry : nullptr;
+  const uint64_t nchunks = (n + per_chunk - 1) / per_chunk;
+  for (uint64_t c = 0; c < nchunks && e == cudaSuccess; ++c) {
+    const int k = int(c % kRing);
+    const uint64_t first = c * per_chunk;
+    const uint64_t cnt = (n - first) < per_chunk ? (n - first) : per_chunk;
+    int32_t *dbuf = reinterpret_cast<int32_t *>(base + 256 + size_t(k) * buf);
+    if (c >= kRing) {  // slot k: chunk c-3 drained, and chunk c-2 read its carry from it
+      e = cudaStreamWaitEvent(cs->h2d, cs->drained[k], 0);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(cs->h2d, cs->computed[(c - 2) % kRing], 0);
+    }
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(dbuf, host_in + first, cnt * 4, cudaMemcpyHostToDevice, cs->h2d);
+    if (e == cudaSuccess) e = cudaEventRecord(cs->landed[k], cs->h2d);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, cs->landed[k], 0);
+    if (e == cudaSuccess) e = launch_scan_i32(dbuf, dbuf, cnt, carry, ws, s);
+    if (e == cudaSuccess) e = cudaEventRecord(cs->computed[k], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs->d2h, cs->computed[k], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(host_out + first, dbuf, cnt * 4, cudaMemcpyDeviceToHost, cs->d2h);
+    if (e == cudaSuccess) e = cudaEventRecord(cs->drained[k], cs->d2h);
+    carry = dbuf + (cnt - 1);  // the next chunk continues from this chunk's last output
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs->d2h);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return cuda_status(e, "host scan");
+}
+
+int wf_compact_gt0_i32_host(const int32_t *host_in, uint64_t n, int32_t *host_out,
+                            uint64_t *host_count, void *staging, size_t staging_bytes, void *ws,
+                            size_t ws_bytes, wf_stream_t stream) {
+  if (host_count == nullptr) return fail(WF_ERR_ARG, "host count pointer is NULL");
+  int rc = host_ring_checks(host_in, host_out, n, staging, staging_bytes, size_t(6) << 20);
+  if (rc) return rc;
+  // [0, 256): per-slot device counts; then three input and three output buffers
+  const size_t buf = ((staging_bytes - 256) / (2 * kRing)) & ~size_t(255);
+  const uint64_t per_chunk = buf / 4;
+  rc = check_ws(WF_OP_COMPACT_GT0_I32, per_chunk, ws, ws_bytes);
+  if (rc) return rc;
+  auto lk = host_call_lock();
+  CopyStreams *cs = nullptr;
+  if ((rc = get_copy_streams(cs))) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char *base = static_cast<char *>(staging);
+  uint64_t *d_counts = reinterpret_cast<uint64_t *>(base);
+  auto in_buf = [&](int k) { return reinterpret_cast<int32_t *>(base + 256 + size_t(k) * buf); };
+  auto out_buf = [&](int k) {
+    return reinterpret_cast<int32_t *>(base + 256 + size_t(kRing + k) * buf);
+  };
+  cudaError_t e = cudaSuccess;
+  uint64_t offset = 0;
+  // chunk c-1's output is drained once its count is on the host
+  auto drain = [&](uint64_t c) -> cudaError_t {
+    const int k = int(c % kRing);
+    cudaError_t r = cudaEventSynchronize(cs->computed[k]);
+    if (r != cudaSuccess) return r;
+    const uint64_t m = cs->pinned[k];
+    if (m) r = cudaMemcpyAsync(host_out + offset, out_buf(k), m * 4, cudaMemcpyDeviceToHost,
+                               cs->d2h);
+    if (r == cudaSuccess) r = cudaEventRecord(cs->drained[k], cs->d2h);
+    offset += m;
+    return r;
+  };
+  const uint64_t nchunks = (n + per_chunk - 1) / per_chunk;
+  for (uint64_t c = 0; c < nchunks && e == cudaSuccess; ++c) {
+    const int k = int(c % kRing);
+    const uint64_t first = c * per_chunk;
+    const uint64_t cnt = (n - first) < per_chunk ? (n - first) : per_chunk;
+    if (c >= kRing) e = cudaStreamWaitEvent(cs->h2d, cs->computed[k], 0);  // in-slot read
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(in_buf(k), host_in + first, cnt * 4, cudaMemcpyHostToDevice, cs->h2d);
+    if (e == cudaSuccess) e = cudaEventRecord(cs->landed[k], cs->h2d);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, cs->landed[k], 0);
+    if (e == cudaSuccess && c >= kRing) e = cudaStreamWaitEvent(s, cs->drained[k], 0);  // out-slot
+    if (e == cudaSuccess) e = launch_compact_gt0_i32(in_buf(k), cnt, out_buf(k), d_counts + k, ws, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(cs->pinned + k, d_counts + k, 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaEventRecord(cs->computed[k], s);
+    if (e == cudaSuccess && c >= 1) e = drain(c - 1);
+  }
+  if (e == cudaSuccess && nchunks >= 1) e = drain(nchunks - 1);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs->d2h);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) *host_count = offset;
+  return cuda_status(e, "host compaction");
 }
 
 }  // extern "C"

@@ -91,6 +91,23 @@ __device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t *p) {
 }
 
 // ---- splitmix64 index hash: the synthetic-input contract --
+// CTA-scope release store / acquire load on shared memory: publish a flag
+// after plain shared stores it guards (PTX memory model, not store order).
+__device__ __forceinline__ void st_release_cta_smem(uint32_t *p, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(p))),
+               "r"(v)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_cta_smem(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];"
+               : "=r"(v)
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p)))
+               : "memory");
+  return v;
+}
+
 __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   uint64_t z = x + 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;

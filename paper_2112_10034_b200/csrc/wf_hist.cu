@@ -122,13 +122,15 @@ __global__ void __launch_bounds__(BLOCK, 2048 / BLOCK)
   __syncthreads();
 
   // fold the 32 lane columns of each bin; rotation keeps the reads of a warp
-  // on 32 distinct banks
+  // on 32 distinct banks.  The fold is 64-bit: one block may count >= 2^32
+  // copies of a byte (each lane column stays < 2^32 by the grid floor of
+  // min_hist_grid, SURVEY.md §8d "a single bin can reach 2^32").
   if (threadIdx.x < 256) {
     const uint32_t b = threadIdx.x;
-    uint32_t s = 0;
+    unsigned long long s = 0;
 #pragma unroll 8
     for (uint32_t l = 0; l < 32; ++l) s += sh[b * kBinWords + ((l + b) & 31u)];
-    if (s) atomicAdd(accum + b, (unsigned long long)s);
+    if (s) atomicAdd(accum + b, s);
   }
   __shared__ bool am_last;
   __syncthreads();
@@ -152,11 +154,18 @@ __global__ void __launch_bounds__(BLOCK, 2048 / BLOCK)
 
 }  // namespace
 
+// Grid floor that keeps every u32 (bin, lane) counter below 2^32: a lane
+// column of a block counts the bytes of 32 threads, at most
+// 32 * (ceil(nvec / threads) * 16 + 2) <= n / (32 * grid) + 576 for any data,
+// so grid >= n / 2^36 bounds it by 2^31 + 576.
+int min_hist_grid(uint64_t n) {
+  const uint64_t g = (n + (uint64_t(1) << 36) - 1) >> 36;
+  return int(g < 1 ? 1 : g);
+}
+
 int auto_hist_grid(uint64_t n) {
   static int per_sm = 0;
-  if (per_sm == 0) {
-    cudaFuncSetAttribute(hist256_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(kHistSmem));
+  if (per_sm == 0) {  // (32 KiB of dynamic smem needs no opt-in for the query)
     int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, hist256_kernel<false>, BLOCK, kHistSmem);
     per_sm = b > 0 ? b : 1;
@@ -165,21 +174,21 @@ int auto_hist_grid(uint64_t n) {
   const uint64_t per_block = uint64_t(BLOCK) * 16 * UNROLL * 4;
   uint64_t need = (n + per_block - 1) / per_block;
   if (need < 1) need = 1;
-  return int(need < full ? need : full);
+  const uint64_t g = need < full ? need : full;
+  const uint64_t floor_g = uint64_t(min_hist_grid(n));
+  return int(g > floor_g ? g : floor_g);
 }
 
 static void configure_hist(bool px) {
-  static uint64_t configured[2] = {0, 0};  // one bit per device
-  const int dev = current_device();
-  if (dev < 64 && !(configured[px] >> dev & 1)) {
+  static DeviceMask configured[2];
+  configured[px].ensure([px] {
     if (px)
       cudaFuncSetAttribute(hist256_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(kHistSmem));
     else
       cudaFuncSetAttribute(hist256_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(kHistSmem));
-    configured[px] |= 1ull << dev;
-  }
+  });
 }
 
 cudaError_t launch_hist256(const uint8_t *in, uint64_t n, uint64_t *bins,

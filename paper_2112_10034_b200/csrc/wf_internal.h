@@ -2,6 +2,7 @@
 // units and the C ABI (wf_abi.cu).  Not part of the public interface.
 #pragma once
 
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -41,6 +42,26 @@ constexpr size_t kHistSmem = 256 * (WF_HIST_PRMT ? 64 : WF_HIST_BINW) * sizeof(u
 int sm_count(int device);
 int current_device();
 
+// Per-device one-time configuration: function attributes such as the
+// dynamic-smem opt-in are per device, so every launcher that needs one runs
+// ensure(f) before each launch; f runs once per device (idempotent, so two
+// threads racing on a first call is harmless).
+struct DeviceMask {
+  std::atomic<uint64_t> bits{0};
+  template <class F>
+  void ensure(F &&f) {
+    const int dev = current_device();
+    if (dev < 0 || dev >= 64) {
+      f();
+      return;
+    }
+    const uint64_t b = uint64_t(1) << dev;
+    if (bits.load(std::memory_order_acquire) & b) return;
+    f();
+    bits.fetch_or(b, std::memory_order_acq_rel);
+  }
+};
+
 // reductions (wf_reduce.cu)
 cudaError_t launch_reduce_i32(const int32_t *in, uint64_t n, int32_t *out,
                               int block, int grid, void *ws,
@@ -76,8 +97,8 @@ cudaError_t launch_compact_gt0_i32(const int32_t *in, uint64_t n,
                                    int32_t *out, uint64_t *count, void *ws,
                                    cudaStream_t s);
 
-// TMEM-parked single-pass scan / compaction (wf_scan_tmem.cu), 16 B aligned
-bool tmem_scan_enabled();
+// TMEM-parked single-pass scan / compaction (wf_scan_tmem.cu), any 4-byte
+// aligned buffers — the product kernels
 cudaError_t launch_scan_tmem_i32(const int32_t *in, int32_t *out, uint64_t n,
                                  const int32_t *carry, void *ws, cudaStream_t s);
 cudaError_t launch_compact_tmem_i32(const int32_t *in, uint64_t n, int32_t *out,
@@ -91,18 +112,29 @@ cudaError_t launch_compact_gt0_i32_mg(const int32_t *in, uint64_t n, int32_t *ou
                                       const void *mine, uint32_t cap, int rank, int world,
                                       uint32_t epoch, uint32_t *err, cudaStream_t s);
 
-// L2-streamed two-pass scan / compaction (wf_scan2p.cu), 16 B aligned buffers
+// Variant builds only (tools/variants/, -DWF_SCAN_IMPL != 0): the round-1
+// register-tile / smem-stage kernels and the L2-streamed two-pass kernels.
+#ifndef WF_SCAN_IMPL
+#define WF_SCAN_IMPL 0  // 0: TMEM (product) 1: smem-stage persistent 2: register tile 3: two-pass
+#endif
+#if WF_SCAN_IMPL != 0
+cudaError_t launch_scan_legacy_i32(int impl, const int32_t *in, int32_t *out, uint64_t n,
+                                   const int32_t *carry, void *ws, cudaStream_t s);
+cudaError_t launch_compact_legacy_i32(int impl, const int32_t *in, uint64_t n, int32_t *out,
+                                      uint64_t *count, void *ws, cudaStream_t s);
 bool two_pass_usable(uint64_t n);
 cudaError_t launch_scan2p_i32(const int32_t *in, int32_t *out, uint64_t n,
                               const int32_t *carry, void *ws, cudaStream_t s);
 cudaError_t launch_compact2p_i32(const int32_t *in, uint64_t n, int32_t *out,
                                  uint64_t *count, void *ws, cudaStream_t s);
+#endif
 
 // histogram (wf_hist.cu)
 cudaError_t launch_hist256(const uint8_t *in, uint64_t n, uint64_t *bins,
                            bool accumulate, int grid, void *ws,
                            cudaStream_t s);
 int auto_hist_grid(uint64_t n);
+int min_hist_grid(uint64_t n);  // counter-overflow floor for a caller's grid
 
 // warp collectives (wf_warp.cu)
 cudaError_t launch_warp_collective(int kind, const int32_t *a,

@@ -47,7 +47,6 @@
 #include "wf_internal.h"
 #include "wf_peer.cuh"
 
-#include <cstdlib>
 
 #ifndef WF_TM_STAGES
 #define WF_TM_STAGES 6  // smem stages per CTA (32 KiB each)
@@ -119,6 +118,7 @@ constexpr uint32_t TM_TILE = 4u * QVEC * 128;  // 8192 x TMUL items
 constexpr uint32_t SLOT_COLS = 64u * TMUL;     // TMEM columns per parked tile
 constexpr uint32_t TM_COLS = uint32_t(P) * SLOT_COLS;
 constexpr uint32_t kNoTileTm = 0xffffffffu;
+constexpr uint32_t kNoItem = 0xffffffffu;  // item_seq before the first publish
 static_assert((P & (P - 1)) == 0 && TM_COLS <= 512, "TMEM slots: power of two, <= 512 cols");
 static_assert(NLB >= 1 && NLB <= P, "look-back warps must not outnumber TMEM slots");
 static_assert(NFG <= NLB, "every finisher group must see one of the NLB stop items");
@@ -250,6 +250,9 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
     for (int p = 0; p < 2 * P; ++p) mbar_init(&sh.pref[p], 1);
     fence_barrier_init();
   }
+  // item ring: no entry holds a valid item index before its first publish
+  // (shared memory keeps whatever an earlier CTA left there)
+  if (threadIdx.x < 2 * P) sh.item_seq[threadIdx.x] = kNoItem;
   if (warp == W_PROD && lane == 0)
     sh.epoch = ld_volatile_u32(&hdr->epoch) & kEpochMask;  // before this CTA's first (release) draw
   tc_fence_before();
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
           if (leader) {
             sh.slot_tile[pe] = kNoTileTm;
             sh.item_tile[ie % (2 * P)] = kNoTileTm;
-            sh.item_seq[ie % (2 * P)] = ie;
+            st_release_cta_smem(&sh.item_seq[ie % (2 * P)], ie);
             mbar_arrive1(&sh.parked[pe]);
           }
         }
@@ -391,7 +394,7 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
         sh.slot_agg[p] = a;
         sh.item_tile[i % (2 * P)] = t;
         sh.item_agg[i % (2 * P)] = a;
-        sh.item_seq[i % (2 * P)] = i;
+        st_release_cta_smem(&sh.item_seq[i % (2 * P)], i);  // after tile / agg
         // publish the aggregate right here, not in the look-back warp: a
         // look-back warp busy with an older tile must never delay it
         if (t == 0) {
@@ -538,11 +541,12 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       // previous use of this slot belonged to another warp; a parity wait
       // issued while that phase is still open passes early.  The item ring
       // entry carries the item index, written before the arrive: wait for it.
+      // The acquire load pairs with the aggregator's release store, so the
+      // tile / aggregate read below are the ones published with index i.
       const int ri = int(i % (2 * P));
-      if (ld_volatile_u32(&sh.item_seq[ri]) != i) {
-        while (ld_volatile_u32(&sh.item_seq[ri]) != i) __nanosleep(32);
+      if (ld_acquire_cta_smem(&sh.item_seq[ri]) != i) {
+        while (ld_acquire_cta_smem(&sh.item_seq[ri]) != i) __nanosleep(32);
       }
-      __threadfence_block();
       const uint32_t t = sh.item_tile[ri];
       if (t == kNoTileTm) break;
       const uint32_t agg = sh.item_agg[ri];
@@ -576,14 +580,19 @@ constexpr size_t tm_smem() {
   return size_t(S) * TM_TILE * 4;
 }
 
-template <bool COMPACT>
+// Sets the dynamic-smem opt-in of the instantiation on the current device
+// (per device, before every launch) and returns the persistent grid.
+template <bool COMPACT, bool PX = false>
 int tmem_grid(uint32_t ntiles) {
   static int per_sm[2] = {0, 0};
+  static DeviceMask configured;
+  configured.ensure([] {
+    cudaFuncSetAttribute(tile_tmem_kernel<COMPACT, PX>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(tm_smem<COMPACT>()));
+  });
   int &b = per_sm[COMPACT];
   if (b == 0) {
-    cudaFuncSetAttribute(tile_tmem_kernel<COMPACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(tm_smem<COMPACT>()));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tile_tmem_kernel<COMPACT>, TM_THREADS,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tile_tmem_kernel<COMPACT, PX>, TM_THREADS,
                                                   tm_smem<COMPACT>());
     if (b > int(512 / TM_COLS)) b = int(512 / TM_COLS);  // TMEM: 512 columns per SM
     if (b < 1) b = 1;
@@ -600,11 +609,6 @@ extern "C" int wf_debug_set_trace_tm(void *buf) {
   return int(cudaMemcpyToSymbol(g_tm_trace, &p, sizeof(p)));
 }
 #endif
-
-bool tmem_scan_enabled() {
-  const char *e = getenv("WF_SCAN_TMEM");
-  return e == nullptr || e[0] != '0';
-}
 
 // `in` / `out` need only 4-byte alignment: the input is rounded down to 16 B
 // and its 0-3 leading elements masked; a scan output at another 16-byte
@@ -644,14 +648,7 @@ cudaError_t launch_compact_tmem_i32_mg(const int32_t *in, uint64_t n, int32_t *o
   const uint32_t head = uint32_t((reinterpret_cast<uintptr_t>(in) & 15u) / 4u);
   const uint64_t nv = n + head;
   const uint32_t nt = uint32_t((nv + TM_TILE - 1) / TM_TILE);
-  static bool configured[64] = {};
-  const int dev = current_device();
-  if (dev >= 0 && dev < 64 && !configured[dev]) {
-    cudaFuncSetAttribute(tile_tmem_kernel<true, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(tm_smem<true>()));
-    configured[dev] = true;
-  }
-  tile_tmem_kernel<true, true><<<tmem_grid<true>(nt), TM_THREADS, tm_smem<true>(), s>>>(
+  tile_tmem_kernel<true, true><<<tmem_grid<true, true>(nt), TM_THREADS, tm_smem<true>(), s>>>(
       in - head, out, nv, nt, nullptr, counts3, desc, hdr, head, false, pa);
   return cudaGetLastError();
 }

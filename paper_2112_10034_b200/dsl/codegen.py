@@ -20,7 +20,15 @@ to make every scalar operation mean exactly what it means in the reference:
 * Every global/shared access is bounds-checked; a violation records the
   reference's message ("out-of-bounds read a[100], length 32",
   interp/oracle.py:65-81) in a device error record, the access reads 0 / is
-  dropped, and the host raises ExecutionError after the launch.
+  dropped, the faulting thread leaves every loop at its next test (it stays
+  alive, so warp collectives keep their participants), and the host raises
+  ExecutionError after the launch.
+* Step limit (interp/oracle.py:113-119): every loop iteration counts one
+  step per thread; a thread past ``wf_step_limit`` records "thread T
+  exceeded the step limit" and leaves its loops, so a non-terminating kernel
+  ends with ExecutionError instead of hanging the GPU.  (An earlier form that
+  `return`ed from inside the loop made NVRTC miscompile kernels that mix
+  segment-masked votes with such loops: fuzz seeds 444 / 713 at W = 4.)
 * Collectives follow passes/warp_lower.py:17-45 / interp/oracle.py:147-161:
   ``shfl_down`` hands out-of-range lanes their own value for ANY offset (one
   SHFL.IDX with an explicitly computed source lane, not the 5-bit-masked
@@ -77,13 +85,23 @@ __device__ __forceinline__ int wf_add(int a, int b) { return (int)((unsigned)a +
 __device__ __forceinline__ int wf_sub(int a, int b) { return (int)((unsigned)a - (unsigned)b); }
 __device__ __forceinline__ int wf_mul(int a, int b) { return (int)((unsigned)a * (unsigned)b); }
 __device__ __forceinline__ int wf_neg(int a) { return (int)(0u - (unsigned)a); }
-__device__ __forceinline__ int wf_div(int a, int b, wf_err_t *e) {
-  if (b == 0) { wf_fail(e, 3, -1, 0, 0); return 0; }
+// loop test: false once the thread faulted or ran out of steps
+__device__ __forceinline__ bool wf_live(int &dead, long long &steps, long long limit, wf_err_t *e) {
+  if (dead) return false;
+  if (++steps > limit) {
+    wf_fail(e, 5, -1, (long long)blockIdx.x * blockDim.x + threadIdx.x, 0);
+    dead = 1;
+    return false;
+  }
+  return true;
+}
+__device__ __forceinline__ int wf_div(int a, int b, wf_err_t *e, int &dead) {
+  if (b == 0) { if (!dead) wf_fail(e, 3, -1, 0, 0); dead = 1; return 0; }
   if (a == WF_INT_MIN && b == -1) return WF_INT_MIN;
   return a / b;
 }
-__device__ __forceinline__ int wf_rem(int a, int b, wf_err_t *e) {
-  if (b == 0) { wf_fail(e, 4, -1, 0, 0); return 0; }
+__device__ __forceinline__ int wf_rem(int a, int b, wf_err_t *e, int &dead) {
+  if (b == 0) { if (!dead) wf_fail(e, 4, -1, 0, 0); dead = 1; return 0; }
   if (b == -1) return 0;
   return a % b;
 }
@@ -92,13 +110,15 @@ __device__ __forceinline__ float wf_f(float a) { return a; }
 __device__ __forceinline__ int wf_land(int a, int b) { return (a != 0 && b != 0) ? 1 : 0; }
 __device__ __forceinline__ int wf_lor(int a, int b) { return (a != 0 || b != 0) ? 1 : 0; }
 template <typename T>
-__device__ __forceinline__ T wf_ld(const T *p, long long len, long long i, long long arg, wf_err_t *e) {
-  if (i < 0 || i >= len) { wf_fail(e, 1, arg, i, len); return (T)0; }
+__device__ __forceinline__ T wf_ld(const T *p, long long len, long long i, long long arg, wf_err_t *e,
+                                   int &dead) {
+  if (i < 0 || i >= len) { if (!dead) wf_fail(e, 1, arg, i, len); dead = 1; return (T)0; }
   return p[i];
 }
 template <typename T>
-__device__ __forceinline__ void wf_st(T *p, long long len, long long i, T v, long long arg, wf_err_t *e) {
-  if (i < 0 || i >= len) { wf_fail(e, 2, arg, i, len); return; }
+__device__ __forceinline__ void wf_st(T *p, long long len, long long i, T v, long long arg, wf_err_t *e,
+                                      int &dead) {
+  if (i < 0 || i >= len) { if (!dead) wf_fail(e, 2, arg, i, len); dead = 1; return; }
   p[i] = v;
 }
 // ---- warp collectives over W-lane segments of the hardware warp ----------
@@ -226,7 +246,7 @@ class CudaGen:
             idx, _ = self.expr(e.index)
             kind = self.t.element_kind(e.base)
             return (f"wf_ld<{CTYPE[kind]}>({self.arr_ptr(e.base)}, {self.arr_len(e.base)}, "
-                    f"(long long)({idx}), {self.arr_id(e.base)}, wf_e)"), kind
+                    f"(long long)({idx}), {self.arr_id(e.base)}, wf_e, wf_dead)"), kind
         if isinstance(e, n.Unary):
             c, k = self.expr(e.operand)
             if e.op == "!":
@@ -254,7 +274,7 @@ class CudaGen:
             fn = {"+": "__fadd_rn", "-": "__fsub_rn", "*": "__fmul_rn", "/": "__fdiv_rn"}[e.op]
             return f"{fn}(wf_f({a}), wf_f({b}))", F32
         if e.op in ("/", "%"):
-            return f"{'wf_div' if e.op == '/' else 'wf_rem'}({a}, {b}, wf_e)", I32
+            return f"{'wf_div' if e.op == '/' else 'wf_rem'}({a}, {b}, wf_e, wf_dead)", I32
         fn = {"+": "wf_add", "-": "wf_sub", "*": "wf_mul"}[e.op]
         return f"{fn}({a}, {b})", I32
 
@@ -303,7 +323,8 @@ class CudaGen:
         else:
             kind = self.t.element_kind(tg.base)
             code = (f"wf_st<{CTYPE[kind]}>({self.arr_ptr(tg.base)}, {self.arr_len(tg.base)}, "
-                    f"(long long)({idx}), {self.convert(val, vk, kind)}, {self.arr_id(tg.base)}, wf_e)")
+                    f"(long long)({idx}), {self.convert(val, vk, kind)}, {self.arr_id(tg.base)}, wf_e, "
+                    f"wf_dead)")
         if self.trace:
             code = f"{code}, wf_tick(wf_tr, {uid})"
         if as_expr:
@@ -371,6 +392,11 @@ class CudaGen:
             raise TransformError(f"cannot generate {type(s).__name__}")
         return True
 
+    # every loop test: the condition first (its collectives run for every
+    # live lane), then the step budget; a faulted thread leaves the loop (the
+    # reference stops at the first fault)
+    LIVE = "wf_live(wf_dead, wf_steps, wf_step_limit, wf_e)"
+
     def loop(self, s: n.For, depth: int) -> None:
         if not self.trace:
             if isinstance(s.init, n.DeclLocal):
@@ -389,7 +415,8 @@ class CudaGen:
             if alive:
                 self.expr(s.cond)
                 self.new_uid("CondBr")
-            self.lines[start] = "  " * depth + f"for ({init}; ({c}) != 0; {step}) {{"
+            self.lines[start] = ("  " * depth +
+                                 f"for ({init}; ({c}) != 0 && {self.LIVE}; {step}) {{")
             self.emit("}", depth)
             return
         # trace mode: the reference's bottom-tested shape (cfg/build.py:116-134)
@@ -397,14 +424,15 @@ class CudaGen:
         self.init_stmt(s.init, depth)
         c1, _ = self.expr(s.cond)
         g = self.new_uid("CondBr")
-        self.emit(f"{self.tick(g)}if (({c1}) != 0) {{", depth)
+        self.emit(f"{self.tick(g)}if (({c1}) != 0 && {self.LIVE}) {{", depth)
         self.emit("do {", depth + 1)
         alive = self.stmts(s.body, depth + 2)
         if alive:
             self.assign(s.step, depth + 2)
             c2, _ = self.expr(s.cond)
             latch = self.new_uid("CondBr")
-            self.emit(f"}} while ((wf_tick(wf_tr, {latch}), ({c2}) != 0));", depth + 1)
+            self.emit(f"}} while ((wf_tick(wf_tr, {latch}), ({c2}) != 0) && {self.LIVE});",
+                      depth + 1)
         else:
             self.emit("} while (0);", depth + 1)
         self.emit("}", depth)
@@ -417,7 +445,7 @@ class CudaGen:
                 params.append(f"long long p_{p.name}_len")
             else:
                 params.append(f"{CTYPE[p.kind]} p_{p.name}")
-        params += ["wf_err_t *__restrict__ wf_e", "long long wf_dyn_len"]
+        params += ["wf_err_t *__restrict__ wf_e", "long long wf_dyn_len", "long long wf_step_limit"]
         if self.trace:
             params.append("unsigned long long *__restrict__ wf_tr")
         ret_uid = self.new_uid("Ret")  # the exit block's Ret is allocated first
@@ -434,6 +462,8 @@ class CudaGen:
                        f"s_{name}[i] = ({CTYPE[kind]})0;")
         if self.t.shared:
             out.append("  __syncthreads();")
+        out.append("  int wf_dead = 0;")
+        out.append("  long long wf_steps = 0;")
         for name, kind in self.t.locals.items():
             out.append(f"  {CTYPE[kind]} v_{name} = ({CTYPE[kind]})0;")
         if self.stmts(self.k.body, 1):

@@ -25,6 +25,12 @@ from . import nodes as n
 from .checker import SymbolTable, check_kernel
 from .codegen import generate, generate_traced
 
+# Loop iterations one thread may run before the launch fails with
+# ExecutionError("thread T exceeded the step limit") — the reference's
+# per-thread interpreter budget (interp/oracle.py:26, :113-119), counted in
+# loop iterations rather than instructions.
+DEFAULT_STEP_LIMIT = 50_000_000
+
 _cache_lock = threading.Lock()
 _fault_bufs: dict = {}
 
@@ -129,7 +135,8 @@ class JitProgram:
                 _module_cache[src] = mod
         return mod
 
-    def run(self, config: LaunchConfig, memory, bound: dict, trace=None) -> None:
+    def run(self, config: LaunchConfig, memory, bound: dict, trace=None,
+            step_limit: int = DEFAULT_STEP_LIMIT) -> None:
         import torch
         if self.specialized and (self.specialized["block_size"] != config.block_size or
                                  self.specialized["grid_size"] != config.grid_size):
@@ -150,7 +157,7 @@ class JitProgram:
         dyn = [s for s, (_, ln) in self.table.shared.items() if ln is None]
         elem = 4
         dyn_len = config.shared_bytes // elem if dyn else 0
-        keep += [C.c_void_p(err.data_ptr()), C.c_longlong(dyn_len)]
+        keep += [C.c_void_p(err.data_ptr()), C.c_longlong(dyn_len), C.c_longlong(int(step_limit))]
         if trace is not None:
             counts = torch.zeros(self.layout.max_uid + 1, dtype=torch.int64, device=memory.device)
             keep.append(C.c_void_p(counts.data_ptr()))
@@ -183,6 +190,8 @@ class JitProgram:
             return "integer division by zero"
         if code == 4:
             return "integer remainder by zero"
+        if code == 5:
+            return f"thread {idx} exceeded the step limit"
         return f"device fault {code}"
 
 

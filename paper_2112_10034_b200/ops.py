@@ -12,6 +12,7 @@ semantics.
 
 from __future__ import annotations
 
+import contextlib
 import threading
 
 import torch
@@ -38,6 +39,16 @@ def _stream_handle(stream=None) -> int:
     if _raw_stream is not None:
         return int(_raw_stream(torch.cuda.current_device()))
     return int(torch.cuda.current_stream().cuda_stream)
+
+
+def _on(device) -> contextlib.AbstractContextManager:
+    """Make ``device`` current for one launch: the C ABI launches on the
+    current device and stream, so a tensor on another GPU must switch first
+    (a no-op context when it is already current)."""
+    idx = device.index if isinstance(device, torch.device) else int(device)
+    if idx is None or idx == torch.cuda.current_device():
+        return contextlib.nullcontext()
+    return torch.cuda.device(idx)
 
 
 def workspace(op: int, n: int, device: torch.device, stream=None) -> torch.Tensor:
@@ -90,10 +101,11 @@ def reduce_sum_i32(x: torch.Tensor, out: torch.Tensor | None = None, block: int 
     if out is None:
         out = torch.empty(1, dtype=torch.int32, device=x.device)
     _require_cuda(out, torch.int32, "out")
-    ws = workspace(_lib.OP_REDUCE_SUM_I32, x.numel(), x.device)
-    check(_lib.load().wf_reduce_sum_i32(x.data_ptr(), x.numel(), out.data_ptr(), block, grid,
-                                        ws.data_ptr(), ws.numel(), _stream_handle()),
-          "reduce_sum_i32")
+    with _on(x.device):
+        ws = workspace(_lib.OP_REDUCE_SUM_I32, x.numel(), x.device)
+        check(_lib.load().wf_reduce_sum_i32(x.data_ptr(), x.numel(), out.data_ptr(), block, grid,
+                                            ws.data_ptr(), ws.numel(), _stream_handle()),
+              "reduce_sum_i32")
     return out
 
 
@@ -105,10 +117,11 @@ def reduce_sum_f32(x: torch.Tensor, out: torch.Tensor | None = None, block: int 
     if out is None:
         out = torch.empty(1, dtype=torch.float32, device=x.device)
     _require_cuda(out, torch.float32, "out")
-    ws = workspace(_lib.OP_REDUCE_SUM_F32, x.numel(), x.device)
-    check(_lib.load().wf_reduce_sum_f32(x.data_ptr(), x.numel(), out.data_ptr(), block, grid,
-                                        ws.data_ptr(), ws.numel(), _stream_handle()),
-          "reduce_sum_f32")
+    with _on(x.device):
+        ws = workspace(_lib.OP_REDUCE_SUM_F32, x.numel(), x.device)
+        check(_lib.load().wf_reduce_sum_f32(x.data_ptr(), x.numel(), out.data_ptr(), block, grid,
+                                            ws.data_ptr(), ws.numel(), _stream_handle()),
+              "reduce_sum_f32")
     return out
 
 
@@ -124,7 +137,8 @@ def fold(vals: torch.Tensor, count: int | None = None,
     _require_cuda(vals, vals.dtype, "vals")
     if out is None:
         out = torch.empty(1, dtype=vals.dtype, device=vals.device)
-    check(fns[vals.dtype](vals.data_ptr(), count, out.data_ptr(), _stream_handle()), "fold")
+    with _on(vals.device):
+        check(fns[vals.dtype](vals.data_ptr(), count, out.data_ptr(), _stream_handle()), "fold")
     return out
 
 
@@ -144,10 +158,11 @@ def scan_inclusive_i32(x: torch.Tensor, out: torch.Tensor | None = None,
     if carry is not None:
         _require_cuda(carry, torch.int32, "carry")
         cptr = carry.data_ptr()
-    ws = workspace(_lib.OP_SCAN_INCLUSIVE_I32, x.numel(), x.device)
-    check(_lib.load().wf_scan_inclusive_i32(x.data_ptr(), out.data_ptr(), x.numel(), cptr,
-                                            ws.data_ptr(), ws.numel(), _stream_handle()),
-          "scan_inclusive_i32")
+    with _on(x.device):
+        ws = workspace(_lib.OP_SCAN_INCLUSIVE_I32, x.numel(), x.device)
+        check(_lib.load().wf_scan_inclusive_i32(x.data_ptr(), out.data_ptr(), x.numel(), cptr,
+                                                ws.data_ptr(), ws.numel(), _stream_handle()),
+              "scan_inclusive_i32")
     return out
 
 
@@ -165,11 +180,12 @@ def compact_gt0_i32(x: torch.Tensor, out: torch.Tensor | None = None,
     if count is None:
         count = torch.empty(1, dtype=torch.int64, device=x.device)
     _require_cuda(count, torch.int64, "count")
-    ws = workspace(_lib.OP_COMPACT_GT0_I32, x.numel(), x.device)
-    check(_lib.load().wf_compact_gt0_i32(x.data_ptr(), x.numel(), out.data_ptr(),
-                                         count.data_ptr(), ws.data_ptr(), ws.numel(),
-                                         _stream_handle()),
-          "compact_gt0_i32")
+    with _on(x.device):
+        ws = workspace(_lib.OP_COMPACT_GT0_I32, x.numel(), x.device)
+        check(_lib.load().wf_compact_gt0_i32(x.data_ptr(), x.numel(), out.data_ptr(),
+                                             count.data_ptr(), ws.data_ptr(), ws.numel(),
+                                             _stream_handle()),
+              "compact_gt0_i32")
     return out, count
 
 
@@ -182,10 +198,11 @@ def histogram256_u8(x: torch.Tensor, bins: torch.Tensor | None = None,
     _require_cuda(bins, torch.int64, "bins")
     if bins.numel() < 256:
         raise LaunchError("bins must hold 256 counters")
-    ws = workspace(_lib.OP_HISTOGRAM256_U8, x.numel(), x.device)
-    check(_lib.load().wf_histogram256_u8(x.data_ptr(), x.numel(), bins.data_ptr(), grid,
-                                         ws.data_ptr(), ws.numel(), _stream_handle()),
-          "histogram256_u8")
+    with _on(x.device):
+        ws = workspace(_lib.OP_HISTOGRAM256_U8, x.numel(), x.device)
+        check(_lib.load().wf_histogram256_u8(x.data_ptr(), x.numel(), bins.data_ptr(), grid,
+                                             ws.data_ptr(), ws.numel(), _stream_handle()),
+              "histogram256_u8")
     return bins
 
 
@@ -209,11 +226,12 @@ def warp_collective(kind: str, a: torch.Tensor, b: torch.Tensor | None = None,
     if out is None:
         out = torch.zeros_like(a)
     _require_cuda(out, torch.int32, "out")
-    check(_lib.load().wf_warp_collective(_lib.COLL[kind], a.data_ptr(),
-                                         b.data_ptr() if b is not None else None,
-                                         int(operand), out.data_ptr(), a.numel(), block, width,
-                                         mask & 0xFFFFFFFF, _stream_handle()),
-          "warp_collective")
+    with _on(a.device):
+        check(_lib.load().wf_warp_collective(_lib.COLL[kind], a.data_ptr(),
+                                             b.data_ptr() if b is not None else None,
+                                             int(operand), out.data_ptr(), a.numel(), block, width,
+                                             mask & 0xFFFFFFFF, _stream_handle()),
+              "warp_collective")
     return out
 
 
@@ -233,10 +251,11 @@ def fill_synthetic(gen: str, n: int, seed: int = 0, base: int = 0, param: int = 
     if out is None:
         device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
         out = torch.empty(n, dtype=_GEN_DTYPE[gen], device=device)
-    check(_lib.load().wf_fill_synthetic(_lib.GEN[gen], out.data_ptr(), n,
-                                        seed & 0xFFFFFFFFFFFFFFFF, base, param,
-                                        _stream_handle()),
-          "fill_synthetic")
+    with _on(out.device):
+        check(_lib.load().wf_fill_synthetic(_lib.GEN[gen], out.data_ptr(), n,
+                                            seed & 0xFFFFFFFFFFFFFFFF, base, param,
+                                            _stream_handle()),
+              "fill_synthetic")
     return out
 
 
@@ -271,11 +290,12 @@ def reduce_sum_f32_host(host_x, device=None) -> float:
     device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
     ptr, n = _host_ptr(host_x)
     out = np.zeros(1, dtype=np.float32)
-    st = _staging(device)
-    ws = workspace(_lib.OP_REDUCE_SUM_F32, n, device)
-    check(_lib.load().wf_reduce_sum_f32_host(ptr, n, out.ctypes.data, st.data_ptr(), st.numel(),
-                                             ws.data_ptr(), ws.numel(), _stream_handle()),
-          "reduce_sum_f32_host")
+    with _on(device):
+        st = _staging(device)
+        ws = workspace(_lib.OP_REDUCE_SUM_F32, n, device)
+        check(_lib.load().wf_reduce_sum_f32_host(ptr, n, out.ctypes.data, st.data_ptr(), st.numel(),
+                                                 ws.data_ptr(), ws.numel(), _stream_handle()),
+              "reduce_sum_f32_host")
     return float(out[0])
 
 
@@ -284,11 +304,12 @@ def reduce_sum_i32_host(host_x, device=None) -> int:
     device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
     ptr, n = _host_ptr(host_x)
     out = np.zeros(1, dtype=np.int32)
-    st = _staging(device)
-    ws = workspace(_lib.OP_REDUCE_SUM_I32, n, device)
-    check(_lib.load().wf_reduce_sum_i32_host(ptr, n, out.ctypes.data, st.data_ptr(), st.numel(),
-                                             ws.data_ptr(), ws.numel(), _stream_handle()),
-          "reduce_sum_i32_host")
+    with _on(device):
+        st = _staging(device)
+        ws = workspace(_lib.OP_REDUCE_SUM_I32, n, device)
+        check(_lib.load().wf_reduce_sum_i32_host(ptr, n, out.ctypes.data, st.data_ptr(), st.numel(),
+                                                 ws.data_ptr(), ws.numel(), _stream_handle()),
+              "reduce_sum_i32_host")
     return int(out[0])
 
 
@@ -297,10 +318,71 @@ def histogram256_u8_host(host_x, device=None):
     device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
     ptr, n = _host_ptr(host_x)
     out = np.zeros(256, dtype=np.uint64)
-    st = _staging(device)
-    ws = workspace(_lib.OP_HISTOGRAM256_U8, n, device)
-    check(_lib.load().wf_histogram256_u8_host(ptr, n, out.ctypes.data, st.data_ptr(),
-                                              st.numel(), ws.data_ptr(), ws.numel(),
-                                              _stream_handle()),
-          "histogram256_u8_host")
+    with _on(device):
+        st = _staging(device)
+        ws = workspace(_lib.OP_HISTOGRAM256_U8, n, device)
+        check(_lib.load().wf_histogram256_u8_host(ptr, n, out.ctypes.data, st.data_ptr(),
+                                                  st.numel(), ws.data_ptr(), ws.numel(),
+                                                  _stream_handle()),
+              "histogram256_u8_host")
     return out
+
+
+def _host_out(host_out, n: int, dtype):
+    import numpy as np
+    if host_out is None:
+        return np.empty(n, dtype=dtype)
+    if isinstance(host_out, torch.Tensor):
+        if host_out.is_cuda or not host_out.is_contiguous() or host_out.numel() < n:
+            raise LaunchError(f"host output must be a contiguous CPU tensor of >= {n} elements")
+        return host_out
+    a = host_out
+    if not (isinstance(a, np.ndarray) and a.flags.c_contiguous and a.flags.writeable and
+            a.dtype == dtype and a.size >= n):
+        raise LaunchError(f"host output must be a writable contiguous {np.dtype(dtype)} array "
+                          f"of >= {n} elements")
+    return a
+
+
+def _addr(a) -> int:
+    return a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data
+
+
+def scan_inclusive_i32_host(host_x, host_out=None, carry: int | None = None, device=None):
+    """End-to-end inclusive scan of a host buffer into a host buffer (pinned
+    for full PCIe speed): H2D, K3 and D2H of successive chunks overlapped,
+    one carry chain across chunks.  Synchronous; returns ``host_out``."""
+    import ctypes
+    import numpy as np
+    device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    ptr, n = _host_ptr(host_x)
+    out = _host_out(host_out, n, np.int32)
+    cin = ctypes.c_int32(int(carry)) if carry is not None else None
+    with _on(device):
+        st = _staging(device)
+        ws = workspace(_lib.OP_SCAN_INCLUSIVE_I32, STAGING_BYTES // 4, device)
+        check(_lib.load().wf_scan_inclusive_i32_host(
+            ptr, _addr(out), n, ctypes.addressof(cin) if cin is not None else None,
+            st.data_ptr(), st.numel(), ws.data_ptr(), ws.numel(), _stream_handle()),
+            "scan_inclusive_i32_host")
+    return out
+
+
+def compact_gt0_i32_host(host_x, host_out=None, device=None):
+    """End-to-end order-preserving ``x[x > 0]`` from a host buffer into a host
+    buffer.  Returns ``(host_out, count)``; the first ``count`` elements are
+    the selected ones.  Synchronous."""
+    import ctypes
+    import numpy as np
+    device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    ptr, n = _host_ptr(host_x)
+    out = _host_out(host_out, n, np.int32)
+    cnt = ctypes.c_uint64(0)
+    with _on(device):
+        st = _staging(device)
+        ws = workspace(_lib.OP_COMPACT_GT0_I32, STAGING_BYTES // 4, device)
+        check(_lib.load().wf_compact_gt0_i32_host(
+            ptr, n, _addr(out), ctypes.addressof(cnt), st.data_ptr(), st.numel(),
+            ws.data_ptr(), ws.numel(), _stream_handle()),
+            "compact_gt0_i32_host")
+    return out, int(cnt.value)

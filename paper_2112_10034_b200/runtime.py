@@ -62,7 +62,7 @@ def bind_args(params, memory: DeviceMemory, args) -> dict:
         if p.is_buffer:
             if not _is_int(a):
                 raise LaunchError(f"argument {p.name!r} must be a buffer id, got {a!r}")
-            bound[p.name] = memory.view(int(a), p.kind)
+            bound[p.name] = memory.bind_view(int(a), p.kind)
         elif p.kind in ("i32", "i64"):
             if not _is_int(a):
                 raise LaunchError(f"argument {p.name!r} must be an {p.kind} scalar, got {a!r}")
@@ -84,11 +84,14 @@ def launch(program, config: LaunchConfig, memory: DeviceMemory, args, trace=None
             f"named native op with no reference CFG")
     bound = bind_args(program.params, memory, args)
     with torch.cuda.device(memory.device):
-        if trace is None:
-            program.run(config, memory, bound)
-        else:  # DSL kernel compiled with per-uid counters (interp/trace.py:9-50)
-            program.run(config, memory, bound, trace=trace)
-        torch.cuda.current_stream(memory.device).synchronize()
+        try:
+            if trace is None:
+                program.run(config, memory, bound)
+            else:  # DSL kernel compiled with per-uid counters (interp/trace.py:9-50)
+                program.run(config, memory, bound, trace=trace)
+            torch.cuda.current_stream(memory.device).synchronize()
+        finally:  # numpy views of the bound buffers show what the kernel wrote
+            memory.refresh([int(a) for p, a in zip(program.params, args) if p.is_buffer])
 
 
 # ---- named programs (K1-K5) ------------------------------------------------

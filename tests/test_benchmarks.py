@@ -73,3 +73,13 @@ def test_bench_cli_scaling_two_processes_one_gpu():
     rows = json.loads(r.stdout.strip().splitlines()[-1])["scaling"]
     assert [row["n_gpus"] for row in rows] == [2] * 4
     assert all(row["exchange"] == "peer memory (fused)" for row in rows), rows
+
+
+def test_bench_refuses_a_world_size_other_than_gpus():
+    """`--gpus N` is the GPU count measured: under a launcher whose world size
+    differs, bench.py exits non-zero instead of reporting another N."""
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0")
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--impl", "reference",
+                        "--no-cpu-baseline"], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=120)
+    assert r.returncode == 2 and "refusing" in r.stderr

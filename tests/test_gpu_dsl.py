@@ -100,6 +100,26 @@ def test_out_of_bounds_reports_index_and_length(wf):
              wf.LaunchConfig(grid_size=1, block_size=32), [("i32", np.zeros(32))])
 
 
+def test_non_terminating_loop_hits_step_limit(wf):
+    """A kernel that never terminates ends with the reference's step-limit
+    ExecutionError (interp/oracle.py:113-119) instead of hanging the GPU."""
+    src = ("__global__ void k(global i32* a) { i32 s = 0; "
+           "for (i32 i = 0; i >= 0; i = i * 1) { s = s + 1; } a[threadIdx.x] = s; }")
+    with pytest.raises(wf.ExecutionError, match="exceeded the step limit"):
+        _run(wf, src, wf.LaunchConfig(grid_size=2, block_size=64), [("i32", np.zeros(128))])
+
+
+def test_scan_past_end_stops_at_first_fault(wf):
+    """A data-dependent loop that walks off the end of its buffer (reads 0
+    after the end, so it would never stop) faults once and leaves: the
+    launch reports the first out-of-bounds read, no hang."""
+    src = ("__global__ void k(global i32* a, global i32* out) { i32 i = 0; "
+           "for (i32 j = 0; a[i] == 0; j = j + 1) { i = i + 1; } out[threadIdx.x] = i; }")
+    with pytest.raises(wf.ExecutionError, match=r"out-of-bounds read a\[8\], length 8"):
+        _run(wf, src, wf.LaunchConfig(grid_size=1, block_size=32),
+             [("i32", np.zeros(8)), ("i32", np.zeros(32))])
+
+
 def test_division_by_zero_faults(wf):
     with pytest.raises(wf.ExecutionError, match="integer division by zero"):
         _run(wf, "__global__ void k(global i32* a, i32 d) { a[threadIdx.x] = 7 / d; }",

@@ -224,89 +224,19 @@ def test_compact_full_config(ops):
     assert torch.equal(out[:m], want)
 
 
-# ---- K3/K4 smem-stage persistent kernel (WF_SCAN_TMEM=0 fallback) -----------
+# ---- K3/K4 many launches on one workspace ----------------------------------
 
-@pytest.mark.parametrize("n", [1, 4097, 8192 * 5 + 3, (1 << 20) + 3, (1 << 22) + 13])
-def test_smem_stage_kernel_scan_compact(ops, monkeypatch, n):
-    """The pre-TMEM kernels stay selectable (A/B baseline): the smem-stage
-    persistent kernel (aligned) and the register-tile kernel (4-byte views)."""
-    monkeypatch.setenv("WF_SCAN_TMEM", "0")
-    a = synthetic.generate("i32_full", n, seed=n + 9)
-    assert np.array_equal(host(ops.scan_inclusive_i32(dev(a))), no.scan_inclusive_i32(a))
-    out, cnt = ops.compact_gt0_i32(dev(a))
-    want = no.compact_gt0_i32(a)
-    assert int(host(cnt)[0]) == len(want) and np.array_equal(host(out)[:len(want)], want)
-    # 4-byte-aligned views: the register-tile single-pass kernels
-    b = dev(np.concatenate([[5], a]).astype(np.int32))
-    assert np.array_equal(host(ops.scan_inclusive_i32(b[1:])), no.scan_inclusive_i32(a))
-    out, cnt = ops.compact_gt0_i32(b[1:])
-    assert int(host(cnt)[0]) == len(want) and np.array_equal(host(out)[:len(want)], want)
-
-
-def test_tmem_kernel_many_launches_interleaved(ops, monkeypatch):
-    """TMEM-parked kernel: epochs/tickets survive interleaving with the smem
-    kernel on one workspace, and sizes from one ragged tile to many tiles."""
+def test_tmem_kernel_many_launches(ops):
+    """TMEM-parked kernel: epochs/tickets survive back-to-back launches on one
+    workspace, sizes from one ragged tile to many tiles.  (The round-1
+    smem-stage / register-tile / two-pass kernels are variant builds now:
+    tools/variants/check_variants.py.)"""
     for i, n in enumerate([8192 * 148 * 3 + 17, 5, 8192, 8193, 1 << 21, 77777]):
-        monkeypatch.setenv("WF_SCAN_TMEM", "0" if i % 3 == 2 else "1")
         a = synthetic.generate("i32_select", n, seed=i, param=700)
         assert np.array_equal(host(ops.scan_inclusive_i32(dev(a))), no.scan_inclusive_i32(a))
         out, cnt = ops.compact_gt0_i32(dev(a))
         want = no.compact_gt0_i32(a)
         assert int(host(cnt)[0]) == len(want) and np.array_equal(host(out)[:len(want)], want)
-
-
-# ---- K3/K4 opt-in L2-streamed two-pass variant (wf_scan2p.cu) ---------------
-
-@pytest.fixture
-def two_pass(monkeypatch):
-    """Enable the two-pass kernels with a tiny size threshold and small chunks
-    so modest inputs span many chunks (look-back over chunk descriptors,
-    ragged last chunk and tile)."""
-    monkeypatch.setenv("WF_SCAN_2P", "1")
-    monkeypatch.setenv("WF_2P_MIN_N", "1")
-    monkeypatch.setenv("WF_2P_CHUNK_TILES", "3")
-    yield monkeypatch
-
-
-@pytest.mark.parametrize("n", [1, 4097, 8192 * 7, 8192 * 7 + 3, 1 << 20, (1 << 22) + 13])
-def test_two_pass_scan_compact(ops, two_pass, n):
-    a = synthetic.generate("i32_full", n, seed=n + 5)
-    assert np.array_equal(host(ops.scan_inclusive_i32(dev(a))), no.scan_inclusive_i32(a))
-    carry = torch.tensor([-7], dtype=torch.int32, device="cuda")
-    assert np.array_equal(host(ops.scan_inclusive_i32(dev(a), carry=carry)),
-                          no.scan_inclusive_i32(a, carry=-7))
-    out, cnt = ops.compact_gt0_i32(dev(a))
-    want = no.compact_gt0_i32(a)
-    assert int(host(cnt)[0]) == len(want) and np.array_equal(host(out)[:len(want)], want)
-
-
-def test_two_pass_interleaved_with_single_pass(ops, two_pass):
-    # one cached workspace serves both designs: stale single-pass descriptors
-    # must never read as two-pass state (8 KiB header rule, epochs)
-    for i, n in enumerate([1 << 18, 5000, (1 << 18) + 77, 1 << 16]):
-        two_pass.setenv("WF_SCAN_2P", "1" if i % 2 == 0 else "0")
-        for chunk in ("1", "64"):
-            two_pass.setenv("WF_2P_CHUNK_TILES", chunk)
-            a = synthetic.generate("i32_select", n, seed=i, param=300)
-            assert np.array_equal(host(ops.scan_inclusive_i32(dev(a))), no.scan_inclusive_i32(a))
-            out, cnt = ops.compact_gt0_i32(dev(a))
-            want = no.compact_gt0_i32(a)
-            assert int(host(cnt)[0]) == len(want)
-            assert np.array_equal(host(out)[:len(want)], want)
-
-
-@pytest.mark.slow
-def test_two_pass_full_config(ops, monkeypatch):
-    monkeypatch.setenv("WF_SCAN_2P", "1")
-    n = 1 << 28
-    x = ops.fill_synthetic("i32_full", n, seed=9)
-    y = ops.scan_inclusive_i32(x)
-    d = (y[1:].to(torch.int64) - y[:-1].to(torch.int64) - x[1:].to(torch.int64)) % (1 << 32)
-    assert int(d.count_nonzero()) == 0 and host(y[:1])[0] == host(x[:1])[0]
-    del y, d
-    out, cnt = ops.compact_gt0_i32(x)
-    want = torch.masked_select(x, x > 0)
-    assert int(host(cnt)[0]) == want.numel() and torch.equal(out[:want.numel()], want)
 
 
 # ---- K5 ----------------------------------------------------------------------
@@ -337,24 +267,66 @@ def test_hist_misaligned_and_grids(ops):
         assert np.array_equal(got, no.histogram256_u8(a))
 
 
+def _bincount_slices(x, parts=16):
+    """Independent check: sum of torch.bincount over ``parts`` slices."""
+    total = torch.zeros(256, dtype=torch.int64, device=x.device)
+    step = (x.numel() + parts - 1) // parts
+    for lo in range(0, x.numel(), step):
+        total += torch.bincount(x[lo:lo + step].to(torch.int32), minlength=256)
+    return total.cpu().numpy().astype(np.uint64)
+
+
 @pytest.mark.slow
 def test_hist_full_config(ops):
-    """BASELINE config 5 on one GPU: 2^32 uint8 (4 GiB)."""
+    """BASELINE config 5 on one GPU: 2^32 uint8 (4 GiB), the whole histogram
+    against 16 independent torch.bincount slices, plus linearity."""
     n = 1 << 32
     x = ops.fill_synthetic("u8_uniform", n, seed=4)
     bins = host(ops.histogram256_u8(x)).view(np.uint64)
     assert int(bins.sum()) == n
-    # linearity: the histogram of the whole == sum of histograms of 8 slices
+    assert np.array_equal(bins, _bincount_slices(x))
     parts = np.zeros(256, dtype=np.uint64)
     step = n // 8
     for k in range(8):
         parts += host(ops.histogram256_u8(x[k * step:(k + 1) * step])).view(np.uint64)
     assert np.array_equal(parts, bins)
-    # one slice against torch's own bincount
-    tb = torch.bincount(x[:1 << 28].to(torch.int32), minlength=256).cpu().numpy()
-    got = host(ops.histogram256_u8(x[:1 << 28])).view(np.uint64)
-    assert np.array_equal(got, tb.astype(np.uint64))
     del x
+
+
+@pytest.mark.slow
+def test_hist_full_config_single_value(ops):
+    """All-same-value bytes at 2^32: one bin reaches 2^32 (overflows any u32
+    count) — exact on the auto grid."""
+    n = 1 << 32
+    x = ops.fill_synthetic("u8_const", n, seed=4)
+    v = int(host(x[:1])[0])
+    bins = host(ops.histogram256_u8(x)).view(np.uint64)
+    want = np.zeros(256, dtype=np.uint64)
+    want[v] = n
+    assert np.array_equal(bins, want)
+    del x
+
+
+@pytest.mark.slow
+def test_hist_one_block_counts_2p32_of_one_byte(ops):
+    """grid=1 over 2^32 equal bytes: the single block's per-bin fold is
+    64-bit (a u32 fold wraps to 0 here), and the per-(bin, lane) u32
+    counters stay below 2^32 (2^27 each)."""
+    n = 1 << 32
+    x = torch.full((n,), 0xA5, dtype=torch.uint8, device="cuda")
+    bins = host(ops.histogram256_u8(x, grid=1)).view(np.uint64)
+    assert int(bins[0xA5]) == n and int(bins.sum()) == n
+    del x
+
+
+def test_hist_grid_floor_keeps_counters_exact(ops):
+    """A caller grid below the counter-overflow floor is raised to it
+    (grid >= n / 2^36); below 2^36 bytes the floor is one block, so any
+    grid >= 1 is exact."""
+    a = synthetic.generate("u8_const", (1 << 20) + 5, seed=2)
+    for g in (1, 2, 3, 7, 1000):
+        got = host(ops.histogram256_u8(dev(a), grid=g)).view(np.uint64)
+        assert np.array_equal(got, no.histogram256_u8(a)), g
 
 
 # ---- P: warp collectives -----------------------------------------------------
@@ -456,6 +428,40 @@ def test_launch_warp_program_partial_warps(ops):
     assert np.array_equal(mem.host_view(ob, "i32"), want)
 
 
+def test_device_memory_numpy_view_contract(ops):
+    """`view` is the reference's writable numpy view (runtime/memory.py:83-85):
+    writes through it reach the next launch, a view held across a launch
+    shows the kernel's output, and copy_in / copy_out / copy stay coherent
+    with it — the reference test idiom `mem.view(b, kind)[:] = init`."""
+    from paper_2112_10034_b200 import DeviceMemory, LaunchConfig, launch, PROGRAMS
+    mem = DeviceMemory()
+    n = 5000
+    a = synthetic.generate("i32_full", n, seed=4)
+    ab, sb = mem.alloc(4 * n), mem.alloc(4 * n)
+    va = mem.view(ab, "i32")
+    assert isinstance(va, np.ndarray) and va.flags.writeable and not va.any()
+    va[:] = a                                # host write through the view
+    vs = mem.view(sb, "i32")                 # held across the launch
+    launch(PROGRAMS["scan_inclusive_i32"], LaunchConfig(), mem, [ab, sb, n])
+    assert np.array_equal(vs, no.scan_inclusive_i32(a))
+    va[0] += 1                               # write again, after the launch
+    launch(PROGRAMS["scan_inclusive_i32"], LaunchConfig(), mem, [ab, sb, n])
+    b = a.copy()
+    b[0] += 1
+    assert np.array_equal(vs, no.scan_inclusive_i32(b))
+    mem.copy_in(ab, np.zeros(2, dtype=np.int32), offset=8)   # copy_in shows in the view
+    assert va[2] == 0 and va[3] == 0 and va[4] == b[4]
+    assert mem.copy_out(ab, 4, offset=0) == np.int32(b[0]).tobytes()
+    mem.copy(sb, ab, 16)
+    assert np.array_equal(vs[:4], va[:4])
+    assert np.array_equal(mem.host_view(sb, "i32")[:4], va[:4])
+    # large copies stream through the pinned chunks, both directions
+    big = synthetic.generate("u8_uniform", (70 << 20) + 3, seed=5)
+    bb = mem.alloc(big.size)
+    mem.copy_in(bb, big)
+    assert mem.copy_out(bb) == big.tobytes()
+
+
 def test_device_memory_roundtrip(ops):
     from paper_2112_10034_b200 import DeviceMemory, LaunchError
     mem = DeviceMemory()
@@ -482,6 +488,33 @@ def test_host_entry_points(ops):
     assert ops.reduce_sum_i32_host(a) == no.reduce_sum_i32(a)
     u = synthetic.generate("u8_uniform", 3 * (128 << 20) + 11, seed=8)
     assert np.array_equal(ops.histogram256_u8_host(u), no.histogram256_u8(u))
+
+
+@pytest.mark.parametrize("n", [0, 1, 5, 8191, (1 << 20) + 3, 3 * 22369536 + 7])
+def test_host_scan_and_compaction(ops, n):
+    """wf_scan_inclusive_i32_host / wf_compact_gt0_i32_host: host buffer in,
+    host buffer out, through the three-slot H2D / kernel / D2H ring; the
+    largest size spans several chunks (carry chain, output offsets)."""
+    a = synthetic.generate("i32_full", n, seed=n + 21)
+    pinned = torch.from_numpy(a).pin_memory()
+    out = torch.empty(n, dtype=torch.int32).pin_memory()
+    got = ops.scan_inclusive_i32_host(pinned, out)
+    assert np.array_equal(got.numpy(), no.scan_inclusive_i32(a))
+    assert np.array_equal(ops.scan_inclusive_i32_host(a, carry=-5), no.scan_inclusive_i32(a, carry=-5))
+    want = no.compact_gt0_i32(a)
+    res, m = ops.compact_gt0_i32_host(pinned, out)
+    assert m == len(want) and np.array_equal(res.numpy()[:m], want)
+    res, m = ops.compact_gt0_i32_host(a)  # pageable in / out
+    assert m == len(want) and np.array_equal(res[:m], want)
+
+
+@pytest.mark.parametrize("permille", [0, 10, 1000])
+def test_host_compaction_selectivity(ops, permille):
+    n = 2 * 11184768 + 333  # three chunks of the compaction ring
+    a = synthetic.generate("i32_select", n, seed=3, param=permille)
+    res, m = ops.compact_gt0_i32_host(a)
+    want = no.compact_gt0_i32(a)
+    assert m == len(want) and np.array_equal(res[:m], want)
 
 
 def test_host_entry_points_from_concurrent_threads(ops):
@@ -556,12 +589,10 @@ def test_compact_max_size(ops):
     assert pos == m
 
 
-@pytest.mark.parametrize("tmem", ["1", "0"])
-def test_c4_c5_reference_pins_on_gpu(ops, golden, monkeypatch, tmem):
+def test_c4_c5_reference_pins_on_gpu(ops, golden):
     """K4 / K5 reproduce the reference-produced vectors of
     tests/golden/c4c5_pin.npz (the reference's expressible serial compaction
-    and per-bin counting kernels), through both scan/compaction kernels."""
-    monkeypatch.setenv("WF_SCAN_TMEM", tmem)
+    and per-bin counting kernels)."""
     g = np.load(golden / "c4c5_pin.npz")
     for tag in [k[:-3] for k in g.files if k.endswith("_in")]:
         a = g[f"{tag}_in"]
@@ -613,3 +644,28 @@ def test_ops_follow_the_current_torch_stream(ops):
         out = ops.reduce_sum_i32(x)
     side.synchronize()
     assert int(out.item()) == int(x.long().sum())
+
+
+@pytest.mark.gpu
+def test_two_devices_in_one_process(ops):
+    """Every op on a tensor of a non-current GPU: the op switches to the
+    tensor's device, and each kernel's dynamic-smem opt-in is set per device
+    (scan / compaction use 192 KiB), so a second GPU in the same process
+    gives the same results as the first."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs in one process")
+    torch.cuda.set_device(0)
+    n = (1 << 22) + 5
+    a = synthetic.generate("i32_full", n, seed=11)
+    u = synthetic.generate("u8_geom", n, seed=11, param=0)
+    for d in (1, 0, 1):
+        x = torch.from_numpy(a).to(f"cuda:{d}")
+        assert torch.cuda.current_device() == 0
+        assert np.array_equal(host(ops.scan_inclusive_i32(x)), no.scan_inclusive_i32(a))
+        out, cnt = ops.compact_gt0_i32(x)
+        want = no.compact_gt0_i32(a)
+        assert int(host(cnt)[0]) == len(want) and np.array_equal(host(out)[:len(want)], want)
+        assert host(ops.reduce_sum_i32(x))[0] == no.reduce_sum_i32(a)
+        bins = host(ops.histogram256_u8(torch.from_numpy(u).to(f"cuda:{d}"))).view(np.uint64)
+        assert np.array_equal(bins, no.histogram256_u8(u))
+        assert out.device.index == d and cnt.device.index == d

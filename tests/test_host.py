@@ -62,7 +62,7 @@ def test_error_hierarchy_matches_reference():
 # ---- bind_args (reference runtime/launch.py:28-46) -------------------------
 
 class _FakeMem:
-    def view(self, buffer_id, kind):
+    def bind_view(self, buffer_id, kind):
         return np.zeros(4, dtype=np.int32)
 
 

@@ -1,5 +1,9 @@
 """Build experimental variants of the library into build/variants/ (travels to
-the GPU box; gitignored).  Usage: python tools/build_variants.py name="-DA=1 -DB=2" ..."""
+the GPU box; gitignored).  Usage: python tools/build_variants.py name="-DA=1 -DB=2" ...
+
+Variant builds also compile tools/variants/*.cu (the round-1 scan/compaction
+kernels that are not in the product library); select them with
+-DWF_SCAN_IMPL=1 (smem-stage persistent), 2 (register tile) or 3 (two-pass)."""
 import subprocess
 import sys
 from concurrent.futures import ThreadPoolExecutor
@@ -17,8 +21,9 @@ for old in out_dir.glob("*.so"):
 
 def one(spec):
     name, flags = spec.split("=", 1)
-    cmd = [build.nvcc_path(), *build.NVCC_FLAGS, f"-I{build.INCLUDE}", *flags.split(),
-           "-o", str(out_dir / f"lib_{name}.so"), *map(str, build.sources())]
+    cmd = [build.nvcc_path(), *build.NVCC_FLAGS, f"-I{build.INCLUDE}", f"-I{build.CSRC}",
+           *flags.split(), "-o", str(out_dir / f"lib_{name}.so"), *map(str, build.sources()),
+           *map(str, sorted((ROOT / "tools" / "variants").glob("*.cu"))), *build.LINK_FLAGS]
     r = subprocess.run(cmd, capture_output=True, text=True)
     return name, r.returncode, r.stderr[-500:]
 
