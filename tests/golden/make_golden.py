@@ -327,7 +327,22 @@ def corpus_traces() -> dict:
     return out
 
 
+def diff_pipeline_expected() -> str:
+    """The reference's own `run --json` output for tests/data/diff_pipeline.json
+    (oracle engine): the committed expected dumps of the GPU `diff` command."""
+    from warpfold.runtime.hostdesc import run_description
+    data = HERE.parent / "data"
+    cfg = LaunchConfig(grid_size=1, block_size=32, warp_size=32, workers=1)
+    _, dumps = run_description(data / "diff_pipeline.json", cfg, engine="oracle")
+    _, dumps2 = run_description(data / "diff_pipeline.json", cfg, engine="mpmd")
+    assert dumps == dumps2  # both reference engines agree on this program
+    return "".join(json.dumps(d) + "\n" for d in dumps)
+
+
 def main() -> None:
+    if "--diff-only" in sys.argv:
+        (HERE.parent / "data" / "diff_pipeline.expected.jsonl").write_text(diff_pipeline_expected())
+        return
     if "--random-only" in sys.argv:
         (HERE / "random_kernels.json").write_text(json.dumps(random_kernels()))
         (HERE / "acceptance_fuzz.json").write_text(json.dumps(acceptance_fuzz()))
@@ -356,6 +371,7 @@ def main() -> None:
     (HERE / "C3_WARP_PREFIX.spk").write_text(C3_WARP_PREFIX)
     (HERE / "C4_COMPACT_SERIAL.spk").write_text(C4_COMPACT_SERIAL)
     (HERE / "C5_HIST_PER_BIN.spk").write_text(C5_HIST_PER_BIN)
+    (HERE.parent / "data" / "diff_pipeline.expected.jsonl").write_text(diff_pipeline_expected())
     print("golden vectors written to", HERE)
 
 

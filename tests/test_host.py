@@ -186,3 +186,43 @@ def test_product_never_imports_oracle():
     for py in pkg.rglob("*.py"):
         text = py.read_text()
         assert not re.search(r"^\s*(from|import)\s+oracle\b", text, re.M), py
+
+
+# ---- diff report logic (reference interp/diff.py:48-72) --------------------
+
+def test_compare_memory_and_dumps():
+    from paper_2112_10034_b200.diff import compare_dumps, compare_memory
+    a = np.arange(8, dtype=np.int32)
+    f = np.linspace(0, 1, 8).astype(np.float32)
+    ref = {1: a.tobytes(), 2: f.tobytes()}
+    assert compare_memory(ref, dict(ref), {1: "i32", 2: "f32"}).equal
+    b = a.copy()
+    b[3] = 99
+    rep = compare_memory(ref, {1: b.tobytes(), 2: f.tobytes()}, {1: "i32", 2: "f32"})
+    assert not rep.equal and rep.divergence == {"buffer": 1, "element": 3, "reference": 3,
+                                                "transformed": 99}
+    assert rep.detail == "buffer 1 diverges at element 3: reference=3 transformed=99"
+    g = f.copy()
+    g[2] += 1e-5
+    got = {1: a.tobytes(), 2: g.tobytes()}
+    assert not compare_memory(ref, got, {1: "i32", 2: "f32"}).equal
+    assert compare_memory(ref, got, {1: "i32", 2: "f32"}, fp_tol=1e-4).equal
+    rep = compare_memory(ref, {1: a.tobytes()[:-1], 2: f.tobytes()}, {})
+    assert rep.divergence["detail"] == "length mismatch"
+    e = [{"buffer": "x", "kind": "i32", "values": [1, 2, 3]}]
+    assert compare_dumps(e, [{"buffer": "x", "kind": "i32", "values": [1, 2, 3]}]).equal
+    rep = compare_dumps(e, [{"buffer": "x", "kind": "i32", "values": [1, 5, 3]}])
+    assert rep.divergence["element"] == 1
+    assert not compare_dumps(e, []).equal
+
+
+def test_refcheck_is_checker_only():
+    """The reference is reached only by the diff command's checker module;
+    no op / runtime / kernel module imports it."""
+    pkg = ROOT / "paper_2112_10034_b200"
+    uses = re.compile(r"^\s*(from\s+\.+\s+import\s+.*\brefcheck\b|from\s+\.refcheck\b|"
+                      r"import\s+.*refcheck)", re.M)
+    assert [p.name for p in pkg.rglob("*.py") if uses.search(p.read_text())] == ["__main__.py"]
+    imports = re.compile(r"^\s*(from\s+warpfold[\s.]|import\s+warpfold\b)", re.M)
+    assert [p.name for p in pkg.rglob("*.py")
+            if imports.search(p.read_text()) and p.name != "refcheck.py"] == []
