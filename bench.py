@@ -563,6 +563,147 @@ def run_ours(args, rank, world, local) -> dict | None:
     }
 
 
+E2E_STEPS = 3
+
+
+def e2e_host_leg(kind: str, x, checks: dict) -> dict:
+    """One per-kernel e2e leg: the op through its C-ABI host entry point
+    (``wf_*_host``: pinned host input -> chunked H2D overlapped with the
+    kernel -> D2H into a pinned host output), timed by the host clock around
+    the synchronous call, checked against the device-resident result.  The
+    link ceiling is the same bytes copied by plain concurrent pinned
+    H2D + D2H (two streams), so ``frac_of_link`` = that time / e2e time."""
+    import torch
+    from paper_2112_10034_b200 import ops
+    n = x.numel()
+    host = torch.empty(n, dtype=x.dtype, pin_memory=True)
+    host.copy_(x)
+    if kind == "scan":
+        want = ops.scan_inclusive_i32(x).cpu()
+        hout = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        call = lambda: ops.scan_inclusive_i32_host(host, hout, device=x.device)  # noqa: E731
+        d2h_bytes = 4 * n
+        ok = lambda r: torch.equal(hout, want)  # noqa: E731
+        path = "wf_scan_inclusive_i32_host"
+    elif kind == "compact":
+        wo, wc = ops.compact_gt0_i32(x)
+        m = int(wc.item())
+        want = wo[:m].cpu()
+        hout = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        call = lambda: ops.compact_gt0_i32_host(host, hout, device=x.device)  # noqa: E731
+        d2h_bytes = 4 * m + 8
+        ok = lambda r: r[1] == m and torch.equal(hout[:m], want)  # noqa: E731
+        path = "wf_compact_gt0_i32_host"
+    else:
+        want = ops.histogram256_u8(x).cpu()
+        hout = None
+        call = lambda: ops.histogram256_u8_host(host, device=x.device)  # noqa: E731
+        d2h_bytes = 256 * 8
+        ok = lambda r: torch.equal(torch.from_numpy(r.view("int64")), want)  # noqa: E731
+        path = "wf_histogram256_u8_host"
+    h2d_bytes = n * x.element_size()
+    r = call()  # warm (staging ring, copy streams)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(E2E_STEPS):
+        r = call()
+    e2e_s = (time.perf_counter() - t) / E2E_STEPS
+    checks[f"e2e/{kind}"] = bool(ok(r))
+    # link ceiling: concurrent plain pinned copies of the same byte counts
+    dev_in = torch.empty_like(x)
+    d2h_elems = max(1, d2h_bytes // 4)
+    src = torch.empty(d2h_elems, dtype=torch.int32, device=x.device)
+    dst = torch.empty(d2h_elems, dtype=torch.int32, pin_memory=True)
+    s1, s2 = torch.cuda.Stream(device=x.device), torch.cuda.Stream(device=x.device)
+    best = None
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        with torch.cuda.stream(s1):
+            dev_in.copy_(host, non_blocking=True)
+        with torch.cuda.stream(s2):
+            dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t
+        best = dt if best is None else min(best, dt)
+    del dev_in, src, dst, host, hout
+    return {"value": round(n / e2e_s / 1e9, 4), "unit": "Gelem/s", "path": path,
+            "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes,
+            "steps": E2E_STEPS, "ms_per_step": round(e2e_s * 1e3, 3),
+            "link_copy_ms": round(best * 1e3, 3),
+            "frac_of_link": round(best / e2e_s, 4),
+            "link": "concurrent pinned H2D + D2H of the same bytes (two streams), best of 3"}
+
+
+def reference_api_rows(dev, peak, steps: int, warm: int, checks: dict) -> dict:
+    """The reference's OWN formulations of C1/C2/C3 (SURVEY §8c kernel
+    texts, tests/golden/*.spk) through the drop-in
+    ``launch(hybrid_transform(kernel, cfg), cfg, memory, args)`` — the call a
+    reference user makes (runtime/launch.py:90).  The structural registry
+    (dsl/patterns.py) routes them to native kernels (csrc/wf_patterns.cu).
+    ``kernel_us``: CUDA events around back-to-back dispatches of the program
+    on the stream; ``launch_us``: host clock around the full join-semantics
+    ``launch`` (argument binding + kernel + synchronise)."""
+    import torch
+    import paper_2112_10034_b200 as wf
+    from paper_2112_10034_b200.dsl import hybrid_transform, parse_module
+    rows = {}
+    specs = (  # key, kernel text, kind, n, grid, block, generator, bytes per element
+        ("c1_wsum_i32", "C1_I32", "i32", N_C1, 4096, 256, "i32_full", 4),
+        ("c2_wsum_f32", "C1_F32", "f32", N_C2, 148 * 8, 256, "f32_unit", 4),
+        ("c3_warp_prefix_i32", "C3_WARP_PREFIX", "i32", N_C3, N_C3 // 256, 256, "i32_full", 8),
+    )
+    for key, spk, kind, n, grid, block, gen, bpe in specs:
+        kernel = parse_module((ROOT / "tests" / "golden" / f"{spk}.spk").read_text()).kernel()
+        cfg = wf.LaunchConfig(grid_size=grid, block_size=block, warp_size=32)
+        prog = hybrid_transform(kernel, cfg)
+        mem = wf.DeviceMemory(dev)
+        a = mem.alloc(4 * n)
+        out_n = n if prog.native is not None and prog.native.n is None else grid * block // 32
+        out = mem.alloc(4 * out_n)
+        wf.ops.fill_synthetic(gen, n, seed=1, out=mem.device_view(a, kind))
+        args = [a, out] if spk == "C3_WARP_PREFIX" else [a, out, n]
+        bound = wf.bind_args(prog.params, mem, args)
+        native = prog.native is not None and prog.native.applicable(cfg, bound)
+        symbol = prog.native.symbol if prog.native is not None else None
+        stream = torch.cuda.current_stream(dev)
+        flush = None
+        if key.startswith("c1"):  # 4 MiB: flush L2 as for the C1 headline row
+            fb = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+            flush = lambda: fb.fill_(1)  # noqa: E731
+        t = time_launches(lambda: prog.native.run(cfg, bound, stream.cuda_stream), steps, warm,
+                          flush=flush)
+        kern_us = statistics.mean(t) * 1e3
+        wf.launch(prog, cfg, mem, args)  # warm
+        t0 = time.perf_counter()
+        reps = max(3, min(steps, 20))
+        for _ in range(reps):
+            wf.launch(prog, cfg, mem, args)
+        launch_us = (time.perf_counter() - t0) / reps * 1e6
+        # check: native result == the generic compiled kernel of the same text
+        got = mem.device_view(out, kind)[:out_n].clone()
+        prog.native = None
+        wf.launch(prog, cfg, mem, args)
+        want = mem.device_view(out, kind)[:out_n]
+        checks[f"reference_api/{key}"] = bool(native and torch.equal(got.view(torch.int32),
+                                                                     want.view(torch.int32)))
+        gbs = bpe * n / (kern_us * 1e-6) / 1e9
+        rows[key] = {"kernel_text": f"tests/golden/{spk}.spk", "n": n, "grid": grid,
+                     "block": block, "native_symbol": symbol,
+                     "registry_hit": native,
+                     "kernel_us": round(kern_us, 2), "gelem_s": round(n / kern_us / 1e3, 2),
+                     "gbs": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4),
+                     "launch_us": round(launch_us, 1),
+                     "bytes_per_elem": bpe,
+                     "l2": "flushed before every launch" if flush else "inputs larger than L2"}
+        if spk != "C3_WARP_PREFIX":
+            rows[key]["output"] = (f"{grid * block // 32} per-warp partials (the reference's "
+                                   f"host fold of them is not timed)")
+        del mem, got, want
+        torch.cuda.empty_cache()
+    return rows
+
+
 def per_kernel(args, rank, world, local, dev, peak, checks: dict) -> dict:
     import torch
     from paper_2112_10034_b200 import distributed as wd, ops
@@ -660,6 +801,12 @@ def per_kernel(args, rank, world, local, dev, peak, checks: dict) -> dict:
             "gbs": round(bpe * (hi - lo) / (ms * 1e-3) / 1e9, 1),
             "gelem_s": round(N_C4 / (max_over_ranks(ms, world) * 1e-3) / 1e9, 3)}
     res["c4_compact_i32"]["selectivity_variants"] = variants
+    if world == 1 and not args.headline_only:
+        # end to end through the C-ABI host entry points (pinned host in and
+        # out, chunked H2D / kernel / D2H ring), beside the link's own ceiling
+        ops.fill_synthetic("i32_full", hi - lo, seed=0, base=lo, out=x)
+        res["c3_scan_i32"]["e2e"] = e2e_host_leg("scan", x, checks)
+        res["c4_compact_i32"]["e2e"] = e2e_host_leg("compact", x, checks)
     del x, y, out
     torch.cuda.empty_cache()
     log(f"rank {rank}: C5")
@@ -680,6 +827,9 @@ def per_kernel(args, rank, world, local, dev, peak, checks: dict) -> dict:
                          "gbs": round((hi - lo) / (ms * 1e-3) / 1e9, 1),
                          "gelem_s": round(N_C5 / (max_over_ranks(ms, world) * 1e-3) / 1e9, 3)}
     res["c5_hist_u8"]["data_variants"] = variants
+    if world == 1 and not args.headline_only:
+        ops.fill_synthetic("u8_uniform", hi - lo, seed=0, base=lo, out=u)
+        res["c5_hist_u8"]["e2e"] = e2e_host_leg("hist", u, checks)
     if exchange is not None:
         if pc is not None and pc.failed():  # a peer never arrived in some call: results invalid
             log(f"rank {rank}: a peer-memory exchange timed out during the C3-C5 runs")
@@ -696,6 +846,9 @@ def per_kernel(args, rank, world, local, dev, peak, checks: dict) -> dict:
                 res[k]["algorithmic_bytes"] = int(res[k]["n"] * res[k]["bytes_per_elem"])
     del u
     torch.cuda.empty_cache()
+    if world == 1:
+        log("rank 0: reference formulations via launch(hybrid_transform(...))")
+        res["via_reference_api"] = reference_api_rows(dev, peak, steps, warm, checks)
     return res
 
 

@@ -236,6 +236,27 @@ int wf_warp_collective(int kind, const int32_t *a, const int32_t *b,
                        int block, int width, uint32_t mask,
                        wf_stream_t stream);
 
+/* ---- the reference's own DSL formulations (registry: dsl/patterns.py) ---
+ * Reached from launch(hybrid_transform(kernel)) when the kernel is, up to
+ * renaming, one the reference itself runs for this path; each writes exactly
+ * what that DSL kernel writes.  Replaces runtime/launch.py:90 +
+ * interp/mpmd.py:237-255 for these kernels.
+ *
+ * wf_warp_partials_sum_{i32,f32}: tests/golden/C1_{I32,F32}.spk = the
+ *   SURVEY 8c per-warp-partials kernel.  out[b*(block/32) + w] = shfl_down
+ *   tree (16,8,4,2,1) of each lane's grid-stride sum (i = tid, tid+S, ...
+ *   while i < n, S = grid*block), fp32 in exactly that order.  Needs
+ *   block % 32 == 0 and grid*block + n <= 2^31-1 (no i32 index wrap).
+ * wf_warp_prefix32_i32: tests/golden/C3_WARP_PREFIX.spk (lane-reversed
+ *   shfl_down suffix tree).  out[32s+k] = a[32s] + ... + a[32s+k], wrapping,
+ *   for n = grid*block elements (n % 32 == 0). */
+int wf_warp_partials_sum_i32(const int32_t *a, int32_t n, int32_t *out,
+                             int grid, int block, wf_stream_t stream);
+int wf_warp_partials_sum_f32(const float *a, int32_t n, float *out,
+                             int grid, int block, wf_stream_t stream);
+int wf_warp_prefix32_i32(const int32_t *a, int32_t *out, uint64_t n,
+                         wf_stream_t stream);
+
 /* ---- synthetic inputs (identical to oracle/synthetic.py) --------------- */
 int wf_fill_synthetic(int gen, void *out, uint64_t n, uint64_t seed,
                       uint64_t index_base, uint32_t param, wf_stream_t stream);

@@ -75,6 +75,9 @@ SIGNATURES = {
     "wf_histogram256_u8": (C.c_int, [_vp, _u64, _vp, C.c_int, _vp, _sz, _vp]),
     "wf_warp_collective": (C.c_int, [C.c_int, _vp, _vp, _i32, _vp, _u64, C.c_int, C.c_int,
                                      _u32, _vp]),
+    "wf_warp_partials_sum_i32": (C.c_int, [_vp, _i32, _vp, C.c_int, C.c_int, _vp]),
+    "wf_warp_partials_sum_f32": (C.c_int, [_vp, _i32, _vp, C.c_int, C.c_int, _vp]),
+    "wf_warp_prefix32_i32": (C.c_int, [_vp, _vp, _u64, _vp]),
     "wf_fill_synthetic": (C.c_int, [C.c_int, _vp, _u64, _u64, _u64, _u32, _vp]),
     "wf_reduce_sum_f32_host": (C.c_int, [_vp, _u64, _vp, _vp, _sz, _vp, _sz, _vp]),
     "wf_reduce_sum_i32_host": (C.c_int, [_vp, _u64, _vp, _vp, _sz, _vp, _sz, _vp]),

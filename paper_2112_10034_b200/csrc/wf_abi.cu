@@ -92,10 +92,10 @@ struct CopyStreams {
   cudaStream_t copy[2] = {nullptr, nullptr};
   cudaEvent_t copied[2] = {nullptr, nullptr};
   cudaEvent_t consumed[2] = {nullptr, nullptr};
-  // three-slot ring of the scan / compaction host paths (H2D in, kernel,
-  // D2H out, all overlapped): landed / computed / drained per slot
+  // slot ring of the scan / compaction host paths (H2D in, kernel, D2H out,
+  // all overlapped): landed / computed / drained per slot (kHostRing slots)
   cudaStream_t h2d = nullptr, d2h = nullptr;
-  cudaEvent_t landed[3] = {}, computed[3] = {}, drained[3] = {};
+  cudaEvent_t landed[8] = {}, computed[8] = {}, drained[8] = {};
   uint64_t *pinned = nullptr;  // per-slot compaction counts read by the host
 };
 static std::mutex g_streams_mu;
@@ -123,7 +123,7 @@ static int get_copy_streams(CopyStreams *&cs) {
     }
     cudaError_t e = cudaStreamCreateWithFlags(&c.h2d, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.d2h, cudaStreamNonBlocking);
-    for (int k = 0; k < 3 && e == cudaSuccess; ++k) {
+    for (int k = 0; k < 8 && e == cudaSuccess; ++k) {
       e = cudaEventCreateWithFlags(&c.landed[k], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.computed[k], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.drained[k], cudaEventDisableTiming);
@@ -464,6 +464,42 @@ int wf_warp_collective(int kind, const int32_t *a, const int32_t *b, int32_t ope
                      "warp_collective");
 }
 
+// ---- the reference's DSL formulations (dsl/patterns.py registry) ---------
+static int check_partials(const void *a, int32_t n, const void *out, int grid, int block) {
+  if (block < 32 || block > 1024 || block % 32)
+    return fail(WF_ERR_CONFIG, "block size must be a multiple of 32 in [32, 1024], got %d", block);
+  if (grid < 0) return fail(WF_ERR_CONFIG, "grid size must be >= 0, got %d", grid);
+  if (int64_t(grid) * block + (n > 0 ? n : 0) > 0x7fffffffll)
+    return fail(WF_ERR_ARG, "grid-stride index would overflow i32 (grid %d x block %d, n %d)",
+                grid, block, n);
+  if (grid && (out == nullptr || (n > 0 && a == nullptr)))
+    return fail(WF_ERR_ARG, "NULL buffer pointer");
+  return WF_OK;
+}
+
+int wf_warp_partials_sum_i32(const int32_t *a, int32_t n, int32_t *out, int grid, int block,
+                             wf_stream_t stream) {
+  if (int rc = check_partials(a, n, out, grid, block)) return rc;
+  return cuda_status(launch_warp_partials(false, a, n, out, grid, block,
+                                          static_cast<cudaStream_t>(stream)),
+                     "warp_partials_sum_i32");
+}
+
+int wf_warp_partials_sum_f32(const float *a, int32_t n, float *out, int grid, int block,
+                             wf_stream_t stream) {
+  if (int rc = check_partials(a, n, out, grid, block)) return rc;
+  return cuda_status(launch_warp_partials(true, a, n, out, grid, block,
+                                          static_cast<cudaStream_t>(stream)),
+                     "warp_partials_sum_f32");
+}
+
+int wf_warp_prefix32_i32(const int32_t *a, int32_t *out, uint64_t n, wf_stream_t stream) {
+  if (n % 32) return fail(WF_ERR_CONFIG, "n (%llu) must be a multiple of 32", (unsigned long long)n);
+  if (n && (a == nullptr || out == nullptr)) return fail(WF_ERR_ARG, "NULL buffer pointer");
+  return cuda_status(launch_warp_prefix32(a, out, n, static_cast<cudaStream_t>(stream)),
+                     "warp_prefix32_i32");
+}
+
 int wf_fill_synthetic(int gen, void *out, uint64_t n, uint64_t seed, uint64_t index_base,
                       uint32_t param, wf_stream_t stream) {
   if (gen < WF_GEN_I32_FULL || gen > WF_GEN_I32_SELECT)
@@ -568,7 +604,12 @@ int wf_histogram256_u8_host(const uint8_t *host_in, uint64_t n, uint64_t *host_b
 // is full duplex, so the D2H of the result hides under the H2D of the input.
 namespace wf {
 namespace {
-constexpr int kRing = 3;
+// 8 slots of at most 16 MiB: the pipeline fill (first H2D) and drain (last
+// D2H) that no copy in the other direction hides are one small chunk each
+// (3 slots of 85 MiB measured 0.905 of the concurrent-copy ceiling for the
+// 2^28 scan: 8 % of the time was fill + drain)
+constexpr int kRing = 8;
+constexpr size_t kRingChunkMax = size_t(16) << 20;
 
 int host_ring_checks(const void *host_in, const void *host_out, uint64_t n, void *staging,
                      size_t staging_bytes, size_t min_bytes) {
@@ -590,8 +631,9 @@ int wf_scan_inclusive_i32_host(const int32_t *host_in, int32_t *host_out, uint64
                                void *ws, size_t ws_bytes, wf_stream_t stream) {
   int rc = host_ring_checks(host_in, host_out, n, staging, staging_bytes, size_t(3) << 20);
   if (rc) return rc;
-  // [0, 256): carry-in slot; then three in-place chunk buffers
-  const size_t buf = ((staging_bytes - 256) / kRing) & ~size_t(255);
+  // [0, 256): carry-in slot; then kRing in-place chunk buffers
+  size_t buf = ((staging_bytes - 256) / kRing) & ~size_t(255);
+  if (buf > kRingChunkMax) buf = kRingChunkMax;
   const uint64_t per_chunk = buf / 4;
   rc = check_ws(WF_OP_SCAN_INCLUSIVE_I32, per_chunk, ws, ws_bytes);
   if (rc) return rc;
@@ -611,9 +653,10 @@ int wf_scan_inclusive_i32_host(const int32_t *host_in, int32_t *host_out, uint64
     const uint64_t first = c * per_chunk;
     const uint64_t cnt = (n - first) < per_chunk ? (n - first) : per_chunk;
     int32_t *dbuf = reinterpret_cast<int32_t *>(base + 256 + size_t(k) * buf);
-    if (c >= kRing) {  // slot k: chunk c-3 drained, and chunk c-2 read its carry from it
+    if (c >= kRing) {  // slot k: chunk c-kRing drained, and chunk c-kRing+1 read its carry from it
       e = cudaStreamWaitEvent(cs->h2d, cs->drained[k], 0);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(cs->h2d, cs->computed[(c - 2) % kRing], 0);
+      if (e == cudaSuccess)
+        e = cudaStreamWaitEvent(cs->h2d, cs->computed[(c - kRing + 1) % kRing], 0);
     }
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(dbuf, host_in + first, cnt * 4, cudaMemcpyHostToDevice, cs->h2d);
@@ -638,8 +681,9 @@ int wf_compact_gt0_i32_host(const int32_t *host_in, uint64_t n, int32_t *host_ou
   if (host_count == nullptr) return fail(WF_ERR_ARG, "host count pointer is NULL");
   int rc = host_ring_checks(host_in, host_out, n, staging, staging_bytes, size_t(6) << 20);
   if (rc) return rc;
-  // [0, 256): per-slot device counts; then three input and three output buffers
-  const size_t buf = ((staging_bytes - 256) / (2 * kRing)) & ~size_t(255);
+  // [0, 256): per-slot device counts; then kRing input and kRing output buffers
+  size_t buf = ((staging_bytes - 256) / (2 * kRing)) & ~size_t(255);
+  if (buf > kRingChunkMax) buf = kRingChunkMax;
   const uint64_t per_chunk = buf / 4;
   rc = check_ws(WF_OP_COMPACT_GT0_I32, per_chunk, ws, ws_bytes);
   if (rc) return rc;

@@ -160,7 +160,8 @@ __device__ __forceinline__ void take_ticket(TileHeader *hdr, uint32_t ntiles,
 // the nearest inclusive prefix is valid — so polling traffic stays small.
 template <int K>
 __device__ __forceinline__ uint32_t lookback_exclusive_wide(const uint64_t *desc,
-                                                            uint32_t tile, uint32_t epoch) {
+                                                            uint32_t tile, uint32_t epoch,
+                                                            uint32_t *polls = nullptr) {
   const uint32_t lane = lane_id();
   uint32_t excl = 0;
   int64_t hi = int64_t(tile) - 1;
@@ -170,6 +171,7 @@ __device__ __forceinline__ uint32_t lookback_exclusive_wide(const uint64_t *desc
     for (int k = 0; k < K; ++k) st[k] = kStInvalid;
     uint32_t backoff = 16;
     while (true) {
+      if (polls) ++*polls;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         if (st[k] == kStInvalid) {

@@ -137,6 +137,10 @@ int auto_hist_grid(uint64_t n);
 int min_hist_grid(uint64_t n);  // counter-overflow floor for a caller's grid
 
 // warp collectives (wf_warp.cu)
+// wf_patterns.cu: the reference's own DSL formulations, natively (dsl/patterns.py)
+cudaError_t launch_warp_partials(bool f32, const void *a, int64_t n, void *out, int grid,
+                                 int block, cudaStream_t s);
+cudaError_t launch_warp_prefix32(const int32_t *a, int32_t *out, uint64_t n, cudaStream_t s);
 cudaError_t launch_warp_collective(int kind, const int32_t *a,
                                    const int32_t *b, int32_t operand,
                                    int32_t *out, uint64_t n_threads, int block,

@@ -1,61 +1,78 @@
 // wf_scan_tmem.cu — K3 scan / K4 compaction: warp-specialised single-pass
-// decoupled look-back with tiles PARKED IN TENSOR MEMORY while their prefix
-// resolves.
+// scan with tiles PARKED IN TENSOR MEMORY while their prefix resolves.
 //
-// Why: the smem-stage kernel of wf_scan.cu holds each 32 KiB stage from its
-// TMA load until the tile's prefix is known (~3 us after the latest
-// predecessor landed), so only a fraction of the stages is ever loading and
-// reads in flight cap at ~3 TB/s (profiles/r01_scan_compact_experiments.md).
-// A first TMEM version that parked one tile per CTA but aggregated the next
-// tile only after finishing the previous one measured slower (490 / 474 us):
-// every aggregate then waited behind a prefix (convoy).  Here every role has
-// its own warps and its own mbarrier pipeline, so a landed tile is reduced
-// and published at once whatever the state of older tiles:
+// Why: a kernel that holds each 32 KiB smem stage from its TMA load until the
+// tile's prefix is known keeps only a fraction of the stages loading, so reads
+// cap at ~3 TB/s (profiles/r01_scan_compact_experiments.md).  Here every role
+// has its own warps and its own mbarrier pipeline, so a landed tile is
+// reduced and published at once whatever the state of older tiles:
 //
-//   producer warp    claims tile ids (ticket, drawn one stage ahead) and
-//                    TMA-loads them into a ring of S smem stages
-//                    (cp.async.bulk + mbarrier complete_tx); ragged last tile
-//                    by guarded copy
-//   aggregator warps 0-3: LDS the landed stage once (the x[j][k] layout of the
-//                    SDK shfl_scan), tcgen05.st it into one of P TMEM slots
+//   producer warp    claims tile ids (one ticket per tile, the next ticket
+//                    examined only when needed) and TMA-loads them into a
+//                    ring of S smem stages (cp.async.bulk + mbarrier
+//                    complete_tx); ragged last tile by guarded copy
+//   aggregator warps two groups of 4 taking stage items alternately: LDS the
+//                    landed stage once (the x[j][k] layout of the SDK
+//                    shfl_scan), tcgen05.st it into one of P TMEM slots
 //                    (64 columns = 32 KiB), release the stage, REDUX the tile
-//                    value and publish its look-back descriptor at once
-//   look-back warps  run the decoupled look-back over the tile descriptors
-//                    (round-robin over tiles, so several resolve at once) and
-//                    post each prefix into a 2P-entry ring
+//                    value and publish its aggregate at once
+//   sweeper warp     (CTA 0 only) reads the published aggregates in tile
+//                    order, 256 per L2 round trip, and publishes every tile's
+//                    exclusive prefix: no per-tile look-back
+//                    (WF_TM_SWEEP=0 builds a decoupled look-back instead)
+//   waiter warp      watches the prefixes of the CTA's parked tiles (one lane
+//                    per item, all polled in the same round trip) and posts
+//                    them to the finishers
 //   finisher warps   4-11, one per tile eighth: tcgen05.ld the tile back, free
 //                    the slot, scan (SHFL.UP, 8 chunk chains interleaved) /
-//                    ballot-compact (VOTE + POPC) it locally, then wait for
-//                    the prefix and store (STG.128 for the scan)
+//                    compact (packed per-chunk counts, one pair of warp
+//                    scans) it locally, then wait for the prefix and store
+//                    (STG.128 for the scan)
 //
 // Hand-offs are mbarriers (full / empty per stage; parked / freed per slot;
 // pref per ring entry), each with a phase per use, so no role ever waits on a
 // CTA-wide barrier.
 //
-// Per SM (default: one CTA, S=6 stages, P=8 slots = all 512 TMEM columns,
-// 6 look-back warps): 6 stages loading + 8 parked tiles = 448 KiB of tiles on
-// chip, against 224 KiB for the smem-only kernel.
+// Per SM (default: one CTA, S=4 stages, P=8 slots = all 512 TMEM columns):
+// 4 stages loading + 8 parked tiles = 384 KiB of tiles on chip.  Per-role
+// cycle accounting (-DWF_TM_PROF=1, tools/prof_tmem.py) and per-tile traces
+// (-DWF_TM_TRACE=1, tools/trace_tmem.py, tools/trace_sweep.py) drove the
+// current split: profiles/r02_scan_compact.md.
 //
-// Deadlock freedom: a CTA's tiles are claimed, aggregated, looked back and
+// Deadlock freedom: a CTA's tiles are claimed, aggregated, resolved and
 // finished in claim order; the smallest unfinished tile in the grid has all
-// predecessors finished, its CTA's older slots are free, so it progresses.
+// predecessors finished (their aggregates are published, so the sweeper
+// reaches it), its CTA's older slots are free, so it progresses.
 //
-// Reference analog: as wf_scan.cu (corpus.py:347-364 warp-level scan; the
-// block/grid carries the reference needs several launches for,
-// runtime/hostdesc.py:109-129; compaction not expressible, dsl/lexer.py:18-25).
+// Reference analog: corpus.py:347-364 (warp-level scan); the block/grid
+// carries the reference needs several launches for, runtime/hostdesc.py:
+// 109-129; compaction is not expressible (dsl/lexer.py:18-25).
 #include "wf_device.cuh"
 #include "wf_internal.h"
 #include "wf_peer.cuh"
 
 
 #ifndef WF_TM_STAGES
-#define WF_TM_STAGES 6  // smem stages per CTA (32 KiB each)
+#define WF_TM_STAGES 4  // smem stages per CTA (32 KiB each; 4 vs 6: 248 vs 250 us compaction, tools/tm_sweep.sh)
 #endif
 #ifndef WF_TM_SLOTS
 #define WF_TM_SLOTS 8  // TMEM slots per CTA (64 columns each; power of two)
 #endif
+#ifndef WF_TM_SWEEP
+#define WF_TM_SWEEP 1  // 1: one grid-wide prefix sweeper + one waiter warp per CTA; 0: per-tile look-back
+#endif
 #ifndef WF_TM_NLB
+#if WF_TM_SWEEP
+#define WF_TM_NLB 1  // the waiter warp
+#else
 #define WF_TM_NLB 3  // look-back warps per CTA (with 2 aggregator groups; tools/nag_sweep3.sh)
+#endif
+#endif
+#ifndef WF_SWEEP_K
+#define WF_SWEEP_K 8  // the sweeper reads 32 * K aggregates per round trip (4 / 8 / 16 / 32: 274 / 248 / 271 / 363 us)
+#endif
+#ifndef WF_TM_BATCH
+#define WF_TM_BATCH 1  // consecutive tiles claimed per ticket draw (2 / 4 measured slower)
 #endif
 #ifndef WF_TM_NFG
 #define WF_TM_NFG 1  // finisher groups (8 warps each), taking tiles round-robin
@@ -79,18 +96,43 @@
 #endif
 
 namespace wf {
+#ifndef WF_TM_PROF
+#define WF_TM_PROF 0
+#endif
+#if WF_TM_PROF
+// per CTA, 16 counters: [0..4] finisher (warp W_FIN lane 0) cycles waiting parked, TMEM read +
+// free, local work, waiting prefix, stores; [5] finisher items; [6..8] aggregator leader
+// (group 0) waiting full, waiting freed, work; [9] its items; [10,11] producer waiting
+// empty, issuing; [12] producer items
+__device__ unsigned long long *g_tm_prof = nullptr;
+#define PROF_T(v) unsigned long long v = clock64()
+#define PROF_ADD(k, a, b) (acc[k] += (b) - (a))
+#else
+#define PROF_T(v)
+#define PROF_ADD(k, a, b)
+#endif
 #if WF_TM_TRACE
 // per tile: [0] claimed+TMA issued  [1] aggregator start (landed, slot free)
 // [2] parked  [3] prefix known  [4] finisher done (warp W_FIN)
+// [5] look-back warp picked the item up  [6] look-back polls  [7] SM id
+constexpr int kTmTraceWords = 8;
 __device__ unsigned long long *g_tm_trace = nullptr;
 __device__ __forceinline__ void tm_stamp(uint32_t tile, int k) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  if (g_tm_trace) g_tm_trace[uint64_t(tile) * 5 + k] = t;
+  if (g_tm_trace) g_tm_trace[uint64_t(tile) * kTmTraceWords + k] = t;
+}
+__device__ __forceinline__ void tm_put(uint32_t tile, int k, unsigned long long v) {
+  if (g_tm_trace) g_tm_trace[uint64_t(tile) * kTmTraceWords + k] = v;
 }
 #define TM_STAMP(tile, k) tm_stamp(tile, k)
+#define TM_PUT(tile, k, v) tm_put(tile, k, v)
+// sweeper iterations: [2 j] = globaltimer at the start of iteration j, [2 j + 1] = f | ready << 32
+__device__ unsigned long long *g_sweep_trace = nullptr;
+__device__ uint32_t g_sweep_cap = 0;
 #else
 #define TM_STAMP(tile, k)
+#define TM_PUT(tile, k, v)
 #endif
 namespace {
 
@@ -102,6 +144,7 @@ constexpr int NFG = WF_TM_NFG;
 constexpr int NFIN = 8 * NFG;             // per group: one finisher warp per tile eighth
 constexpr int W_LB = W_FIN + NFIN;        // look-back warps W_LB .. W_LB+NLB-1
 constexpr int W_PROD = W_LB + NLB;        // producer warp
+constexpr int W_SWEEP = W_PROD + 1;       // prefix sweeper (CTA 0 only; WF_TM_SWEEP)
 #ifndef WF_TM_NAG
 #define WF_TM_NAG 2  // aggregator groups (4 warps each), taking stage items round-robin
 #endif
@@ -118,12 +161,15 @@ constexpr uint32_t TM_TILE = 4u * QVEC * 128;  // 8192 x TMUL items
 constexpr uint32_t SLOT_COLS = 64u * TMUL;     // TMEM columns per parked tile
 constexpr uint32_t TM_COLS = uint32_t(P) * SLOT_COLS;
 constexpr uint32_t kNoTileTm = 0xffffffffu;
+constexpr uint32_t kBatch = WF_TM_BATCH;
 constexpr uint32_t kNoItem = 0xffffffffu;  // item_seq before the first publish
 static_assert((P & (P - 1)) == 0 && TM_COLS <= 512, "TMEM slots: power of two, <= 512 cols");
 static_assert(NLB >= 1 && NLB <= P, "look-back warps must not outnumber TMEM slots");
-static_assert(NFG <= NLB, "every finisher group must see one of the NLB stop items");
-static_assert(!(NAG == 2 && NFG > 1), "two aggregator groups with two finisher groups hang "
-              "(tools/sweep_final.sh): not a supported combination");
+static_assert(!WF_TM_SWEEP || (NLB == 1 && NAG == 2 && W_SWEEP < W_AGG2),
+              "the sweeper warp sits in the gap before the second aggregator group");
+// stop items: one per look-back warp and one per finisher group
+constexpr int NSTOP = NLB > NFG ? NLB : NFG;
+static_assert(NSTOP <= P, "stop items must fit the TMEM slots");
 // With two aggregator groups taking stage items round-robin, an odd stage
 // count would hand one stage to both groups alternately: a group could then
 // wait on that stage's mbarrier for a phase two ahead of the current one,
@@ -211,10 +257,16 @@ struct TmShared {
   uint32_t item_tile[2 * P];
   uint32_t item_agg[2 * P];
   uint32_t item_seq[2 * P];
+  uint32_t item_posted[2 * P];  // waiter: item whose prefix was posted at this ring entry
   uint32_t slot_wtot[P][4][2];  // per tile quarter and half
   uint32_t tmem_base;
   uint32_t epoch;
 };
+
+// sweeper layout: aggregates desc[0, ntiles), exclusive prefixes from
+// desc[pref_offset) on, both one u64 per tile (the workspace holds 128 B per
+// 4096 elements, far more)
+__device__ __forceinline__ uint32_t pref_offset(uint32_t ntiles) { return (ntiles + 15u) & ~15u; }
 
 // PX (compaction only): the finisher warp of the last tile also runs the
 // offset exchange of wf_peer.cuh (peer_exscan_warp): count = {this rank's
@@ -252,7 +304,10 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
   }
   // item ring: no entry holds a valid item index before its first publish
   // (shared memory keeps whatever an earlier CTA left there)
-  if (threadIdx.x < 2 * P) sh.item_seq[threadIdx.x] = kNoItem;
+  if (threadIdx.x < 2 * P) {
+    sh.item_seq[threadIdx.x] = kNoItem;
+    sh.item_posted[threadIdx.x] = kNoItem;
+  }
   if (warp == W_PROD && lane == 0)
     sh.epoch = ld_volatile_u32(&hdr->epoch) & kEpochMask;  // before this CTA's first (release) draw
   tc_fence_before();
@@ -262,27 +317,49 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
 
   if (warp == W_PROD) {
     // ------------------------------ producer ------------------------------
-    // Tickets are drawn one stage ahead: the atomic's round trip overlaps the
-    // wait for the next free stage instead of serialising with it.
-    auto draw = [&](bool first) -> uint32_t {
-      uint32_t t = first ? atom_add_acq_rel_gpu(&hdr->ticket, 1u) : atom_add_relaxed_gpu(&hdr->ticket, 1u);
-      if (t >= ntiles) {
-        if (t == ntiles + gridDim.x - 1) {  // last of all draws: reset for the next launch
-          fence_acq_rel_gpu();
-          atomicExch(&hdr->ticket, 0u);
-          atomicExch(&hdr->epoch, (epoch + 1) & kEpochMask);
-        }
-        t = kNoTileTm;
+    // Tiles are claimed in batches of B consecutive tiles per ticket (one
+    // atomicAdd(ticket, B)), and the next batch's ticket is drawn when the
+    // current batch starts and examined only when it is needed: the atomic's
+    // L2 round trip (~1 us under full HBM load) never sits between a stage
+    // becoming free and its TMA load.  (One tile per draw, examined at once,
+    // capped the CTA at one tile per round trip: ~140 tiles/us grid-wide.)
+    const uint32_t nbatches = (ntiles + kBatch - 1) / kBatch;
+    auto failing = [&](uint32_t base) {  // each CTA examines exactly one failing draw
+      if (base == (nbatches + gridDim.x - 1) * kBatch) {  // last of all draws: reset for the next launch
+        fence_acq_rel_gpu();
+        atomicExch(&hdr->ticket, 0u);
+        atomicExch(&hdr->epoch, (epoch + 1) & kEpochMask);
       }
-      return t;
     };
-    uint32_t ahead = lane == 0 ? draw(true) : 0u;
+    uint32_t cur = lane == 0 ? atom_add_acq_rel_gpu(&hdr->ticket, kBatch) : 0u;  // after the epoch read
+    uint32_t nxt = 0, j = 0;
+#if WF_TM_PROF
+    unsigned long long acc[3] = {0, 0, 0};
+#endif
     for (uint32_t i = 0;; ++i) {
       const int s = int(i % S);
       const uint32_t k = i / S;
+      PROF_T(p0);
       if (k > 0) mbar_wait(&sh.empty[s], (k - 1) & 1u);
-      uint32_t t = ahead;
-      if (lane == 0 && t != kNoTileTm) ahead = draw(false);
+      PROF_T(p1);
+      uint32_t t = kNoTileTm;
+      if (lane == 0) {
+        if (j == 0) {
+          if (cur >= ntiles) {
+            failing(cur);
+          } else {
+            nxt = atom_add_relaxed_gpu(&hdr->ticket, kBatch);  // examined at the end of this batch
+            t = cur;
+          }
+        } else {
+          t = cur + j < ntiles ? cur + j : kNoTileTm;
+          if (t == kNoTileTm) failing(nxt);  // ragged last batch: the draw behind it failed
+        }
+        if (t != kNoTileTm && ++j == kBatch) {
+          cur = nxt;
+          j = 0;
+        }
+      }
       t = __shfl_sync(kFull, t, 0);
       int32_t *stage = stages + s * TM_TILE;
       const uint64_t tbase = uint64_t(t) * TM_TILE;
@@ -303,6 +380,14 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
           mbar_arrive1(&sh.full[s]);
         }
       }
+#if WF_TM_PROF
+      PROF_T(p2);
+      PROF_ADD(0, p0, p1);
+      PROF_ADD(1, p1, p2);
+      acc[2] += 1;
+      if (t == kNoTileTm && lane == 0 && g_tm_prof)
+        for (int q = 0; q < 3; ++q) g_tm_prof[blockIdx.x * 16 + 10 + q] = acc[q];
+#endif
       if (t == kNoTileTm) {
         if (NAG == 2) {  // the other aggregator group's stop item
           const int s2 = int((i + 1) % S);
@@ -322,20 +407,26 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
     const uint32_t grp = (NAG == 2 && warp >= W_AGG2) ? 1u : 0u;
     const bool leader = warp == (grp ? uint32_t(W_AGG2) : 0u) && lane == 0;
     const uint32_t tcol = sh.tmem_base + ((32u * q) << 16);
+#if WF_TM_PROF
+    unsigned long long acc[4] = {0, 0, 0, 0};
+#endif
     for (uint32_t i = grp;; i += NAG) {
       const int s = int(i % S), p = int(i % P);
       const uint32_t kp = i / P;
+      PROF_T(g0);
       mbar_wait(&sh.full[s], (i / S) & 1u);
+      PROF_T(g1);
       const uint32_t t = sh.stage_tile[s];
       if (t == kExitOnly) break;
       if (kp > 0) mbar_wait(&sh.freed[p], (kp - 1) & 1u);
+      PROF_T(g2);
       tc_fence_after();
       if (leader && t != kNoTileTm) TM_STAMP(t, 1);
       if (t == kNoTileTm) {
         // one stop item per look-back warp (items i .. i+NLB-1); the finishers
         // stop at the first.  Slot p is free (waited above); the next NLB-1
         // slots held items that the finishers have completed or will complete.
-        for (uint32_t e = 0; e < uint32_t(NLB); ++e) {
+        for (uint32_t e = 0; e < uint32_t(NSTOP); ++e) {
           const uint32_t ie = i + e;
           const int pe = int(ie % P);
           if (e > 0 && ie / P > 0) mbar_wait(&sh.freed[pe], (ie / P - 1) & 1u);
@@ -397,16 +488,31 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
         st_release_cta_smem(&sh.item_seq[i % (2 * P)], i);  // after tile / agg
         // publish the aggregate right here, not in the look-back warp: a
         // look-back warp busy with an older tile must never delay it
+#if WF_TM_SWEEP
+        st_relaxed_gpu(desc + t, pack_desc(epoch, kStAggregate, a));  // dense: the sweeper reads 32 K per trip
+#else
         if (t == 0) {
           const uint32_t c0 = (!COMPACT && carry_in != nullptr) ? uint32_t(*carry_in) : 0u;
           st_relaxed_gpu(desc, pack_desc(epoch, kStPrefix, c0 + a));
         } else {
           st_relaxed_gpu(desc + uint64_t(t) * kDescStride, pack_desc(epoch, kStAggregate, a));
         }
+#endif
         TM_STAMP(t, 2);
         mbar_arrive1(&sh.parked[p]);
       }
+#if WF_TM_PROF
+      PROF_T(g3);
+      PROF_ADD(0, g0, g1);
+      PROF_ADD(1, g1, g2);
+      PROF_ADD(2, g2, g3);
+      acc[3] += 1;
+#endif
     }
+#if WF_TM_PROF
+    if (warp == 0 && lane == 0 && g_tm_prof)
+      for (int k = 0; k < 4; ++k) g_tm_prof[blockIdx.x * 16 + 6 + k] = acc[k];
+#endif
   } else if (warp < W_LB) {
     // ------------------------------ finishers -----------------------------
     // warp f handles tile eighth (q, h): TMEM lane quarter q = warp % 4 (the
@@ -414,13 +520,25 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
     const uint32_t q = warp & 3u, h = ((warp - W_FIN) >> 2) & 1u;
     const uint32_t grp = (warp - W_FIN) >> 3;
     const uint32_t tcol = sh.tmem_base + ((32u * q) << 16);
-    const uint32_t lt = lanemask_lt();
+#if WF_TM_PROF
+    unsigned long long acc[6] = {0, 0, 0, 0, 0, 0};
+#endif
     for (uint32_t i = grp;; i += NFG) {
       const int p = int(i % P);
       const uint32_t kp = i / P;
+      PROF_T(f0);
       mbar_wait(&sh.parked[p], kp & 1u);
+      PROF_T(f1);
       const uint32_t t = sh.slot_tile[p];
       if (t == kNoTileTm) break;
+#if WF_TM_TRACE && WF_TM_SWEEP
+      if (q == 0 && h == 0 && lane == 0) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        TM_STAMP(t, 5);
+        TM_PUT(t, 7, smid);
+      }
+#endif
       tc_fence_after();
       // everything that does not need the prefix happens before waiting for
       // it: read the slot (metadata + TMEM), free it at once — the tile now
@@ -436,6 +554,7 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive1(&sh.freed[p]);
+      PROF_T(f2);
       const bool full = vec_out && uint64_t(t + 1) * TM_TILE <= n && (t > 0 || head == 0);
       const uint64_t base0 = uint64_t(t) * TM_TILE + q * (QVEC * 128) + (8 * TMUL * h) * 128 + lane * 4;
       uint32_t loc[TMUL][8];  // scan: chunk add (local); compaction: chunk write position (local)
@@ -467,25 +586,46 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
             run += __shfl_sync(kFull, sc[j], 31);
           }
         } else {
-          // ballot + popc positions (per-lane stores after the prefix; staging
-          // in smem for 16-byte stores measured slower: 330 vs 290 us)
+          // positions: each lane's selected count per chunk (0-4) packed
+          // into byte fields, chunks 0-3 in one word and 4-7 in another, so
+          // ONE pair of warp scans yields every chunk's lane offset (a field
+          // sums to at most 128: no carry between fields).  32 ballots +
+          // 64 POPC per tile eighth took ~1150 cycles of the finisher's
+          // ~2000 per tile (WF_TM_PROF), the finisher being the pipeline's
+          // slowest stage.
+          uint32_t pk[2] = {0u, 0u};
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const uint32_t *x = v[m] + 4 * j;
-            uint32_t excl = 0, tot = 0;
+            const uint32_t c = (int32_t(x[0]) > 0) + (int32_t(x[1]) > 0) + (int32_t(x[2]) > 0) +
+                               (int32_t(x[3]) > 0);
+            pk[j >> 2] |= c << (8 * (j & 3));
+          }
+          uint32_t inc[2] = {pk[0], pk[1]};
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint32_t b = __ballot_sync(kFull, int32_t(x[k]) > 0);
-              excl += __popc(b & lt);
-              tot += __popc(b);
+          for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+            for (int w = 0; w < 2; ++w) {
+              const uint32_t y = __shfl_up_sync(kFull, inc[w], d);
+              if (lane >= uint32_t(d)) inc[w] += y;
             }
-            loc[m][j] = run + excl;
-            run += tot;
+          }
+          const uint32_t tot[2] = {__shfl_sync(kFull, inc[0], 31), __shfl_sync(kFull, inc[1], 31)};
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t sh8 = 8 * (j & 3);
+            loc[m][j] = run + (((inc[j >> 2] - pk[j >> 2]) >> sh8) & 0xffu);
+            run += (tot[j >> 2] >> sh8) & 0xffu;
           }
         }
       }
       const int r = int(i % (2 * P));
+#if WF_TM_SWEEP
+      if (q == 0 && h == 0 && lane == 0) TM_STAMP(t, 6);
+#endif
+      PROF_T(f3);
       mbar_wait(&sh.pref[r], (i / (2 * P)) & 1u);
+      PROF_T(f4);
       const uint32_t prefix = sh.item_prefix[r];
       const uint32_t off = prefix + wexcl;
 #pragma unroll
@@ -505,7 +645,7 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
               for (int k = 0; k < 4; ++k)
                 if (e + k < n && e + k >= head) out[e + k] = int32_t(x[k] + add);
             }
-          } else {
+          } else if (run != 0) {  // warp-uniform: nothing selected in this eighth, nothing to store
             uint32_t pos = off + loc[m][j];
 #pragma unroll
             for (int k = 0; k < 4; ++k)
@@ -529,7 +669,149 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
         if (COMPACT && t == ntiles - 1 && q == 0 && h == 0 && lane == 0) *count = uint64_t(prefix) + agg;
       }
       if (q == 0 && h == 0 && lane == 0) TM_STAMP(t, 4);
+#if WF_TM_PROF
+      PROF_T(f5);
+      PROF_ADD(0, f0, f1);
+      PROF_ADD(1, f1, f2);
+      PROF_ADD(2, f2, f3);
+      PROF_ADD(3, f3, f4);
+      PROF_ADD(4, f4, f5);
+      acc[5] += 1;
+#endif
     }
+#if WF_TM_PROF
+    if (warp == W_FIN && lane == 0 && g_tm_prof)
+      for (int k = 0; k < 6; ++k) g_tm_prof[blockIdx.x * 16 + k] = acc[k];
+#endif
+#if WF_TM_SWEEP
+  } else if (warp == W_LB) {
+    // ------------------------------- waiter -------------------------------
+    // The prefixes come from the grid's sweeper (below); this warp only
+    // watches them.  Lane j follows this CTA's item base + j (j < 2P, the
+    // item ring): once the item is parked it polls pref[tile] and posts the
+    // prefix to the finishers.  All of the CTA's parked items are polled in
+    // the same L2 round trip, so a late prefix never delays the next ones.
+    const uint64_t *pref = desc + pref_offset(ntiles);
+    const uint32_t tag_pref = uint32_t(pack_desc(epoch, kStPrefix, 0u) >> 32);
+    uint32_t base = 0;
+    while (true) {
+      const uint32_t item = base + lane;
+      const int r = int(item % (2 * P));
+      bool posted = false, stop = false, polled = false;
+      if (lane < 2 * P && ld_acquire_cta_smem(&sh.item_seq[r]) == item) {
+        const uint32_t t = sh.item_tile[r];
+        if (t == kNoTileTm) {
+          stop = true;
+        } else if (sh.item_posted[r] == item) {
+          posted = true;
+        } else {
+          polled = true;
+          const uint64_t d = ld_relaxed_gpu(pref + t);
+          if (uint32_t(d >> 32) == tag_pref) {  // epoch AND status: zeroed memory is epoch 0
+            sh.item_prefix[r] = uint32_t(d);
+            sh.item_posted[r] = item;
+            TM_STAMP(t, 3);
+            mbar_arrive1(&sh.pref[r]);  // release: the finishers read item_prefix
+            posted = true;
+          }
+        }
+      }
+      const uint32_t done = __ballot_sync(kFull, posted);
+      const uint32_t stops = __ballot_sync(kFull, stop);
+      const uint32_t adv = uint32_t(__ffs(~done)) - 1u;  // items posted in a row from base
+      if ((stops >> adv) & 1u) break;                      // the next item is the stop item
+      base += adv;
+      if (!__any_sync(kFull, polled)) __nanosleep(64);  // nothing parked: do not hammer smem
+      __syncwarp();
+    }
+  } else if (warp == W_SWEEP) {
+    // ------------------------------- sweeper ------------------------------
+    // One warp of CTA 0 turns the aggregates into exclusive prefixes in tile
+    // order: it reads 32 K aggregates per L2 round trip, takes the run that is
+    // published from the frontier on, scans it and publishes the prefixes.
+    // Every tile thus waits one sweep + one poll for its prefix, instead of a
+    // per-tile look-back that must walk back to an older resolved prefix and
+    // occupies a look-back warp for its whole duration (per-tile traces:
+    // ~5 us waiting for a free look-back warp + ~2.8 us of look-back).
+    if (blockIdx.x == 0) {
+      uint64_t *pref = desc + pref_offset(ntiles);
+      const uint32_t tag_agg = uint32_t(pack_desc(epoch, kStAggregate, 0u) >> 32);
+      uint32_t run = (!COMPACT && carry_in != nullptr) ? uint32_t(*carry_in) : 0u;
+      uint32_t f = 0, backoff = 32;
+      constexpr int K = WF_SWEEP_K;
+#if WF_TM_TRACE
+      uint32_t it = 0;
+#endif
+      while (f < ntiles) {
+#if WF_TM_TRACE
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#endif
+        // all K loads are issued before any result is examined: a compare
+        // scheduled right behind its load would serialise the K round trips
+        // (measured: 5-6 us per iteration instead of one round trip)
+        uint64_t d[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const uint32_t idx = f + lane + 32u * k;
+          d[k] = idx < ntiles ? ld_relaxed_gpu(desc + idx) : 0ull;
+        }
+        uint32_t v[K];
+        bool ok[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          ok[k] = uint32_t(d[k] >> 32) == tag_agg;  // zeroed memory (epoch 0, status 0) never matches
+          v[k] = uint32_t(d[k]);
+        }
+        uint32_t ready = 0;
+        bool gap = false;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const uint32_t b = __ballot_sync(kFull, ok[k]);
+          if (!gap) {
+            if (b == kFull) {
+              ready += 32;
+            } else {
+              ready += uint32_t(__ffs(~b)) - 1u;
+              gap = true;
+            }
+          }
+        }
+#if WF_TM_TRACE
+        if (lane == 0 && g_sweep_trace && it < g_sweep_cap) {
+          g_sweep_trace[2 * it] = t0;
+          g_sweep_trace[2 * it + 1] = f | (uint64_t(ready) << 32);
+        }
+        ++it;
+#endif
+        if (ready == 0) {
+          __nanosleep(backoff);
+          backoff = backoff < 256 ? backoff * 2 : 256;
+          continue;
+        }
+        backoff = 32;
+        uint32_t sc[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) sc[k] = 32u * k + lane < ready ? v[k] : 0u;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const uint32_t y = __shfl_up_sync(kFull, sc[k], d);
+            if (lane >= uint32_t(d)) sc[k] += y;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const uint32_t j = 32u * k + lane;
+          if (j < ready) st_relaxed_gpu(pref + f + j, pack_desc(epoch, kStPrefix, run + sc[k] - v[k]));
+          run += __shfl_sync(kFull, sc[k], 31);
+        }
+        f += ready;
+      }
+    }
+  }
+#else
   } else if (warp < W_PROD) {
     // ----------------------------- look-back ------------------------------
     const uint32_t me = warp - W_LB;
@@ -550,11 +832,24 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       const uint32_t t = sh.item_tile[ri];
       if (t == kNoTileTm) break;
       const uint32_t agg = sh.item_agg[ri];
+      if (lane == 0) TM_STAMP(t, 5);
       uint32_t excl;
       if (t == 0) {  // its prefix descriptor was published by the aggregator
         excl = (!COMPACT && carry_in != nullptr) ? uint32_t(*carry_in) : 0u;
       } else {
+#if WF_TM_TRACE
+        uint32_t polls = 0;
+        excl = lookback_exclusive_wide<COMPACT ? WF_LBK_COMPACT_TM : WF_LBK_TM>(desc, t, epoch,
+                                                                               &polls);
+        if (lane == 0) {
+          uint32_t smid;
+          asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+          TM_PUT(t, 6, polls);
+          TM_PUT(t, 7, smid);
+        }
+#else
         excl = lookback_exclusive_wide<COMPACT ? WF_LBK_COMPACT_TM : WF_LBK_TM>(desc, t, epoch);
+#endif
         if (lane == 0)
           st_relaxed_gpu(desc + uint64_t(t) * kDescStride, pack_desc(epoch, kStPrefix, excl + agg));
       }
@@ -567,6 +862,7 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       __syncwarp();
     }
   }
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -598,7 +894,8 @@ int tmem_grid(uint32_t ntiles) {
     if (b < 1) b = 1;
   }
   const uint32_t g = uint32_t(b) * uint32_t(sm_count(current_device()));
-  return int(ntiles < g ? ntiles : g);
+  const uint32_t want = (ntiles + kBatch - 1) / kBatch;  // a CTA's first draw is a whole batch
+  return int(want < g ? want : g);
 }
 
 }  // namespace
@@ -607,6 +904,20 @@ int tmem_grid(uint32_t ntiles) {
 extern "C" int wf_debug_set_trace_tm(void *buf) {
   unsigned long long *p = static_cast<unsigned long long *>(buf);
   return int(cudaMemcpyToSymbol(g_tm_trace, &p, sizeof(p)));
+}
+#endif
+#if WF_TM_PROF
+extern "C" int wf_debug_set_prof_tm(void *buf) {
+  unsigned long long *p = static_cast<unsigned long long *>(buf);
+  return int(cudaMemcpyToSymbol(g_tm_prof, &p, sizeof(p)));
+}
+#endif
+#if WF_TM_TRACE
+extern "C" int wf_debug_set_trace_sweep(void *buf, uint32_t cap) {
+  unsigned long long *p = static_cast<unsigned long long *>(buf);
+  cudaError_t e = cudaMemcpyToSymbol(g_sweep_trace, &p, sizeof(p));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_sweep_cap, &cap, sizeof(cap));
+  return int(e);
 }
 #endif
 

@@ -493,7 +493,7 @@ def test_host_entry_points(ops):
 @pytest.mark.parametrize("n", [0, 1, 5, 8191, (1 << 20) + 3, 3 * 22369536 + 7])
 def test_host_scan_and_compaction(ops, n):
     """wf_scan_inclusive_i32_host / wf_compact_gt0_i32_host: host buffer in,
-    host buffer out, through the three-slot H2D / kernel / D2H ring; the
+    host buffer out, through the 8-slot H2D / kernel / D2H ring; the
     largest size spans several chunks (carry chain, output offsets)."""
     a = synthetic.generate("i32_full", n, seed=n + 21)
     pinned = torch.from_numpy(a).pin_memory()
@@ -510,7 +510,7 @@ def test_host_scan_and_compaction(ops, n):
 
 @pytest.mark.parametrize("permille", [0, 10, 1000])
 def test_host_compaction_selectivity(ops, permille):
-    n = 2 * 11184768 + 333  # three chunks of the compaction ring
+    n = 2 * 11184768 + 333  # several 16 MiB chunks of the compaction ring
     a = synthetic.generate("i32_select", n, seed=3, param=permille)
     res, m = ops.compact_gt0_i32_host(a)
     want = no.compact_gt0_i32(a)

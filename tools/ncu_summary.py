@@ -24,7 +24,11 @@ NAMES = {"reduce_kernel<wf::<unnamed>::SumI32": "reduce_sum_i32",
          # two template parameters since the fused multi-GPU form: <COMPACT, PX>
          "tile_tmem_kernel<0, ": "scan_inclusive_i32", "tile_tmem_kernel<1, ": "compact_gt0_i32",
          "tile_tmem_kernel<(bool)0, ": "scan_inclusive_i32",
-         "tile_tmem_kernel<(bool)1, ": "compact_gt0_i32"}
+         "tile_tmem_kernel<(bool)1, ": "compact_gt0_i32",
+         "warp_partials_kernel<1>": "warp_partials_sum_f32 (reference C1_F32 text)",
+         "warp_partials_kernel<true>": "warp_partials_sum_f32 (reference C1_F32 text)",
+         "warp_partials_kernel<(bool)1>": "warp_partials_sum_f32 (reference C1_F32 text)",
+         "warp_prefix32_vec_kernel": "warp_prefix32_i32 (reference C3_WARP_PREFIX text)"}
 
 
 def op_name(kernel: str) -> str:

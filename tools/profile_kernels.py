@@ -9,7 +9,7 @@ import torch  # noqa: E402
 
 from paper_2112_10034_b200 import ops  # noqa: E402
 
-which = sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"]
+which = sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5", "ref"]
 torch.cuda.set_device(0)
 reps = 2
 if "c1" in which:
@@ -31,6 +31,23 @@ if "c3" in which or "c4" in which:
     if "c4" in which:
         for _ in range(reps):
             ops.compact_gt0_i32(x, y)
+    del x, y
+if "ref" in which:  # the reference's own formulations (dsl/patterns.py native kernels)
+    from paper_2112_10034_b200.dsl import patterns
+    pw = patterns.NativePattern("warp_partials_sum_f32", "wf_warp_partials_sum_f32", "a", "out", "n")
+    pp = patterns.NativePattern("warp_prefix32_i32", "wf_warp_prefix32_i32", "a", "out")
+    x = ops.fill_synthetic("f32_unit", 1 << 30, seed=1)
+    o = torch.empty(148 * 8 * 8, dtype=torch.float32, device="cuda")
+    cfg = type("C", (), {"grid_size": 148 * 8, "block_size": 256, "warp_size": 32})()
+    st = torch.cuda.current_stream().cuda_stream
+    for _ in range(reps):
+        pw.run(cfg, {"a": x, "out": o, "n": 1 << 30}, st)
+    del x, o
+    x = ops.fill_synthetic("i32_full", 1 << 28, seed=0)
+    y = torch.empty_like(x)
+    cfg = type("C", (), {"grid_size": (1 << 28) // 256, "block_size": 256, "warp_size": 32})()
+    for _ in range(reps):
+        pp.run(cfg, {"a": x, "out": y}, st)
     del x, y
 if "c5" in which:
     u = ops.fill_synthetic("u8_uniform", 1 << 32, seed=0)
