@@ -38,6 +38,31 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
   return r;
 }
 
+// 128-bit load marking the line evict_last in L2 (cache-policy form): for
+// data the next kernel re-reads (the sharded scan's pass 1).
+__device__ __forceinline__ uint4 ldg_keep(const uint4 *p) {
+  uint4 r;
+  asm volatile(
+      "{\n\t.reg .b64 pol;\n\t"
+      "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+      "ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], pol;\n\t}"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p));
+  return r;
+}
+
+// 128-bit load marking the line evict_first in L2: read once, never again.
+__device__ __forceinline__ uint4 ldg_evict_first(const uint4 *p) {
+  uint4 r;
+  asm volatile(
+      "{\n\t.reg .b64 pol;\n\t"
+      "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+      "ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], pol;\n\t}"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p));
+  return r;
+}
+
 // 128-bit streaming store (evict-first: output is not re-read by the kernel).
 __device__ __forceinline__ void stg_stream(uint4 *p, const uint4 &v) {
   asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p),

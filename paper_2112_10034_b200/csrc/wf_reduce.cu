@@ -108,6 +108,13 @@ __device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long
   return v;
 }
 
+#ifndef WF_PX_KEEP_MB
+#define WF_PX_KEEP_MB 32  // pass 1 of the sharded scan: its last 32 MB read are marked evict_last, the rest evict_first
+#endif
+#ifndef WF_PX_REV
+#define WF_PX_REV 1  // pass 1 of the sharded scan streams its shard backwards
+#endif
+
 // PX (i32 only): the last block also runs the peer exchange of wf_peer.cuh on
 // the rank total (exclusive scan over ranks, mod 2^32), so out = {carry of
 // this rank's shard, global total} — the sharded scan's pass 1 and its carry
@@ -148,11 +155,23 @@ __global__ void __launch_bounds__(BLOCK)
 #pragma unroll
     for (int k = 0; k < 4; ++k) acc[u][k] = Op::zero();
 
+  // PX (pass 1 of the sharded scan) streams the shard from its END to its
+  // start, so the lines read last — the shard's head, which the scan that
+  // follows reads first — are the ones still in L2 when it starts (the i32
+  // wrapping sum is order-free)
+  auto vec_at = [&](uint64_t v) { return (PX && WF_PX_REV) ? vin + (nvec - 1 - v) : vin + v; };
+  const uint64_t keep_vec = (uint64_t(WF_PX_KEEP_MB) << 20) / 16;
   uint64_t i = gtid;
   for (; i + uint64_t(UNROLL - 1) * nthreads < nvec; i += UNROLL * nthreads) {
     uint4 q[UNROLL];
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) q[u] = ldg_stream(vin + i + u * nthreads);
+    for (int u = 0; u < UNROLL; ++u) {
+      const uint64_t v = i + u * nthreads;
+      if (PX && WF_PX_KEEP_MB > 0)  // read last = the scan's first reads: keep; the rest: evict first
+        q[u] = v + keep_vec >= nvec ? ldg_keep(vec_at(v)) : ldg_evict_first(vec_at(v));
+      else
+        q[u] = ldg_stream(vec_at(v));
+    }
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
       acc[u][0] = Op::add(acc[u][0], Op::from_bits(q[u].x));
@@ -164,7 +183,7 @@ __global__ void __launch_bounds__(BLOCK)
 #pragma unroll
   for (int u = 0; u < UNROLL; ++u) {  // remainder: < UNROLL vectors left
     if (i < nvec) {
-      const uint4 q = ldg_stream(vin + i);
+      const uint4 q = ldg_stream(vec_at(i));
       acc[u][0] = Op::add(acc[u][0], Op::from_bits(q.x));
       acc[u][1] = Op::add(acc[u][1], Op::from_bits(q.y));
       acc[u][2] = Op::add(acc[u][2], Op::from_bits(q.z));
