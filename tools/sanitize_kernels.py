@@ -20,6 +20,22 @@ r = [ops.reduce_sum_i32(x), ops.reduce_sum_f32(f), ops.scan_inclusive_i32(x),
 a = torch.arange(96, dtype=torch.int32, device="cuda")
 for kind in ("shfl_down", "shfl_up", "shfl_xor", "shfl_idx", "vote_all", "vote_any", "ballot", "reduce_add"):
     r.append(ops.warp_collective(kind, a, operand=3, block=96))
+# the reference's own formulations (dsl/patterns.py native kernels)
+from paper_2112_10034_b200.dsl import patterns  # noqa: E402
+st = torch.cuda.current_stream().cuda_stream
+for name, sym, nn in (("warp_partials_sum_i32", "wf_warp_partials_sum_i32", "n"),
+                      ("warp_partials_sum_f32", "wf_warp_partials_sum_f32", "n")):
+    pat = patterns.NativePattern(name, sym, "a", "out", nn)
+    cfg = type("C", (), {"grid_size": 37, "block_size": 96, "warp_size": 32})()
+    o = torch.zeros(37 * 3, dtype=torch.int32, device="cuda")
+    pat.run(cfg, {"a": x if "i32" in name else f, "out": o, "n": n}, st)
+    r.append(o)
+pat = patterns.NativePattern("warp_prefix32_i32", "wf_warp_prefix32_i32", "a", "out")
+cfg = type("C", (), {"grid_size": 300, "block_size": 256, "warp_size": 32})()
+o = torch.zeros(300 * 256, dtype=torch.int32, device="cuda")
+pat.run(cfg, {"a": x, "out": o}, st)
+pat.run(cfg, {"a": x[1:], "out": o}, st)
+r.append(o)
 # the fused multi-GPU forms (world 1: own mailbox; the peer stores and the
 # flag/epoch protocol still run)
 from paper_2112_10034_b200 import p2p  # noqa: E402
