@@ -852,7 +852,7 @@ def per_kernel(args, rank, world, local, dev, peak, checks: dict) -> dict:
     return res
 
 
-def warpfold_python_sample(n: int = 1 << 18) -> dict | None:
+def warpfold_python_sample(n: int = 1 << 20) -> dict | None:
     """The reference's OWN CPU path, unmodified: warpfold's
     launch(hybrid_transform(kernel)) (runtime/launch.py:90,
     passes/pipeline.py:103) on the per-warp-partials fp32 kernel of SURVEY
