@@ -81,6 +81,17 @@ __device__ __noinline__ void wf_fail(wf_err_t *e, unsigned long long code, long 
 }
 // execution counting (ExecTrace): one counter per reference CFG uid
 __device__ __forceinline__ void wf_tick(unsigned long long *t, int uid) { atomicAdd(t + uid, 1ull); }
+// barrier arrival log (ExecTrace.barrier_arrivals, interp/oracle.py:207,237):
+// a[0] = record count; record i at a[4 + 4 i] = {uid, block, phase << 32 |
+// warp episode, warp << 32 | arrival mask (warp = 0xffffffff: the whole block)}
+__device__ __noinline__ void wf_arrive(unsigned long long *a, long long cap, int uid,
+                                       unsigned long long ph_ep, unsigned long long warp_mask) {
+  const unsigned long long i = atomicAdd(a, 1ull);
+  if ((long long)i < cap) {
+    unsigned long long *r = a + 4 + 4 * i;
+    r[0] = (unsigned long long)uid; r[1] = blockIdx.x; r[2] = ph_ep; r[3] = warp_mask;
+  }
+}
 __device__ __forceinline__ int wf_add(int a, int b) { return (int)((unsigned)a + (unsigned)b); }
 __device__ __forceinline__ int wf_sub(int a, int b) { return (int)((unsigned)a - (unsigned)b); }
 __device__ __forceinline__ int wf_mul(int a, int b) { return (int)((unsigned)a * (unsigned)b); }
@@ -379,11 +390,24 @@ class CudaGen:
             self.loop(s, depth)
         elif isinstance(s, n.SyncThreads):
             uid = self.new_uid("Barrier")
-            self.emit(f"{self.tick(uid)}__syncthreads();", depth)
+            if self.trace:  # one rendezvous of the whole block (interp/oracle.py:237)
+                self.emit(f"{self.tick(uid)}if (threadIdx.x == 0) wf_arrive(wf_arr, wf_arr_cap, {uid}, "
+                          f"(unsigned long long)wf_phase << 32, 0xffffffff00000000ull); "
+                          f"__syncthreads(); ++wf_phase;", depth)
+            else:
+                self.emit("__syncthreads();", depth)
         elif isinstance(s, n.SyncWarp):
             m = self.mask(s.mask)
             uid = self.new_uid("Barrier")
-            self.emit(f"{self.tick(uid)}__syncwarp({m});", depth)
+            if self.trace:  # the logical warp's arriving lanes (interp/oracle.py:207)
+                self.emit(f"{{ {self.tick(uid)}const unsigned wf_m = {m}; "
+                          f"const unsigned wf_am = __activemask() & wf_m; "
+                          f"if ((threadIdx.x & 31u) == (unsigned)(__ffs(wf_am) - 1)) "
+                          f"wf_arrive(wf_arr, wf_arr_cap, {uid}, ((unsigned long long)wf_phase << 32) | "
+                          f"(unsigned)wf_wep, ((unsigned long long)(threadIdx.x / WF_W) << 32) | "
+                          f"(wf_am >> wf_seg())); __syncwarp(wf_m); ++wf_wep; }}", depth)
+            else:
+                self.emit(f"__syncwarp({m});", depth)
         elif isinstance(s, n.Return):
             uid = self.new_uid("Br")
             self.emit(f"{self.tick(uid)}goto wf_exit;" if self.trace else "return;", depth)
@@ -448,6 +472,8 @@ class CudaGen:
         params += ["wf_err_t *__restrict__ wf_e", "long long wf_dyn_len", "long long wf_step_limit"]
         if self.trace:
             params.append("unsigned long long *__restrict__ wf_tr")
+            params.append("unsigned long long *__restrict__ wf_arr")
+            params.append("long long wf_arr_cap")
         ret_uid = self.new_uid("Ret")  # the exit block's Ret is allocated first
         out = [f"#define WF_W {self.W}u", PRELUDE,
                f'extern "C" __global__ void __launch_bounds__(1024) wf_kernel({", ".join(params)}) {{']
@@ -463,6 +489,8 @@ class CudaGen:
         if self.t.shared:
             out.append("  __syncthreads();")
         out.append("  int wf_dead = 0;")
+        if self.trace:
+            out.append("  int wf_phase = 0, wf_wep = 0;  // block-barrier phase, warp-barrier episode")
         out.append("  long long wf_steps = 0;")
         for name, kind in self.t.locals.items():
             out.append(f"  {CTYPE[kind]} v_{name} = ({CTYPE[kind]})0;")

@@ -31,6 +31,8 @@ from .codegen import generate, generate_traced
 # per-thread interpreter budget (interp/oracle.py:26, :113-119), counted in
 # loop iterations rather than instructions.
 DEFAULT_STEP_LIMIT = 50_000_000
+# barrier episodes one traced launch may record (ExecTrace.barrier_arrivals)
+ARRIVAL_CAP = 1 << 20
 
 _cache_lock = threading.Lock()
 _fault_bufs: dict = {}
@@ -170,7 +172,9 @@ class JitProgram:
         keep += [C.c_void_p(err.data_ptr()), C.c_longlong(dyn_len), C.c_longlong(int(step_limit))]
         if trace is not None:
             counts = torch.zeros(self.layout.max_uid + 1, dtype=torch.int64, device=memory.device)
-            keep.append(C.c_void_p(counts.data_ptr()))
+            arr = torch.zeros(4 + 4 * ARRIVAL_CAP, dtype=torch.int64, device=memory.device)
+            keep += [C.c_void_p(counts.data_ptr()), C.c_void_p(arr.data_ptr()),
+                     C.c_longlong(ARRIVAL_CAP)]
         argv = (C.c_void_p * len(keep))(*[C.addressof(k) for k in keep])
         stream = torch.cuda.current_stream(memory.device)
         rc = _lib.load().wf_jit_launch(mod, config.grid_size, config.block_size,
@@ -190,6 +194,32 @@ class JitProgram:
             for uid in self.layout.term_uids:
                 if c[uid]:
                     trace.count_term(uid, c[uid])
+            self._record_arrivals(arr, config, trace)
+
+    def _record_arrivals(self, arr, config: LaunchConfig, trace) -> None:
+        """Barrier arrival sets in the reference's order (interp/oracle.py:
+        blocks one after another; within a block, phase by phase between
+        block barriers; within a phase, warp 0's warp-barrier episodes, then
+        warp 1's ...): one frozenset of block-local thread ids per episode."""
+        n_rec = int(arr[0].item())
+        if n_rec > ARRIVAL_CAP:
+            raise ExecutionError(f"barrier arrival log overflow: {n_rec} episodes "
+                                 f"(capacity {ARRIVAL_CAP})")
+        if n_rec == 0:
+            return
+        rec = arr[4:4 + 4 * n_rec].view(-1, 4).cpu().numpy().astype(np.uint64)
+        W = config.warp_size
+        full = frozenset(range(config.block_size))
+        rows = []
+        for uid, blk, ph_ep, warp_mask in rec.tolist():
+            warp, mask = warp_mask >> 32, warp_mask & 0xFFFFFFFF
+            block_level = warp == 0xFFFFFFFF
+            key = (blk, ph_ep >> 32, -1 if block_level else warp, ph_ep & 0xFFFFFFFF)
+            tids = full if block_level else frozenset(
+                warp * W + l for l in range(W) if (mask >> l) & 1)
+            rows.append((key, uid, tids))
+        for _, uid, tids in sorted(rows, key=lambda r: r[0]):
+            trace.record_arrival(int(uid), tids)
 
     def _message(self, code, arg, idx, length) -> str:
         if code in (1, 2):

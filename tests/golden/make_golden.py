@@ -321,9 +321,12 @@ def corpus_traces() -> dict:
             cfg = LaunchConfig(grid_size=grid, block_size=block, warp_size=warp, workers=1)
             tr = ExecTrace()
             run_oracle(kernel, cfg, bind_args(kernel.params, mem, args), tr)
-            out["runs"][f"{k.name}__g{grid}b{block}w{warp}"] = {
-                "instr": {str(u): c for u, c in sorted(tr.instr_counts.items())},
-                "term": {str(u): c for u, c in sorted(tr.term_counts.items())}}
+            run = {"instr": {str(u): c for u, c in sorted(tr.instr_counts.items())},
+                   "term": {str(u): c for u, c in sorted(tr.term_counts.items())}}
+            if tr.barrier_arrivals:  # interp/oracle.py:207 (warp), :237 (block)
+                run["arrivals"] = {str(u): [sorted(s) for s in sets]
+                                   for u, sets in sorted(tr.barrier_arrivals.items())}
+            out["runs"][f"{k.name}__g{grid}b{block}w{warp}"] = run
     return out
 
 

@@ -106,3 +106,7 @@ def test_gpu_exec_counts_equal_reference_oracle(tag):
     assert all(u > max_uid for u in extra), (tag, extra)
     # every thread reaches the exit exactly once (the Ret allocated first)
     assert trace.term_counts[1] == m["grid"] * m["block"]
+    # barrier arrival sets, episode by episode in the oracle's order
+    # (interp/oracle.py:207 warp barriers, :237 block barriers)
+    got = {str(u): [sorted(s) for s in sets] for u, sets in trace.barrier_arrivals.items()}
+    assert got == want.get("arrivals", {}), tag
