@@ -193,6 +193,38 @@ int wf_peer_exchange(int mode, const void *d_vals, uint32_t count, uint32_t cap,
                      int rank, int world, uint32_t epoch, uint32_t *d_err,
                      wf_stream_t stream);
 
+/* ---- single-process multi-GPU (wf_mg_init + wf_mg_<op>) --
+ * One host thread drives `ngpus` ranks on the listed devices (ranks may share
+ * a device).  Each call enqueues one rank's kernel per device on the
+ * context's per-rank stream, each kernel carrying its exchange over peer
+ * memory (NVLink / NVSwitch peer access, enabled by wf_mg_init); arrays are
+ * indexed by rank, pointers are device pointers on that rank's device, shards
+ * are the caller's contiguous split (runtime/launch.py:137-147 `_split`
+ * across devices).  Results are valid after wf_mg_synchronize, which returns
+ * WF_ERR_COMM if a rank's peers never arrived.
+ *   reduce_sum_f32: d_out[r][0] = the fp32 sum of all shards, bit-identical
+ *                   on every rank (fixed rank-order fold)
+ *   scan_inclusive_i32: d_out[r] = the global inclusive scan over rank r's shard
+ *   compact_gt0_i32: d_out[r] = rank r's selected elements, d_counts3[r] =
+ *                   {count, global offset, global total}
+ *   histogram256_u8: d_bins[r] = the global 256 bins on every rank
+ * Reference anchor: runtime/launch.py:95-147 (block-range split + join). */
+typedef struct wf_mg wf_mg_t;
+int wf_mg_init(int ngpus, const int *devs, wf_mg_t **ctx);
+int wf_mg_size(const wf_mg_t *ctx);
+int wf_mg_stream(wf_mg_t *ctx, int rank, wf_stream_t *stream);
+int wf_mg_reduce_sum_f32(wf_mg_t *ctx, const float *const *d_in,
+                         const uint64_t *n, float *const *d_out);
+int wf_mg_scan_inclusive_i32(wf_mg_t *ctx, const int32_t *const *d_in,
+                             int32_t *const *d_out, const uint64_t *n);
+int wf_mg_compact_gt0_i32(wf_mg_t *ctx, const int32_t *const *d_in,
+                          const uint64_t *n, int32_t *const *d_out,
+                          uint64_t *const *d_counts3);
+int wf_mg_histogram256_u8(wf_mg_t *ctx, const uint8_t *const *d_in,
+                          const uint64_t *n, uint64_t *const *d_bins);
+int wf_mg_synchronize(wf_mg_t *ctx);
+void wf_mg_destroy(wf_mg_t *ctx);
+
 /* ---- K3: shfl_scan inclusive prefix sum --------------------------------
  * out[i] = carry + in[0] + ... + in[i] (wrapping), single pass with
  * decoupled look-back.  d_carry_in: device int32 (NULL = 0), used by the

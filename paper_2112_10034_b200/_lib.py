@@ -78,6 +78,15 @@ SIGNATURES = {
     "wf_warp_partials_sum_i32": (C.c_int, [_vp, _i32, _vp, C.c_int, C.c_int, _vp]),
     "wf_warp_partials_sum_f32": (C.c_int, [_vp, _i32, _vp, C.c_int, C.c_int, _vp]),
     "wf_warp_prefix32_i32": (C.c_int, [_vp, _vp, _u64, _vp]),
+    "wf_mg_init": (C.c_int, [C.c_int, _vp, C.POINTER(_vp)]),
+    "wf_mg_size": (C.c_int, [_vp]),
+    "wf_mg_stream": (C.c_int, [_vp, C.c_int, C.POINTER(_vp)]),
+    "wf_mg_reduce_sum_f32": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "wf_mg_scan_inclusive_i32": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "wf_mg_compact_gt0_i32": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "wf_mg_histogram256_u8": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "wf_mg_synchronize": (C.c_int, [_vp]),
+    "wf_mg_destroy": (None, [_vp]),
     "wf_fill_synthetic": (C.c_int, [C.c_int, _vp, _u64, _u64, _u64, _u32, _vp]),
     "wf_reduce_sum_f32_host": (C.c_int, [_vp, _u64, _vp, _vp, _sz, _vp, _sz, _vp]),
     "wf_reduce_sum_i32_host": (C.c_int, [_vp, _u64, _vp, _vp, _sz, _vp, _sz, _vp]),

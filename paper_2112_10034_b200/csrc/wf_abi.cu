@@ -29,6 +29,8 @@ static int fail(int code, const char *fmt, ...) {
   return code;
 }
 
+int set_error(int code, const char *msg) { return fail(code, "%s", msg); }
+
 static int cuda_status(cudaError_t e, const char *what) {
   if (e == cudaSuccess) return WF_OK;
   cudaGetLastError();  // clear the sticky-free error state
@@ -248,9 +250,23 @@ size_t wf_mailbox_bytes(int world) {
   return world < 1 ? 0 : (size_t(2) * size_t(world) * 8 + 255) & ~size_t(255);
 }
 
+// Every kernel that may spin on its peers, loaded on the current device at
+// mailbox set-up (before any exchange can be in flight): with lazy module
+// loading, the first launch of a not-yet-loaded kernel can wait for the
+// device to go idle — which a peer kernel already spinning on the same
+// device never lets happen (ranks sharing a device, the wf_mg ABI).
+static int preload_exchange_kernels() {
+  cudaError_t e = preload_peer_kernels();
+  if (e == cudaSuccess) e = preload_hist_mg_kernels();
+  if (e == cudaSuccess) e = preload_reduce_mg_kernels();
+  if (e == cudaSuccess) e = preload_tmem_mg_kernels();
+  return cuda_status(e, "loading the exchange kernels");
+}
+
 int wf_mailbox_alloc(int world, void **d_mailbox) {
   if (d_mailbox == nullptr || world < 1 || world > 32)
     return fail(WF_ERR_ARG, "mailbox: world must be in [1, 32]");
+  if (int rc = preload_exchange_kernels()) return rc;
   const size_t b = wf_mailbox_bytes(world);
   int rc = cuda_status(cudaMalloc(d_mailbox, b), "mailbox alloc");
   if (rc) return rc;
@@ -301,6 +317,7 @@ size_t wf_peer_mailbox_bytes(int world, uint32_t cap) {
 int wf_peer_mailbox_alloc(int world, uint32_t cap, void **d_mailbox) {
   if (d_mailbox == nullptr || world < 1 || world > 256 || cap < 1 || cap > (1u << 20))
     return fail(WF_ERR_ARG, "peer mailbox: world in [1, 256], cap in [1, 2^20]");
+  if (int rc = preload_exchange_kernels()) return rc;
   const size_t b = peer_mailbox_bytes(world, cap);
   int rc = cuda_status(cudaMalloc(d_mailbox, b), "peer mailbox alloc");
   if (rc) return rc;

@@ -215,4 +215,10 @@ cudaError_t launch_hist256_mg(const uint8_t *in, uint64_t n, uint64_t *bins, int
   return cudaGetLastError();
 }
 
+cudaError_t preload_hist_mg_kernels() {
+  configure_hist(true);
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, hist256_kernel<true>);
+}
+
 }  // namespace wf

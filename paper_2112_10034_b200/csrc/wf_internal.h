@@ -40,6 +40,12 @@ constexpr int kHistBlock = WF_HIST_BLOCK;
 constexpr size_t kHistSmem = 256 * (WF_HIST_PRMT ? 64 : WF_HIST_BINW) * sizeof(uint32_t);
 
 int sm_count(int device);
+int set_error(int code, const char *msg);  // wf_last_error() text + return code
+// load the exchange-carrying kernels on the current device (see wf_peer.cu)
+cudaError_t preload_peer_kernels();
+cudaError_t preload_hist_mg_kernels();
+cudaError_t preload_reduce_mg_kernels();
+cudaError_t preload_tmem_mg_kernels();
 int current_device();
 
 // Per-device one-time configuration: function attributes such as the

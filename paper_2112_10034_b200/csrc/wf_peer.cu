@@ -43,4 +43,13 @@ cudaError_t launch_peer_exchange(int mode, const void *vals, uint32_t count, uin
   return cudaGetLastError();
 }
 
+// Loads the exchange kernel's module on the current device now: with lazy
+// module loading a first launch can wait for the device to go idle, which a
+// peer already spinning on this exchange never lets happen (wf_mg / ranks
+// sharing a device).
+cudaError_t preload_peer_kernels() {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, peer_exchange_kernel);
+}
+
 }  // namespace wf

@@ -480,4 +480,21 @@ cudaError_t launch_fold_u64(const uint64_t *v, uint32_t count, uint64_t *out,
   return cudaGetLastError();
 }
 
+cudaError_t preload_reduce_mg_kernels() {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaSuccess;
+  auto get = [&](const void *f) {
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, f);
+  };
+  get(reinterpret_cast<const void *>(reduce_kernel<SumI32, 128, kUnroll, false, true>));
+  get(reinterpret_cast<const void *>(reduce_kernel<SumI32, 256, kUnroll, false, true>));
+  get(reinterpret_cast<const void *>(reduce_kernel<SumI32, 512, kUnroll, false, true>));
+  get(reinterpret_cast<const void *>(reduce_kernel<SumI32, 1024, kUnroll, false, true>));
+  get(reinterpret_cast<const void *>(reduce_kernel<SumF32, 128, kUnroll, true>));
+  get(reinterpret_cast<const void *>(reduce_kernel<SumF32, 256, kUnroll, true>));
+  get(reinterpret_cast<const void *>(reduce_kernel<SumF32, 512, kUnroll, true>));
+  get(reinterpret_cast<const void *>(reduce_kernel<SumF32, 1024, kUnroll, true>));
+  return e;
+}
+
 }  // namespace wf

@@ -964,4 +964,10 @@ cudaError_t launch_compact_tmem_i32_mg(const int32_t *in, uint64_t n, int32_t *o
   return cudaGetLastError();
 }
 
+cudaError_t preload_tmem_mg_kernels() {
+  tmem_grid<true, true>(1);  // dynamic-smem opt-in on this device
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, tile_tmem_kernel<true, true>);
+}
+
 }  // namespace wf

@@ -24,7 +24,7 @@ import torch
 
 from . import ops
 from .config import LaunchConfig
-from .errors import ExecutionError, LaunchError, UnsupportedFeatureError
+from .errors import ConfigError, ExecutionError, LaunchError, UnsupportedFeatureError
 from .memory import DeviceMemory
 
 
@@ -76,6 +76,11 @@ def bind_args(params, memory: DeviceMemory, args) -> dict:
 
 def launch(program, config: LaunchConfig, memory: DeviceMemory, args, trace=None) -> None:
     config.validate(hierarchical=(getattr(program, "mode", "hier") == "hier"))
+    if config.device is not None and int(config.device) != memory.device.index:
+        # the buffers live on the memory's device; a launch elsewhere would
+        # read them over the peer path or fault
+        raise ConfigError(f"LaunchConfig.device is {config.device} but the memory's buffers "
+                          f"live on cuda:{memory.device.index}")
     if config.grid_size == 0:
         return
     if trace is not None and isinstance(program, NativeProgram):
