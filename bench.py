@@ -650,7 +650,7 @@ def reference_api_rows(dev, peak, steps: int, warm: int, checks: dict) -> dict:
     rows = {}
     specs = (  # key, kernel text, kind, n, grid, block, generator, bytes per element
         ("c1_wsum_i32", "C1_I32", "i32", N_C1, 4096, 256, "i32_full", 4),
-        ("c2_wsum_f32", "C1_F32", "f32", N_C2, 148 * 8, 256, "f32_unit", 4),
+        ("c2_wsum_f32", "C1_F32", "f32", N_C2, 4096, 256, "f32_unit", 4),
         ("c3_warp_prefix_i32", "C3_WARP_PREFIX", "i32", N_C3, N_C3 // 256, 256, "i32_full", 8),
     )
     for key, spk, kind, n, grid, block, gen, bpe in specs:

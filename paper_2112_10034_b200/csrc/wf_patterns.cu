@@ -31,7 +31,10 @@
 namespace wf {
 namespace {
 
-constexpr int kPartialsUnroll = 16;  // loads in flight per thread ahead of the in-order adds
+#ifndef WF_PARTIALS_UNROLL
+#define WF_PARTIALS_UNROLL 16
+#endif
+constexpr int kPartialsUnroll = WF_PARTIALS_UNROLL;  // loads in flight per thread ahead of the in-order adds
 
 __device__ __forceinline__ uint32_t ldg_na_u32(const uint32_t *p) {
   uint32_t r;
@@ -96,7 +99,13 @@ __global__ void __launch_bounds__(1024) warp_partials_kernel(const uint32_t *__r
 // 8 lanes per 32-element segment, 4 elements per lane (one 16-byte load),
 // kPrefixVec vectors per thread per iteration (all loads issued first),
 // grid-stride over the n/4 vectors; width-8 SHFL.UP scan of the lane totals.
-constexpr int kPrefixVec = 4;
+#ifndef WF_PREFIX_VEC
+#define WF_PREFIX_VEC 4
+#endif
+#ifndef WF_PREFIX_CTAS
+#define WF_PREFIX_CTAS 16  // CTAs per SM the grid is sized for (8: 361 us, 16: 345 us at 2^28; tools/patterns_probe.py)
+#endif
+constexpr int kPrefixVec = WF_PREFIX_VEC;
 __global__ void __launch_bounds__(256) warp_prefix32_vec_kernel(const uint4 *__restrict__ a,
                                                                 uint4 *__restrict__ out,
                                                                 uint64_t nvec) {
@@ -181,7 +190,8 @@ cudaError_t launch_warp_prefix32(const int32_t *a, int32_t *out, uint64_t n, cud
   if (((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(out)) & 15u) == 0) {
     const uint64_t nvec = n / 4;
     const uint64_t want = (nvec + 256 * kPrefixVec - 1) / (256 * kPrefixVec);
-    const uint64_t grid = want < uint64_t(sms) * 8 ? want : uint64_t(sms) * 8;
+    const uint64_t cap = uint64_t(sms) * WF_PREFIX_CTAS;
+    const uint64_t grid = want < cap ? want : cap;
     warp_prefix32_vec_kernel<<<unsigned(grid), 256, 0, s>>>(reinterpret_cast<const uint4 *>(a),
                                                             reinterpret_cast<uint4 *>(out), nvec);
   } else {
