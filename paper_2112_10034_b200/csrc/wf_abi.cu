@@ -625,8 +625,14 @@ namespace {
 // D2H) that no copy in the other direction hides are one small chunk each
 // (3 slots of 85 MiB measured 0.905 of the concurrent-copy ceiling for the
 // 2^28 scan: 8 % of the time was fill + drain)
+#ifndef WF_RING_CHUNK_MB
+#define WF_RING_CHUNK_MB 16
+#endif
+#ifndef WF_RING_SKIP_KERNEL
+#define WF_RING_SKIP_KERNEL 0  // tools-only A/B: the ring's copies without the scan kernel
+#endif
 constexpr int kRing = 8;
-constexpr size_t kRingChunkMax = size_t(16) << 20;
+constexpr size_t kRingChunkMax = size_t(WF_RING_CHUNK_MB) << 20;
 
 int host_ring_checks(const void *host_in, const void *host_out, uint64_t n, void *staging,
                      size_t staging_bytes, size_t min_bytes) {
@@ -679,7 +685,7 @@ int wf_scan_inclusive_i32_host(const int32_t *host_in, int32_t *host_out, uint64
       e = cudaMemcpyAsync(dbuf, host_in + first, cnt * 4, cudaMemcpyHostToDevice, cs->h2d);
     if (e == cudaSuccess) e = cudaEventRecord(cs->landed[k], cs->h2d);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, cs->landed[k], 0);
-    if (e == cudaSuccess) e = launch_scan_i32(dbuf, dbuf, cnt, carry, ws, s);
+    if (e == cudaSuccess && !WF_RING_SKIP_KERNEL) e = launch_scan_i32(dbuf, dbuf, cnt, carry, ws, s);
     if (e == cudaSuccess) e = cudaEventRecord(cs->computed[k], s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(cs->d2h, cs->computed[k], 0);
     if (e == cudaSuccess)
