@@ -42,6 +42,9 @@ N_C5 = 1 << 32
 # only after ~25 launches (606-612 before; tools/bench_loop_probe2.py,
 # profiles/r01_reduce_experiments.md) — 512 is the robust choice.
 BLOCK_C2 = int(os.environ.get("WF_BENCH_BLOCK_C2", "512"))
+# headline steps as programmatic dependent launches (WF_FLAG_INPUT_STABLE);
+# WF_BENCH_PDL=0 measures plain stream-ordered launches for comparison
+PDL_C2 = os.environ.get("WF_BENCH_PDL", "1") != "0"
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 NOMINAL_HBM_GBS = 8000.0   # north_star / BASELINE.md §4: % of peak also vs 8.0 TB/s
 
@@ -423,10 +426,13 @@ def run_ours(args, rank, world, local) -> dict | None:
 
     def step():
         nonlocal launches
+        # consecutive steps read the same input and nothing between them
+        # writes it: each step is a programmatic dependent launch that streams
+        # while the previous step drains (WF_FLAG_INPUT_STABLE; same bits)
         if peer is not None:  # one kernel: local reduce + exchange + fold
-            part = peer.reduce_sum_f32(x, block=BLOCK_C2)
+            part = peer.reduce_sum_f32(x, block=BLOCK_C2, input_stable=PDL_C2)
         else:
-            part = ops.reduce_sum_f32(x, block=BLOCK_C2)
+            part = ops.reduce_sum_f32(x, block=BLOCK_C2, input_stable=PDL_C2)
         launches += 1
         if world > 1 and peer is None:
             ops.fold(wd.exchange(part).reshape(-1))
@@ -538,6 +544,9 @@ def run_ours(args, rank, world, local) -> dict | None:
                         f"{world} B200",
             "exchange": exchange,
             "n": N_C2, "block": BLOCK_C2, "parallelism": f"shard{world}",
+            "launch": ("programmatic dependent launches: each step streams its input while "
+                       "the previous step drains (WF_FLAG_INPUT_STABLE)" if PDL_C2
+                       else "stream-ordered launches"),
             "l2": "inputs larger than L2 (4 GiB vs 126 MB), no flush needed",
         },
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,

@@ -107,6 +107,18 @@ int wf_reduce_sum_i32(const int32_t *in, uint64_t n, int32_t *out, int block,
 int wf_reduce_sum_f32(const float *in, uint64_t n, float *out, int block,
                       int grid, void *ws, size_t ws_bytes, wf_stream_t stream);
 
+/* Launch flags of the *_ex entry points.
+ * WF_FLAG_INPUT_STABLE: the caller promises that the kernel issued just
+ *   before this call on `stream` does not write `in` (e.g. the previous call
+ *   of a loop over the same input, or anything after a stream / event
+ *   synchronisation).  The reduction is then a programmatic dependent launch:
+ *   it streams `in` while that kernel drains and touches `ws` / `out` only
+ *   after it has completed.  Same result bits as without the flag. */
+#define WF_FLAG_INPUT_STABLE 1u
+int wf_reduce_sum_f32_ex(const float *in, uint64_t n, float *out, int block,
+                         int grid, void *ws, size_t ws_bytes, unsigned flags,
+                         wf_stream_t stream);
+
 /* Fixed-order folds of `count` device values (cross-GPU partial combine,
  * SURVEY.md §8e).  out[0] = vals[0] + vals[1] + ... + vals[count-1] in that
  * association order for f32; wrapping for i32. */
@@ -142,6 +154,12 @@ int wf_reduce_sum_f32_mg(const float *in, uint64_t n, float *out, int block,
                          int grid, void *ws, size_t ws_bytes,
                          void *const *d_peers, const void *d_mailbox, int rank,
                          int world, uint32_t epoch, wf_stream_t stream);
+/* ... with launch flags (WF_FLAG_INPUT_STABLE, as wf_reduce_sum_f32_ex) */
+int wf_reduce_sum_f32_mg_ex(const float *in, uint64_t n, float *out, int block,
+                            int grid, void *ws, size_t ws_bytes,
+                            void *const *d_peers, const void *d_mailbox,
+                            int rank, int world, uint32_t epoch,
+                            unsigned flags, wf_stream_t stream);
 
 /* Small collectives over the same kind of peer-memory mailboxes, one
  * single-block kernel per rank (replace NCCL all-gather / all-reduce + fold

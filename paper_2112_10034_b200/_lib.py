@@ -30,6 +30,8 @@ OP_COMPACT_GT0_I32 = 4
 OP_HISTOGRAM256_U8 = 5
 OP_WARP_COLLECTIVE = 6
 
+FLAG_INPUT_STABLE = 1  # WF_FLAG_INPUT_STABLE (include/warpfold_b200.h)
+
 COLL = {"shfl_down": 0, "shfl_up": 1, "shfl_xor": 2, "shfl_idx": 3,
         "vote_all": 4, "vote_any": 5, "ballot": 6, "reduce_add": 7}
 
@@ -49,6 +51,7 @@ SIGNATURES = {
     "wf_shutdown": (None, []),
     "wf_reduce_sum_i32": (C.c_int, [_vp, _u64, _vp, C.c_int, C.c_int, _vp, _sz, _vp]),
     "wf_reduce_sum_f32": (C.c_int, [_vp, _u64, _vp, C.c_int, C.c_int, _vp, _sz, _vp]),
+    "wf_reduce_sum_f32_ex": (C.c_int, [_vp, _u64, _vp, C.c_int, C.c_int, _vp, _sz, C.c_uint, _vp]),
     "wf_fold_f32": (C.c_int, [_vp, _u32, _vp, _vp]),
     "wf_mailbox_bytes": (_sz, [C.c_int]),
     "wf_mailbox_alloc": (C.c_int, [C.c_int, C.POINTER(_vp)]),
@@ -68,6 +71,8 @@ SIGNATURES = {
                                         C.c_int, _u32, _vp, _vp]),
     "wf_reduce_sum_f32_mg": (C.c_int, [_vp, _u64, _vp, C.c_int, C.c_int, _vp, _sz, _vp, _vp,
                                        C.c_int, C.c_int, _u32, _vp]),
+    "wf_reduce_sum_f32_mg_ex": (C.c_int, [_vp, _u64, _vp, C.c_int, C.c_int, _vp, _sz, _vp, _vp,
+                                          C.c_int, C.c_int, _u32, C.c_uint, _vp]),
     "wf_fold_i32": (C.c_int, [_vp, _u32, _vp, _vp]),
     "wf_fold_u64": (C.c_int, [_vp, _u32, _vp, _vp]),
     "wf_scan_inclusive_i32": (C.c_int, [_vp, _vp, _u64, _vp, _vp, _sz, _vp]),

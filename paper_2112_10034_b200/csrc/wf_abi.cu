@@ -239,10 +239,17 @@ int wf_reduce_sum_i32(const int32_t *in, uint64_t n, int32_t *out, int block, in
 
 int wf_reduce_sum_f32(const float *in, uint64_t n, float *out, int block, int grid, void *ws,
                       size_t ws_bytes, wf_stream_t stream) {
+  return wf_reduce_sum_f32_ex(in, n, out, block, grid, ws, ws_bytes, 0u, stream);
+}
+
+int wf_reduce_sum_f32_ex(const float *in, uint64_t n, float *out, int block, int grid, void *ws,
+                         size_t ws_bytes, unsigned flags, wf_stream_t stream) {
+  if (flags & ~unsigned(WF_FLAG_INPUT_STABLE)) return fail(WF_ERR_ARG, "unknown flags 0x%x", flags);
   int rc = reduce_common(WF_OP_REDUCE_SUM_F32, in, n, out, block, grid, ws, ws_bytes);
   if (rc) return rc;
   if (grid == 0) grid = auto_reduce_grid(true, block, n);
-  return cuda_status(launch_reduce_f32(in, n, out, block, grid, ws, static_cast<cudaStream_t>(stream)),
+  return cuda_status(launch_reduce_f32(in, n, out, block, grid, ws, static_cast<cudaStream_t>(stream),
+                                       (flags & WF_FLAG_INPUT_STABLE) != 0),
                      "reduce_sum_f32");
 }
 
@@ -298,6 +305,15 @@ int wf_ipc_close(void *d_ptr) { return cuda_status(cudaIpcCloseMemHandle(d_ptr),
 int wf_reduce_sum_f32_mg(const float *in, uint64_t n, float *out, int block, int grid, void *ws,
                          size_t ws_bytes, void *const *d_peers, const void *d_mailbox, int rank,
                          int world, uint32_t epoch, wf_stream_t stream) {
+  return wf_reduce_sum_f32_mg_ex(in, n, out, block, grid, ws, ws_bytes, d_peers, d_mailbox, rank,
+                                 world, epoch, 0u, stream);
+}
+
+int wf_reduce_sum_f32_mg_ex(const float *in, uint64_t n, float *out, int block, int grid,
+                            void *ws, size_t ws_bytes, void *const *d_peers,
+                            const void *d_mailbox, int rank, int world, uint32_t epoch,
+                            unsigned flags, wf_stream_t stream) {
+  if (flags & ~unsigned(WF_FLAG_INPUT_STABLE)) return fail(WF_ERR_ARG, "unknown flags 0x%x", flags);
   int rc = reduce_common(WF_OP_REDUCE_SUM_F32, in, n, out, block, grid, ws, ws_bytes);
   if (rc) return rc;
   if (d_peers == nullptr || d_mailbox == nullptr) return fail(WF_ERR_ARG, "NULL mailbox pointer");
@@ -306,7 +322,8 @@ int wf_reduce_sum_f32_mg(const float *in, uint64_t n, float *out, int block, int
   if (epoch == 0) return fail(WF_ERR_ARG, "epoch must start at 1");
   if (grid == 0) grid = auto_reduce_grid(true, block, n);
   return cuda_status(launch_reduce_f32_mg(in, n, out, block, grid, ws, d_peers, d_mailbox, rank,
-                                          world, epoch, static_cast<cudaStream_t>(stream)),
+                                          world, epoch, (flags & WF_FLAG_INPUT_STABLE) != 0,
+                                          static_cast<cudaStream_t>(stream)),
                      "reduce_sum_f32_mg");
 }
 

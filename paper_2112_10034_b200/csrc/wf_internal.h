@@ -72,12 +72,15 @@ struct DeviceMask {
 cudaError_t launch_reduce_i32(const int32_t *in, uint64_t n, int32_t *out,
                               int block, int grid, void *ws,
                               cudaStream_t s);
+// early: programmatic dependent launch on the caller's WF_FLAG_INPUT_STABLE
+// promise (wf_reduce.cu)
 cudaError_t launch_reduce_f32(const float *in, uint64_t n, float *out,
-                              int block, int grid, void *ws, cudaStream_t s);
+                              int block, int grid, void *ws, cudaStream_t s,
+                              bool early = false);
 int auto_reduce_grid(bool is_f32, int block, uint64_t n);
 cudaError_t launch_reduce_f32_mg(const float *in, uint64_t n, float *out, int block, int grid,
                                  void *ws, void *const *peers, const void *mine, int rank,
-                                 int world, uint32_t epoch, cudaStream_t s);
+                                 int world, uint32_t epoch, bool early, cudaStream_t s);
 cudaError_t launch_reduce_i32_exscan_mg(const int32_t *in, uint64_t n, int32_t *out2, int block,
                                         int grid, void *ws, void *const *peers, const void *mine,
                                         uint32_t cap, int rank, int world, uint32_t epoch,

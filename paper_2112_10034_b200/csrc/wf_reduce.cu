@@ -22,15 +22,38 @@
 #include "wf_internal.h"
 #include "wf_peer.cuh"
 
-#ifndef WF_RED_PDL
-#define WF_RED_PDL 0  // programmatic dependent launch between consecutive K2 launches
-#endif
-#ifndef WF_RED_PDL_EARLY
-#define WF_RED_PDL_EARLY 0  // 1: wait only before touching ws/out (unsafe if the
-                            // previous kernel in the stream produced `in`)
+// Programmatic dependent launch (PDL).  Every reduce kernel signals
+// `griddepcontrol.launch_dependents` as it starts, so a dependent launch may
+// get its CTAs going on SMs this grid no longer needs.  Only EARLY launches
+// (the caller's WF_FLAG_INPUT_STABLE promise: the kernel issued just before
+// on the stream does not write `in`) are dependent launches: they stream
+// their input while the previous grid drains (its last CTAs, its partial
+// fold, the kernel boundary: ~6 us per launch, tools/red_trace.py) and wait
+// for it (`griddepcontrol.wait`: completed and flushed) before touching the
+// workspace or the output.  Without the flag the launch is stream-ordered as
+// usual.
+
+#ifndef WF_RED_TRACE
+#define WF_RED_TRACE 0  // tools-only: per-block globaltimer stamps (tools/red_trace.py)
 #endif
 
 namespace wf {
+#if WF_RED_TRACE
+// per block: [0] start, [1] streaming done (block sum formed), [2] SM id;
+// [4 * grid]: the last block's fold done.  Launch number g_red_seq (bumped by
+// the last block) stamps record g_red_seq of stride 4 * 16384 + 8 words.
+__device__ unsigned long long *g_red_trace = nullptr;
+__device__ unsigned int g_red_seq = 0;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define RED_STAMP(k, v) \
+  if (g_red_trace) g_red_trace[uint64_t(*(volatile unsigned *)&g_red_seq) * (4 * 16384 + 8) + (k)] = (v)
+#else
+#define RED_STAMP(k, v)
+#endif
 namespace {
 
 struct SumI32 {
@@ -119,7 +142,7 @@ __device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long
 // the rank total (exclusive scan over ranks, mod 2^32), so out = {carry of
 // this rank's shard, global total} — the sharded scan's pass 1 and its carry
 // exchange in ONE kernel (wf_reduce_sum_i32_exscan_mg).
-template <class Op, int BLOCK, int UNROLL, bool MG = false, bool PX = false>
+template <class Op, int BLOCK, int UNROLL, bool MG = false, bool PX = false, bool EARLY = false>
 __global__ void __launch_bounds__(BLOCK)
     reduce_kernel(const typename Op::elem_t *__restrict__ in, uint64_t n,
                   typename Op::elem_t *__restrict__ out,
@@ -130,16 +153,16 @@ __global__ void __launch_bounds__(BLOCK)
   using elem_t = typename Op::elem_t;
   const uint64_t gtid = uint64_t(blockIdx.x) * BLOCK + threadIdx.x;
   const uint64_t nthreads = uint64_t(gridDim.x) * BLOCK;
-#if WF_RED_PDL
-  // let the next launch in the stream get its CTAs resident while this grid's
-  // tail (last CTAs, partial fold) finishes
+#if WF_RED_TRACE
+  if (threadIdx.x == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    RED_STAMP(blockIdx.x * 4ull, gtimer());
+    RED_STAMP(blockIdx.x * 4ull + 2, smid);
+  }
+#endif
+  // a dependent (EARLY) launch behind this one may start its streaming now
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-#if !WF_RED_PDL_EARLY
-  // ... but touch nothing before every earlier grid in the stream (e.g. the
-  // producer of `in`) has completed and flushed
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-#endif
-#endif
 
   // head (scalar until 16 B alignment) | body (16 B vectors) | tail (scalar)
   const uintptr_t addr = reinterpret_cast<uintptr_t>(in);
@@ -205,10 +228,14 @@ __global__ void __launch_bounds__(BLOCK)
     for (int u = 0; u + s < UNROLL; u += 2 * s) acc[u][0] = Op::add(acc[u][0], acc[u + s][0]);
 
   const acc_t bsum = block_sum<Op, BLOCK>(acc[0][0]);
-#if WF_RED_PDL && WF_RED_PDL_EARLY
-  // early variant: the streaming above overlapped the previous grid's tail
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+#if WF_RED_TRACE
+  if (threadIdx.x == 0) RED_STAMP(blockIdx.x * 4ull + 1, gtimer());
 #endif
+  if constexpr (EARLY) {
+    // the streaming above overlapped the previous grid's tail; the workspace
+    // and the output are touched only once that grid has completed and flushed
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
 
   if constexpr (PX) {
     __shared__ bool s_last;
@@ -290,6 +317,10 @@ __global__ void __launch_bounds__(BLOCK)
   if (threadIdx.x == 0) {
     out[0] = Op::to_elem(f);
     *ticket = 0u;
+#if WF_RED_TRACE
+    RED_STAMP(gridDim.x * 4ull, gtimer());
+    g_red_seq += 1;
+#endif
   }
 }
 
@@ -325,41 +356,45 @@ __global__ void __launch_bounds__(256)
 #endif
 constexpr int kUnroll = WF_RED_UNROLL;
 
-template <class Op, int BLOCK>
-cudaError_t launch_block(const typename Op::elem_t *in, uint64_t n,
-                         typename Op::elem_t *out, int grid, void *ws,
-                         cudaStream_t s) {
-  auto *ticket = reinterpret_cast<uint32_t *>(ws);
-  auto *partials = reinterpret_cast<typename Op::acc_t *>(
-      static_cast<char *>(ws) + kWsHeader);
-#if WF_RED_PDL
+// EARLY: a programmatic dependent launch (see the top of this file)
+template <class Kernel, class... Args>
+cudaError_t launch_pdl(Kernel k, int grid, int block, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(BLOCK);
+  cfg.blockDim = dim3(block);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, reduce_kernel<Op, BLOCK, kUnroll, false>, in, n, out, partials,
-                            ticket, MgArgs{}, PeerArgs{});
-#else
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+template <class Op, int BLOCK>
+cudaError_t launch_block(const typename Op::elem_t *in, uint64_t n,
+                         typename Op::elem_t *out, int grid, void *ws, bool early,
+                         cudaStream_t s) {
+  auto *ticket = reinterpret_cast<uint32_t *>(ws);
+  auto *partials = reinterpret_cast<typename Op::acc_t *>(
+      static_cast<char *>(ws) + kWsHeader);
+  if (early)
+    return launch_pdl(reduce_kernel<Op, BLOCK, kUnroll, false, false, true>, grid, BLOCK, s, in,
+                      n, out, partials, ticket, MgArgs{}, PeerArgs{});
   reduce_kernel<Op, BLOCK, kUnroll>
       <<<grid, BLOCK, 0, s>>>(in, n, out, partials, ticket);
   return cudaGetLastError();
-#endif
 }
 
 template <class Op>
 cudaError_t launch_reduce(const typename Op::elem_t *in, uint64_t n,
                           typename Op::elem_t *out, int block, int grid,
-                          void *ws, cudaStream_t s) {
+                          void *ws, bool early, cudaStream_t s) {
   switch (block) {
-    case 128: return launch_block<Op, 128>(in, n, out, grid, ws, s);
-    case 256: return launch_block<Op, 256>(in, n, out, grid, ws, s);
-    case 512: return launch_block<Op, 512>(in, n, out, grid, ws, s);
-    case 1024: return launch_block<Op, 1024>(in, n, out, grid, ws, s);
+    case 128: return launch_block<Op, 128>(in, n, out, grid, ws, early, s);
+    case 256: return launch_block<Op, 256>(in, n, out, grid, ws, early, s);
+    case 512: return launch_block<Op, 512>(in, n, out, grid, ws, early, s);
+    case 1024: return launch_block<Op, 1024>(in, n, out, grid, ws, early, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -384,9 +419,12 @@ int resident_blocks(int block) {
 
 template <int BLOCK>
 cudaError_t launch_mg_block(const float *in, uint64_t n, float *out, int grid, void *ws,
-                            const MgArgs &mg, cudaStream_t s) {
+                            const MgArgs &mg, bool early, cudaStream_t s) {
   auto *ticket = reinterpret_cast<uint32_t *>(ws);
   auto *partials = reinterpret_cast<float *>(static_cast<char *>(ws) + kWsHeader);
+  if (early)
+    return launch_pdl(reduce_kernel<SumF32, BLOCK, kUnroll, true, false, true>, grid, BLOCK, s,
+                      in, n, out, partials, ticket, mg, PeerArgs{});
   reduce_kernel<SumF32, BLOCK, kUnroll, true><<<grid, BLOCK, 0, s>>>(in, n, out, partials,
                                                                      ticket, mg);
   return cudaGetLastError();
@@ -403,6 +441,16 @@ cudaError_t launch_px_block(const int32_t *in, uint64_t n, int32_t *out2, int gr
 }
 
 }  // namespace
+
+#if WF_RED_TRACE
+extern "C" int wf_debug_set_trace_red(void *buf) {
+  unsigned long long *p = static_cast<unsigned long long *>(buf);
+  unsigned int z = 0;
+  cudaError_t e = cudaMemcpyToSymbol(g_red_trace, &p, sizeof(p));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_red_seq, &z, sizeof(z));
+  return int(e);
+}
+#endif
 
 cudaError_t launch_reduce_i32_exscan_mg(const int32_t *in, uint64_t n, int32_t *out2, int block,
                                         int grid, void *ws, void *const *peers, const void *mine,
@@ -421,7 +469,7 @@ cudaError_t launch_reduce_i32_exscan_mg(const int32_t *in, uint64_t n, int32_t *
 
 cudaError_t launch_reduce_f32_mg(const float *in, uint64_t n, float *out, int block, int grid,
                                  void *ws, void *const *peers, const void *mine, int rank,
-                                 int world, uint32_t epoch, cudaStream_t s) {
+                                 int world, uint32_t epoch, bool early, cudaStream_t s) {
   MgArgs mg;
   mg.peers = reinterpret_cast<unsigned long long *const *>(peers);
   mg.mine = static_cast<const unsigned long long *>(mine);
@@ -429,10 +477,10 @@ cudaError_t launch_reduce_f32_mg(const float *in, uint64_t n, float *out, int bl
   mg.world = world;
   mg.epoch = epoch;
   switch (block) {
-    case 128: return launch_mg_block<128>(in, n, out, grid, ws, mg, s);
-    case 256: return launch_mg_block<256>(in, n, out, grid, ws, mg, s);
-    case 512: return launch_mg_block<512>(in, n, out, grid, ws, mg, s);
-    case 1024: return launch_mg_block<1024>(in, n, out, grid, ws, mg, s);
+    case 128: return launch_mg_block<128>(in, n, out, grid, ws, mg, early, s);
+    case 256: return launch_mg_block<256>(in, n, out, grid, ws, mg, early, s);
+    case 512: return launch_mg_block<512>(in, n, out, grid, ws, mg, early, s);
+    case 1024: return launch_mg_block<1024>(in, n, out, grid, ws, mg, early, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -454,12 +502,12 @@ int auto_reduce_grid(bool is_f32, int block, uint64_t n) {
 
 cudaError_t launch_reduce_i32(const int32_t *in, uint64_t n, int32_t *out,
                               int block, int grid, void *ws, cudaStream_t s) {
-  return launch_reduce<SumI32>(in, n, out, block, grid, ws, s);
+  return launch_reduce<SumI32>(in, n, out, block, grid, ws, false, s);
 }
 
 cudaError_t launch_reduce_f32(const float *in, uint64_t n, float *out,
-                              int block, int grid, void *ws, cudaStream_t s) {
-  return launch_reduce<SumF32>(in, n, out, block, grid, ws, s);
+                              int block, int grid, void *ws, cudaStream_t s, bool early) {
+  return launch_reduce<SumF32>(in, n, out, block, grid, ws, early, s);
 }
 
 cudaError_t launch_fold_f32(const float *v, uint32_t count, float *out,

@@ -110,8 +110,14 @@ def reduce_sum_i32(x: torch.Tensor, out: torch.Tensor | None = None, block: int 
 
 
 def reduce_sum_f32(x: torch.Tensor, out: torch.Tensor | None = None, block: int = 256,
-                   grid: int = 0) -> torch.Tensor:
-    """fp32 sum of ``x`` into ``out[0]`` with a fixed association order (K2)."""
+                   grid: int = 0, input_stable: bool = False) -> torch.Tensor:
+    """fp32 sum of ``x`` into ``out[0]`` with a fixed association order (K2).
+
+    ``input_stable=True`` is the caller's promise that the kernel issued just
+    before on the current stream does not write ``x`` (e.g. the previous call
+    of a loop over the same input): the launch then overlaps that kernel's
+    tail (``WF_FLAG_INPUT_STABLE``, programmatic dependent launch).  Same
+    result bits either way."""
     _require_cuda(x, torch.float32, "x")
     _check_block(block)
     if out is None:
@@ -119,8 +125,10 @@ def reduce_sum_f32(x: torch.Tensor, out: torch.Tensor | None = None, block: int 
     _require_cuda(out, torch.float32, "out")
     with _on(x.device):
         ws = workspace(_lib.OP_REDUCE_SUM_F32, x.numel(), x.device)
-        check(_lib.load().wf_reduce_sum_f32(x.data_ptr(), x.numel(), out.data_ptr(), block, grid,
-                                            ws.data_ptr(), ws.numel(), _stream_handle()),
+        check(_lib.load().wf_reduce_sum_f32_ex(x.data_ptr(), x.numel(), out.data_ptr(), block,
+                                               grid, ws.data_ptr(), ws.numel(),
+                                               _lib.FLAG_INPUT_STABLE if input_stable else 0,
+                                               _stream_handle()),
               "reduce_sum_f32")
     return out
 

@@ -127,18 +127,20 @@ class PeerReducer:
         return cls(boxes, dist.get_rank(group), dist.get_world_size(group))
 
     def reduce_sum_f32(self, x_local: torch.Tensor, out: torch.Tensor | None = None,
-                       block: int = 256, stream=None) -> torch.Tensor:
+                       block: int = 256, stream=None, input_stable: bool = False) -> torch.Tensor:
+        """``input_stable``: as ``ops.reduce_sum_f32`` (WF_FLAG_INPUT_STABLE)."""
         ops._require_cuda(x_local, torch.float32, "x")
         if out is None:
             out = torch.empty(1, dtype=torch.float32, device=x_local.device)
         self.epoch += 1
         ws = ops.workspace(_lib.OP_REDUCE_SUM_F32, x_local.numel(), x_local.device, stream)
         lib = _lib.load()
-        _check(lib.wf_reduce_sum_f32_mg(x_local.data_ptr(), x_local.numel(), out.data_ptr(),
-                                        block, 0, ws.data_ptr(), ws.numel(),
-                                        self.boxes.peers.data_ptr(), self.boxes.own,
-                                        self.rank, self.world, self.epoch,
-                                        ops._stream_handle(stream)),
+        _check(lib.wf_reduce_sum_f32_mg_ex(x_local.data_ptr(), x_local.numel(), out.data_ptr(),
+                                           block, 0, ws.data_ptr(), ws.numel(),
+                                           self.boxes.peers.data_ptr(), self.boxes.own,
+                                           self.rank, self.world, self.epoch,
+                                           _lib.FLAG_INPUT_STABLE if input_stable else 0,
+                                           ops._stream_handle(stream)),
                "wf_reduce_sum_f32_mg")
         return out
 

@@ -61,6 +61,30 @@ def test_fused_exchange_in_process(mods, world):
         boxes[0].close()
 
 
+def test_fused_exchange_input_stable_chain(mods):
+    """wf_reduce_sum_f32_mg_ex with WF_FLAG_INPUT_STABLE (what bench.py's
+    headline steps use at N>1): a back-to-back chain of dependent launches on
+    one mailbox, epochs alternating banks, every result bit-identical to the
+    plain fused launch (world 1: own mailbox only; ranks sharing one GPU are
+    not chained, they would compete for SM slots with their own successors)."""
+    ops, p2p, wd = mods
+    dev = torch.device("cuda", 0)
+    x = ops.fill_synthetic("f32_unit", (1 << 23) + 77, seed=3)
+    boxes = p2p.Mailboxes.local(1, dev)
+    try:
+        pr = p2p.PeerReducer(boxes[0], 0, 1)
+        want = pr.reduce_sum_f32(x).clone()
+        torch.cuda.synchronize()
+        outs = torch.empty(12, dtype=torch.float32, device=dev)
+        for k in range(12):
+            pr.reduce_sum_f32(x, outs[k:k + 1], input_stable=True)
+        torch.cuda.synchronize()
+        assert torch.equal(outs.view(torch.int32), want.view(torch.int32).expand(12))
+    finally:
+        torch.cuda.synchronize()
+        boxes[0].close()
+
+
 def _child_read_mailbox(handle: bytes, world: int, q) -> None:
     import ctypes as C
     import torch as T

@@ -128,6 +128,50 @@ def test_reduce_f32_full_config(ops, block):
     del x
 
 
+@pytest.mark.parametrize("block", [256, 512, 1024])
+def test_reduce_f32_input_stable_launches(ops, block):
+    """WF_FLAG_INPUT_STABLE (programmatic dependent launch): a chain of
+    back-to-back launches, each streaming while the previous one drains, over
+    several inputs, each result into its own output — every one bit-identical
+    to the plain launch.  The workspace is shared by the whole chain, so a
+    dependent launch that touched it before its predecessor finished would
+    corrupt the folds."""
+    n = (1 << 24) + 5
+    xs = [ops.fill_synthetic("f32_unit", n, seed=s) for s in range(3)]
+    want = [host(ops.reduce_sum_f32(x, block=block)).view(np.int32)[0] for x in xs]
+    outs = torch.empty(30, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    for k in range(30):
+        ops.reduce_sum_f32(xs[k % 3], outs[k:k + 1], block=block, input_stable=True)
+    got = host(outs).view(np.int32)
+    assert [int(v) for v in got] == [int(want[k % 3]) for k in range(30)]
+
+
+def test_reduce_f32_input_stable_after_a_writer_and_sync(ops):
+    """The promise covers the kernel issued just before: after a synchronise,
+    a writer of the input followed by a plain launch then flagged launches,
+    the flagged results follow the new data."""
+    n = 1 << 22
+    x = ops.fill_synthetic("f32_unit", n, seed=1)
+    torch.cuda.synchronize()
+    a = host(ops.reduce_sum_f32(x, input_stable=True)).view(np.int32)[0]
+    ops.fill_synthetic("f32_unit", n, seed=2, out=x)  # writes x
+    ops.reduce_sum_f32(x)  # plain launch after the writer
+    b = host(ops.reduce_sum_f32(x, input_stable=True)).view(np.int32)[0]
+    want_a = host(ops.reduce_sum_f32(ops.fill_synthetic("f32_unit", n, seed=1))).view(np.int32)[0]
+    want_b = host(ops.reduce_sum_f32(ops.fill_synthetic("f32_unit", n, seed=2))).view(np.int32)[0]
+    assert (a, b) == (want_a, want_b)
+
+
+def test_reduce_f32_ex_rejects_unknown_flags(ops):
+    from paper_2112_10034_b200 import _lib
+    x = torch.zeros(16, dtype=torch.float32, device="cuda")
+    out = torch.empty(1, dtype=torch.float32, device="cuda")
+    rc = _lib.load().wf_reduce_sum_f32_ex(x.data_ptr(), 16, out.data_ptr(), 256, 0, None, 0, 6,
+                                          None)
+    assert rc == _lib.WF_ERR_ARG and b"flags" in _lib.load().wf_last_error()
+
+
 # ---- K3 ----------------------------------------------------------------------
 
 @pytest.mark.parametrize("n", SIZES)
