@@ -370,6 +370,7 @@ def time_launches(fn, steps: int, warmup: int, flush=None):
     is returned for each; with a flush (C1) every launch is bracketed by its
     own events right after the L2 flush."""
     import torch
+    torch.cuda.synchronize()  # whatever wrote the inputs has finished (WF_FLAG_INPUT_STABLE)
     for _ in range(warmup):
         if flush is not None:
             flush()
@@ -824,16 +825,17 @@ def per_kernel(args, rank, world, local, dev, peak, checks: dict) -> dict:
     # C5 histogram
     lo, hi = wd.shard_range(N_C5, rank, world)
     u = ops.fill_synthetic("u8_uniform", hi - lo, seed=0, base=lo, device=dev)
-    t = time_launches(lambda: wd.histogram256_u8(u, peer=pc), steps, warm)
+    t = time_launches(lambda: wd.histogram256_u8(u, peer=pc, input_stable=PDL_C2), steps, warm)
     res["c5_hist_u8"] = stats(t, hi - lo, 1, N_C5)
-    checks["c5_hist_u8"] = check_c5(wd.histogram256_u8(u, peer=pc), u, world)
+    checks["c5_hist_u8"] = check_c5(wd.histogram256_u8(u, peer=pc, input_stable=PDL_C2), u, world)
     # also all-same-value and skewed (geometric) bytes
     variants = {}
     for gen in ("u8_const", "u8_geom"):
         ops.fill_synthetic(gen, hi - lo, seed=0, base=lo, out=u)
-        t = time_launches(lambda: wd.histogram256_u8(u, peer=pc), steps, warm)
+        t = time_launches(lambda: wd.histogram256_u8(u, peer=pc, input_stable=PDL_C2), steps, warm)
         ms = statistics.mean(t)
-        checks[f"c5_hist_u8/{gen}"] = check_c5(wd.histogram256_u8(u, peer=pc), u, world)
+        checks[f"c5_hist_u8/{gen}"] = check_c5(
+            wd.histogram256_u8(u, peer=pc, input_stable=PDL_C2), u, world)
         variants[gen] = {"kernel_us": round(ms * 1e3, 2),
                          "gbs": round((hi - lo) / (ms * 1e-3) / 1e9, 1),
                          "gelem_s": round(N_C5 / (max_over_ranks(ms, world) * 1e-3) / 1e9, 3)}

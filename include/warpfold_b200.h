@@ -205,6 +205,12 @@ int wf_histogram256_u8_mg(const uint8_t *in, uint64_t n, uint64_t *d_bins,
                           const void *d_mailbox, uint32_t cap, int rank,
                           int world, uint32_t epoch, uint32_t *d_err,
                           wf_stream_t stream);
+/* ... with launch flags (WF_FLAG_INPUT_STABLE, as wf_reduce_sum_f32_ex) */
+int wf_histogram256_u8_mg_ex(const uint8_t *in, uint64_t n, uint64_t *d_bins,
+                             void *ws, size_t ws_bytes, void *const *d_peers,
+                             const void *d_mailbox, uint32_t cap, int rank,
+                             int world, uint32_t epoch, uint32_t *d_err,
+                             unsigned flags, wf_stream_t stream);
 int wf_peer_mailbox_alloc(int world, uint32_t cap, void **d_mailbox);
 int wf_peer_exchange(int mode, const void *d_vals, uint32_t count, uint32_t cap,
                      void *d_out, void *const *d_peers, const void *d_mailbox,
@@ -262,6 +268,11 @@ int wf_compact_gt0_i32(const int32_t *in, uint64_t n, int32_t *out,
  * bins[b] = #{i : in[i] == b} as uint64 (overwrites bins). */
 int wf_histogram256_u8(const uint8_t *in, uint64_t n, uint64_t *bins, int grid,
                        void *ws, size_t ws_bytes, wf_stream_t stream);
+/* ... with launch flags (WF_FLAG_INPUT_STABLE, as wf_reduce_sum_f32_ex: the
+ * counting overlaps the previous kernel's drain) */
+int wf_histogram256_u8_ex(const uint8_t *in, uint64_t n, uint64_t *bins, int grid,
+                          void *ws, size_t ws_bytes, unsigned flags,
+                          wf_stream_t stream);
 
 /* ---- P: warp collectives with reference semantics ----------------------
  * Runs n_threads logical threads as blocks of `block` threads (the last warp

@@ -391,6 +391,15 @@ int wf_histogram256_u8_mg(const uint8_t *in, uint64_t n, uint64_t *d_bins, void 
                           size_t ws_bytes, void *const *d_peers, const void *d_mailbox,
                           uint32_t cap, int rank, int world, uint32_t epoch, uint32_t *d_err,
                           wf_stream_t stream) {
+  return wf_histogram256_u8_mg_ex(in, n, d_bins, ws, ws_bytes, d_peers, d_mailbox, cap, rank,
+                                  world, epoch, d_err, 0u, stream);
+}
+
+int wf_histogram256_u8_mg_ex(const uint8_t *in, uint64_t n, uint64_t *d_bins, void *ws,
+                             size_t ws_bytes, void *const *d_peers, const void *d_mailbox,
+                             uint32_t cap, int rank, int world, uint32_t epoch, uint32_t *d_err,
+                             unsigned flags, wf_stream_t stream) {
+  if (flags & ~unsigned(WF_FLAG_INPUT_STABLE)) return fail(WF_ERR_ARG, "unknown flags 0x%x", flags);
   if (d_bins == nullptr) return fail(WF_ERR_ARG, "bins pointer is NULL");
   if (n && in == nullptr) return fail(WF_ERR_ARG, "input pointer is NULL");
   int rc = check_ws(WF_OP_HISTOGRAM256_U8, n, ws, ws_bytes);
@@ -399,7 +408,8 @@ int wf_histogram256_u8_mg(const uint8_t *in, uint64_t n, uint64_t *d_bins, void 
   if (rc) return rc;
   return cuda_status(launch_hist256_mg(in, n, d_bins, auto_hist_grid(n), ws, d_peers, d_mailbox,
                                        cap, rank, world, epoch, d_err,
-                                       static_cast<cudaStream_t>(stream)),
+                                       static_cast<cudaStream_t>(stream),
+                                       (flags & WF_FLAG_INPUT_STABLE) != 0),
                      "histogram256_u8_mg");
 }
 
@@ -468,6 +478,12 @@ int wf_compact_gt0_i32(const int32_t *in, uint64_t n, int32_t *out, uint64_t *d_
 
 int wf_histogram256_u8(const uint8_t *in, uint64_t n, uint64_t *bins, int grid, void *ws,
                        size_t ws_bytes, wf_stream_t stream) {
+  return wf_histogram256_u8_ex(in, n, bins, grid, ws, ws_bytes, 0u, stream);
+}
+
+int wf_histogram256_u8_ex(const uint8_t *in, uint64_t n, uint64_t *bins, int grid, void *ws,
+                          size_t ws_bytes, unsigned flags, wf_stream_t stream) {
+  if (flags & ~unsigned(WF_FLAG_INPUT_STABLE)) return fail(WF_ERR_ARG, "unknown flags 0x%x", flags);
   if (bins == nullptr) return fail(WF_ERR_ARG, "bins pointer is NULL");
   if (n > 0 && in == nullptr) return fail(WF_ERR_ARG, "input pointer is NULL");
   if (grid < 0) return fail(WF_ERR_CONFIG, "grid size must be >= 0, got %d", grid);
@@ -476,7 +492,8 @@ int wf_histogram256_u8(const uint8_t *in, uint64_t n, uint64_t *bins, int grid, 
   if (grid == 0) grid = auto_hist_grid(n);
   if (grid < min_hist_grid(n)) grid = min_hist_grid(n);  // u32 lane counters stay < 2^32
   return cuda_status(
-      launch_hist256(in, n, bins, false, grid, ws, static_cast<cudaStream_t>(stream)),
+      launch_hist256(in, n, bins, false, grid, ws, static_cast<cudaStream_t>(stream),
+                     (flags & WF_FLAG_INPUT_STABLE) != 0),
       "histogram256_u8");
 }
 

@@ -66,12 +66,18 @@ __device__ __forceinline__ void count_word(uint32_t *col, uint32_t w) {
 // PX: the last block runs the peer all-reduce of wf_peer.cuh on the rank's
 // 256 bins, so `bins` receives the sum over all ranks — the sharded
 // histogram and its bin exchange in ONE kernel (wf_histogram256_u8_mg).
-template <bool PX>
+//
+// EARLY (the caller's WF_FLAG_INPUT_STABLE promise; a programmatic dependent
+// launch, as K2 in wf_reduce.cu): the counting overlaps the previous grid's
+// drain, and `griddepcontrol.wait` precedes the first workspace access.
+template <bool PX, bool EARLY = false>
 __global__ void __launch_bounds__(BLOCK, 2048 / BLOCK)
     hist256_kernel(const uint8_t *__restrict__ in, uint64_t n,
                    unsigned long long *__restrict__ bins, bool accumulate,
                    unsigned long long *__restrict__ accum,
                    uint32_t *__restrict__ ticket, PeerArgs pa) {
+  // a dependent (EARLY) launch behind this one may start counting now
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ uint32_t sh[];  // [256][kBinWords], lane l counts in word l
   for (uint32_t i = threadIdx.x; i < 256 * kBinWords; i += BLOCK) sh[i] = 0u;
   __syncthreads();
@@ -120,6 +126,9 @@ __global__ void __launch_bounds__(BLOCK, 2048 / BLOCK)
 #undef WF_CNT4
 #undef WF_CNT1
   __syncthreads();
+  // EARLY: the counting overlapped the previous grid's drain; the workspace
+  // (accumulators, ticket) and the bins only once it has completed
+  if constexpr (EARLY) asm volatile("griddepcontrol.wait;" ::: "memory");
 
   // fold the 32 lane columns of each bin; rotation keeps the reads of a warp
   // on 32 distinct banks.  The fold is 64-bit: one block may count >= 2^32
@@ -182,43 +191,70 @@ int auto_hist_grid(uint64_t n) {
 static void configure_hist(bool px) {
   static DeviceMask configured[2];
   configured[px].ensure([px] {
-    if (px)
+    if (px) {
       cudaFuncSetAttribute(hist256_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(kHistSmem));
-    else
+      cudaFuncSetAttribute(hist256_kernel<true, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(kHistSmem));
+    } else {
       cudaFuncSetAttribute(hist256_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(kHistSmem));
+      cudaFuncSetAttribute(hist256_kernel<false, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(kHistSmem));
+    }
   });
+}
+
+template <class Kernel, class... Args>
+cudaError_t launch_hist_kernel(Kernel k, bool early, int grid, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(BLOCK);
+  cfg.dynamicSmemBytes = kHistSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = early ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
 cudaError_t launch_hist256(const uint8_t *in, uint64_t n, uint64_t *bins,
                            bool accumulate, int grid, void *ws,
-                           cudaStream_t s) {
+                           cudaStream_t s, bool early) {
   auto *ticket = reinterpret_cast<uint32_t *>(ws);
   auto *accum = reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + kWsHeader);
   configure_hist(false);
-  hist256_kernel<false><<<grid, BLOCK, kHistSmem, s>>>(
-      in, n, reinterpret_cast<unsigned long long *>(bins), accumulate, accum, ticket, PeerArgs{});
-  return cudaGetLastError();
+  auto *b = reinterpret_cast<unsigned long long *>(bins);
+  return early ? launch_hist_kernel(hist256_kernel<false, true>, true, grid, s, in, n, b,
+                                    accumulate, accum, ticket, PeerArgs{})
+               : launch_hist_kernel(hist256_kernel<false>, false, grid, s, in, n, b, accumulate,
+                                    accum, ticket, PeerArgs{});
 }
 
 cudaError_t launch_hist256_mg(const uint8_t *in, uint64_t n, uint64_t *bins, int grid, void *ws,
                               void *const *peers, const void *mine, uint32_t cap, int rank,
-                              int world, uint32_t epoch, uint32_t *err, cudaStream_t s) {
+                              int world, uint32_t epoch, uint32_t *err, cudaStream_t s,
+                              bool early) {
   auto *ticket = reinterpret_cast<uint32_t *>(ws);
   auto *accum = reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + kWsHeader);
   configure_hist(true);
   PeerArgs pa{reinterpret_cast<uint64_t *const *>(peers), static_cast<const uint64_t *>(mine),
               cap, rank, world, epoch, err};
-  hist256_kernel<true><<<grid, BLOCK, kHistSmem, s>>>(
-      in, n, reinterpret_cast<unsigned long long *>(bins), false, accum, ticket, pa);
-  return cudaGetLastError();
+  auto *b = reinterpret_cast<unsigned long long *>(bins);
+  return early ? launch_hist_kernel(hist256_kernel<true, true>, true, grid, s, in, n, b, false,
+                                    accum, ticket, pa)
+               : launch_hist_kernel(hist256_kernel<true>, false, grid, s, in, n, b, false, accum,
+                                    ticket, pa);
 }
 
 cudaError_t preload_hist_mg_kernels() {
   configure_hist(true);
   cudaFuncAttributes a;
-  return cudaFuncGetAttributes(&a, hist256_kernel<true>);
+  cudaError_t e = cudaFuncGetAttributes(&a, hist256_kernel<true>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, hist256_kernel<true, true>);
+  return e;
 }
 
 }  // namespace wf

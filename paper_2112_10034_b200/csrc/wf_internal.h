@@ -87,7 +87,8 @@ cudaError_t launch_reduce_i32_exscan_mg(const int32_t *in, uint64_t n, int32_t *
                                         uint32_t *err, cudaStream_t s);
 cudaError_t launch_hist256_mg(const uint8_t *in, uint64_t n, uint64_t *bins, int grid, void *ws,
                               void *const *peers, const void *mine, uint32_t cap, int rank,
-                              int world, uint32_t epoch, uint32_t *err, cudaStream_t s);
+                              int world, uint32_t epoch, uint32_t *err, cudaStream_t s,
+                              bool early = false);
 size_t peer_mailbox_bytes(int world, uint32_t count);
 cudaError_t launch_peer_exchange(int mode, const void *vals, uint32_t count, uint32_t cap,
                                  void *out, void *const *peers, const void *mine, int rank,
@@ -141,7 +142,7 @@ cudaError_t launch_compact2p_i32(const int32_t *in, uint64_t n, int32_t *out,
 // histogram (wf_hist.cu)
 cudaError_t launch_hist256(const uint8_t *in, uint64_t n, uint64_t *bins,
                            bool accumulate, int grid, void *ws,
-                           cudaStream_t s);
+                           cudaStream_t s, bool early = false);
 int auto_hist_grid(uint64_t n);
 int min_hist_grid(uint64_t n);  // counter-overflow floor for a caller's grid
 

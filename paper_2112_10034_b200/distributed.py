@@ -117,11 +117,14 @@ def compact_gt0_i32(x_local: torch.Tensor, out: torch.Tensor | None = None, grou
     return out, count, offset, total
 
 
-def histogram256_u8(x_local: torch.Tensor, group=None, peer=None) -> torch.Tensor:
+def histogram256_u8(x_local: torch.Tensor, group=None, peer=None,
+                    input_stable: bool = False) -> torch.Tensor:
+    """`input_stable`: WF_FLAG_INPUT_STABLE (the kernel issued just before on
+    the stream does not write `x_local`)."""
     rank, world = _world(group)
     if world > 1 and peer is not None:  # histogram + bin all-reduce in one kernel
-        return peer.histogram256_u8(x_local)
-    bins = ops.histogram256_u8(x_local)
+        return peer.histogram256_u8(x_local, input_stable=input_stable)
+    bins = ops.histogram256_u8(x_local, input_stable=input_stable)
     if world > 1:
         dist.all_reduce(bins, op=dist.ReduceOp.SUM, group=group)
     return bins

@@ -198,8 +198,9 @@ def compact_gt0_i32(x: torch.Tensor, out: torch.Tensor | None = None,
 
 
 def histogram256_u8(x: torch.Tensor, bins: torch.Tensor | None = None,
-                    grid: int = 0) -> torch.Tensor:
-    """256-bin byte histogram (K5) as a device int64[256] (== uint64 bits)."""
+                    grid: int = 0, input_stable: bool = False) -> torch.Tensor:
+    """256-bin byte histogram (K5) as a device int64[256] (== uint64 bits).
+    ``input_stable``: as ``reduce_sum_f32`` (WF_FLAG_INPUT_STABLE)."""
     _require_cuda(x, torch.uint8, "x")
     if bins is None:
         bins = torch.empty(256, dtype=torch.int64, device=x.device)
@@ -208,8 +209,10 @@ def histogram256_u8(x: torch.Tensor, bins: torch.Tensor | None = None,
         raise LaunchError("bins must hold 256 counters")
     with _on(x.device):
         ws = workspace(_lib.OP_HISTOGRAM256_U8, x.numel(), x.device)
-        check(_lib.load().wf_histogram256_u8(x.data_ptr(), x.numel(), bins.data_ptr(), grid,
-                                             ws.data_ptr(), ws.numel(), _stream_handle()),
+        check(_lib.load().wf_histogram256_u8_ex(x.data_ptr(), x.numel(), bins.data_ptr(), grid,
+                                                ws.data_ptr(), ws.numel(),
+                                                _lib.FLAG_INPUT_STABLE if input_stable else 0,
+                                                _stream_handle()),
               "histogram256_u8")
     return bins
 

@@ -230,19 +230,20 @@ class PeerCollectives:
         return out, counts
 
     def histogram256_u8(self, x_local: torch.Tensor, bins: torch.Tensor | None = None,
-                        stream=None) -> torch.Tensor:
+                        stream=None, input_stable: bool = False) -> torch.Tensor:
         """K5 over this rank's shard with the bin all-reduce fused into its
         last block (``wf_histogram256_u8_mg``): the global int64[256] bins on
-        every rank."""
+        every rank.  ``input_stable``: WF_FLAG_INPUT_STABLE."""
         ops._require_cuda(x_local, torch.uint8, "x")
         if bins is None:
             bins = torch.empty(256, dtype=torch.int64, device=x_local.device)
         self.epoch += 1
         ws = ops.workspace(_lib.OP_HISTOGRAM256_U8, x_local.numel(), x_local.device, stream)
-        _check(_lib.load().wf_histogram256_u8_mg(
+        _check(_lib.load().wf_histogram256_u8_mg_ex(
             x_local.data_ptr(), x_local.numel(), bins.data_ptr(), ws.data_ptr(), ws.numel(),
             self.boxes.peers.data_ptr(), self.boxes.own, self.cap, self.rank, self.world,
-            self.epoch, self.err.data_ptr(), ops._stream_handle(stream)),
+            self.epoch, self.err.data_ptr(), _lib.FLAG_INPUT_STABLE if input_stable else 0,
+            ops._stream_handle(stream)),
             "wf_histogram256_u8_mg")
         return bins
 

@@ -85,6 +85,27 @@ def test_fused_exchange_input_stable_chain(mods):
         boxes[0].close()
 
 
+def test_fused_histogram_input_stable_chain(mods):
+    """wf_histogram256_u8_mg_ex with WF_FLAG_INPUT_STABLE, world 1: a chain of
+    dependent launches on one mailbox, every result equal to the plain one."""
+    ops, p2p, wd = mods
+    dev = torch.device("cuda", 0)
+    u = ops.fill_synthetic("u8_geom", (1 << 24) + 3, seed=2)
+    boxes = p2p.Mailboxes.local(1, dev, cap=256)
+    try:
+        pc = p2p.PeerCollectives(boxes[0], 0, 1, 256, dev)
+        want = pc.histogram256_u8(u).clone()
+        torch.cuda.synchronize()
+        bins = torch.empty(8, 256, dtype=torch.int64, device=dev)
+        for k in range(8):
+            pc.histogram256_u8(u, bins[k], input_stable=True)
+        torch.cuda.synchronize()
+        assert torch.equal(bins, want.expand(8, 256)) and not pc.failed()
+    finally:
+        torch.cuda.synchronize()
+        boxes[0].close()
+
+
 def _child_read_mailbox(handle: bytes, world: int, q) -> None:
     import ctypes as C
     import torch as T

@@ -300,6 +300,24 @@ def test_hist_skewed(ops, gen, param):
     assert np.array_equal(host(ops.histogram256_u8(x)).view(np.uint64), want)
 
 
+def test_hist_input_stable_launches(ops):
+    """K5 with WF_FLAG_INPUT_STABLE: a back-to-back chain of dependent
+    launches over three inputs (uniform, constant, skewed), each into its own
+    bins, all equal to the oracle; the shared workspace accumulators would be
+    corrupted by a launch that touched them before its predecessor ended."""
+    n = (1 << 24) + 13
+    gens = [("u8_uniform", 0), ("u8_const", 7), ("u8_geom", 0)]
+    xs = [ops.fill_synthetic(g, n, seed=5, param=p) for g, p in gens]
+    want = [no.histogram256_u8(synthetic.generate(g, n, seed=5, param=p)) for g, p in gens]
+    bins = torch.empty(12, 256, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    for k in range(12):
+        ops.histogram256_u8(xs[k % 3], bins[k], input_stable=True)
+    got = host(bins).view(np.uint64)
+    for k in range(12):
+        assert np.array_equal(got[k], want[k % 3]), k
+
+
 def test_hist_misaligned_and_grids(ops):
     a = synthetic.generate("u8_uniform", 1 << 20, seed=6)
     d = dev(a)
