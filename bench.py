@@ -42,9 +42,10 @@ N_C5 = 1 << 32
 # only after ~25 launches (606-612 before; tools/bench_loop_probe2.py,
 # profiles/r01_reduce_experiments.md) — 512 is the robust choice.
 BLOCK_C2 = int(os.environ.get("WF_BENCH_BLOCK_C2", "512"))
-# headline steps as programmatic dependent launches (WF_FLAG_INPUT_STABLE);
-# WF_BENCH_PDL=0 measures plain stream-ordered launches for comparison
-PDL_C2 = os.environ.get("WF_BENCH_PDL", "1") != "0"
+# timed steps (headline and C3-C5) as programmatic dependent launches
+# (WF_FLAG_INPUT_STABLE: consecutive steps read one input that nothing
+# between them writes); WF_BENCH_PDL=0 measures plain stream-ordered launches
+PDL_STEPS = os.environ.get("WF_BENCH_PDL", "1") != "0"
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 NOMINAL_HBM_GBS = 8000.0   # north_star / BASELINE.md §4: % of peak also vs 8.0 TB/s
 
@@ -431,9 +432,9 @@ def run_ours(args, rank, world, local) -> dict | None:
         # writes it: each step is a programmatic dependent launch that streams
         # while the previous step drains (WF_FLAG_INPUT_STABLE; same bits)
         if peer is not None:  # one kernel: local reduce + exchange + fold
-            part = peer.reduce_sum_f32(x, block=BLOCK_C2, input_stable=PDL_C2)
+            part = peer.reduce_sum_f32(x, block=BLOCK_C2, input_stable=PDL_STEPS)
         else:
-            part = ops.reduce_sum_f32(x, block=BLOCK_C2, input_stable=PDL_C2)
+            part = ops.reduce_sum_f32(x, block=BLOCK_C2, input_stable=PDL_STEPS)
         launches += 1
         if world > 1 and peer is None:
             ops.fold(wd.exchange(part).reshape(-1))
@@ -545,9 +546,10 @@ def run_ours(args, rank, world, local) -> dict | None:
                         f"{world} B200",
             "exchange": exchange,
             "n": N_C2, "block": BLOCK_C2, "parallelism": f"shard{world}",
-            "launch": ("programmatic dependent launches: each step streams its input while "
-                       "the previous step drains (WF_FLAG_INPUT_STABLE)" if PDL_C2
-                       else "stream-ordered launches"),
+            "launch": ("programmatic dependent launches: each timed step (headline and "
+                       "per_kernel C3-C5) starts streaming its input while the previous "
+                       "step drains (WF_FLAG_INPUT_STABLE); every step still reads all of "
+                       "its input" if PDL_STEPS else "stream-ordered launches"),
             "l2": "inputs larger than L2 (4 GiB vs 126 MB), no flush needed",
         },
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
@@ -789,25 +791,26 @@ def per_kernel(args, rank, world, local, dev, peak, checks: dict) -> dict:
     lo, hi = wd.shard_range(N_C3, rank, world)
     x = ops.fill_synthetic("i32_full", hi - lo, seed=0, base=lo, device=dev)
     y = torch.empty_like(x)
-    t = time_launches(lambda: wd.scan_inclusive_i32(x, y, peer=pc), steps, warm)
+    scan = lambda: wd.scan_inclusive_i32(x, y, peer=pc, input_stable=PDL_STEPS)  # noqa: E731
+    t = time_launches(scan, steps, warm)
     res["c3_scan_i32"] = stats(t, hi - lo, 8 if world == 1 else 12, N_C3)
-    checks["c3_scan_i32"] = check_c3(wd.scan_inclusive_i32(x, y, peer=pc), x, world, rank)
+    checks["c3_scan_i32"] = check_c3(scan(), x, world, rank)
     log(f"rank {rank}: C4")
     # C4 compaction
     out = torch.empty_like(x)
-    t = time_launches(lambda: wd.compact_gt0_i32(x, out, peer=pc), steps, warm)
+    compact = lambda: wd.compact_gt0_i32(x, out, peer=pc, input_stable=PDL_STEPS)  # noqa: E731
+    t = time_launches(compact, steps, warm)
     res["c4_compact_i32"] = stats(t, hi - lo, 6, N_C4)
-    checks["c4_compact_i32"] = check_c4(wd.compact_gt0_i32(x, out, peer=pc), x, world, rank)
+    checks["c4_compact_i32"] = check_c4(compact(), x, world, rank)
     res["c4_compact_i32"]["bytes_per_elem_note"] = "4 B read + 4 B x selectivity (~0.5) written"
     # also 0 %, 1 % and 100 % selectivity (same n, i32_select)
     variants = {}
     for permille in (0, 10, 1000):
         ops.fill_synthetic("i32_select", hi - lo, seed=0, base=lo, param=permille, out=x)
-        t = time_launches(lambda: wd.compact_gt0_i32(x, out, peer=pc), steps, warm)
+        t = time_launches(compact, steps, warm)
         ms = statistics.mean(t)
         bpe = 4 + 4 * permille / 1000
-        checks[f"c4_compact_i32/{permille / 10:g}%"] = check_c4(
-            wd.compact_gt0_i32(x, out, peer=pc), x, world, rank)
+        checks[f"c4_compact_i32/{permille / 10:g}%"] = check_c4(compact(), x, world, rank)
         variants[f"{permille / 10:g}%"] = {
             "kernel_us": round(ms * 1e3, 2),
             "gbs": round(bpe * (hi - lo) / (ms * 1e-3) / 1e9, 1),
@@ -825,17 +828,17 @@ def per_kernel(args, rank, world, local, dev, peak, checks: dict) -> dict:
     # C5 histogram
     lo, hi = wd.shard_range(N_C5, rank, world)
     u = ops.fill_synthetic("u8_uniform", hi - lo, seed=0, base=lo, device=dev)
-    t = time_launches(lambda: wd.histogram256_u8(u, peer=pc, input_stable=PDL_C2), steps, warm)
+    hist = lambda: wd.histogram256_u8(u, peer=pc, input_stable=PDL_STEPS)  # noqa: E731
+    t = time_launches(hist, steps, warm)
     res["c5_hist_u8"] = stats(t, hi - lo, 1, N_C5)
-    checks["c5_hist_u8"] = check_c5(wd.histogram256_u8(u, peer=pc, input_stable=PDL_C2), u, world)
+    checks["c5_hist_u8"] = check_c5(hist(), u, world)
     # also all-same-value and skewed (geometric) bytes
     variants = {}
     for gen in ("u8_const", "u8_geom"):
         ops.fill_synthetic(gen, hi - lo, seed=0, base=lo, out=u)
-        t = time_launches(lambda: wd.histogram256_u8(u, peer=pc, input_stable=PDL_C2), steps, warm)
+        t = time_launches(hist, steps, warm)
         ms = statistics.mean(t)
-        checks[f"c5_hist_u8/{gen}"] = check_c5(
-            wd.histogram256_u8(u, peer=pc, input_stable=PDL_C2), u, world)
+        checks[f"c5_hist_u8/{gen}"] = check_c5(hist(), u, world)
         variants[gen] = {"kernel_us": round(ms * 1e3, 2),
                          "gbs": round((hi - lo) / (ms * 1e-3) / 1e9, 1),
                          "gelem_s": round(N_C5 / (max_over_ranks(ms, world) * 1e-3) / 1e9, 3)}

@@ -200,6 +200,18 @@ int wf_compact_gt0_i32_mg(const int32_t *in, uint64_t n, int32_t *out,
                           void *const *d_peers, const void *d_mailbox,
                           uint32_t cap, int rank, int world, uint32_t epoch,
                           uint32_t *d_err, wf_stream_t stream);
+/* ... with launch flags (WF_FLAG_INPUT_STABLE, as wf_reduce_sum_f32_ex) */
+int wf_reduce_sum_i32_exscan_mg_ex(const int32_t *in, uint64_t n, int32_t *d_out2,
+                                   int block, int grid, void *ws, size_t ws_bytes,
+                                   void *const *d_peers, const void *d_mailbox,
+                                   uint32_t cap, int rank, int world,
+                                   uint32_t epoch, uint32_t *d_err,
+                                   unsigned flags, wf_stream_t stream);
+int wf_compact_gt0_i32_mg_ex(const int32_t *in, uint64_t n, int32_t *out,
+                             uint64_t *d_counts3, void *ws, size_t ws_bytes,
+                             void *const *d_peers, const void *d_mailbox,
+                             uint32_t cap, int rank, int world, uint32_t epoch,
+                             uint32_t *d_err, unsigned flags, wf_stream_t stream);
 int wf_histogram256_u8_mg(const uint8_t *in, uint64_t n, uint64_t *d_bins,
                           void *ws, size_t ws_bytes, void *const *d_peers,
                           const void *d_mailbox, uint32_t cap, int rank,
@@ -256,6 +268,12 @@ void wf_mg_destroy(wf_mg_t *ctx);
 int wf_scan_inclusive_i32(const int32_t *in, int32_t *out, uint64_t n,
                           const int32_t *d_carry_in, void *ws, size_t ws_bytes,
                           wf_stream_t stream);
+/* ... with launch flags (WF_FLAG_INPUT_STABLE: the first tiles' loads overlap
+ * the previous kernel's drain; d_carry_in is read after it has completed, so
+ * it may be that kernel's output) */
+int wf_scan_inclusive_i32_ex(const int32_t *in, int32_t *out, uint64_t n,
+                             const int32_t *d_carry_in, void *ws, size_t ws_bytes,
+                             unsigned flags, wf_stream_t stream);
 
 /* ---- K4: warp-aggregated stream compaction -----------------------------
  * out[0..m) = in[i] for in[i] > 0 in index order; *d_count = m (uint64).
@@ -263,6 +281,10 @@ int wf_scan_inclusive_i32(const int32_t *in, int32_t *out, uint64_t n,
 int wf_compact_gt0_i32(const int32_t *in, uint64_t n, int32_t *out,
                        uint64_t *d_count, void *ws, size_t ws_bytes,
                        wf_stream_t stream);
+/* ... with launch flags (WF_FLAG_INPUT_STABLE, as wf_scan_inclusive_i32_ex) */
+int wf_compact_gt0_i32_ex(const int32_t *in, uint64_t n, int32_t *out,
+                          uint64_t *d_count, void *ws, size_t ws_bytes,
+                          unsigned flags, wf_stream_t stream);
 
 /* ---- K5: smem-privatised 256-bin histogram -----------------------------
  * bins[b] = #{i : in[i] == b} as uint64 (overwrites bins). */

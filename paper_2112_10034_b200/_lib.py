@@ -67,6 +67,11 @@ SIGNATURES = {
                                               _vp, _u32, C.c_int, C.c_int, _u32, _vp, _vp]),
     "wf_compact_gt0_i32_mg": (C.c_int, [_vp, _u64, _vp, _vp, _vp, _sz, _vp, _vp, _u32, C.c_int,
                                         C.c_int, _u32, _vp, _vp]),
+    "wf_compact_gt0_i32_mg_ex": (C.c_int, [_vp, _u64, _vp, _vp, _vp, _sz, _vp, _vp, _u32,
+                                           C.c_int, C.c_int, _u32, _vp, C.c_uint, _vp]),
+    "wf_reduce_sum_i32_exscan_mg_ex": (C.c_int, [_vp, _u64, _vp, C.c_int, C.c_int, _vp, _sz, _vp,
+                                                 _vp, _u32, C.c_int, C.c_int, _u32, _vp, C.c_uint,
+                                                 _vp]),
     "wf_histogram256_u8_mg": (C.c_int, [_vp, _u64, _vp, _vp, _sz, _vp, _vp, _u32, C.c_int,
                                         C.c_int, _u32, _vp, _vp]),
     "wf_histogram256_u8_mg_ex": (C.c_int, [_vp, _u64, _vp, _vp, _sz, _vp, _vp, _u32, C.c_int,
@@ -79,6 +84,8 @@ SIGNATURES = {
     "wf_fold_u64": (C.c_int, [_vp, _u32, _vp, _vp]),
     "wf_scan_inclusive_i32": (C.c_int, [_vp, _vp, _u64, _vp, _vp, _sz, _vp]),
     "wf_compact_gt0_i32": (C.c_int, [_vp, _u64, _vp, _vp, _vp, _sz, _vp]),
+    "wf_scan_inclusive_i32_ex": (C.c_int, [_vp, _vp, _u64, _vp, _vp, _sz, C.c_uint, _vp]),
+    "wf_compact_gt0_i32_ex": (C.c_int, [_vp, _u64, _vp, _vp, _vp, _sz, C.c_uint, _vp]),
     "wf_histogram256_u8": (C.c_int, [_vp, _u64, _vp, C.c_int, _vp, _sz, _vp]),
     "wf_histogram256_u8_ex": (C.c_int, [_vp, _u64, _vp, C.c_int, _vp, _sz, C.c_uint, _vp]),
     "wf_warp_collective": (C.c_int, [C.c_int, _vp, _vp, _i32, _vp, _u64, C.c_int, C.c_int,

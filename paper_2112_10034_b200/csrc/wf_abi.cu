@@ -356,6 +356,16 @@ int wf_reduce_sum_i32_exscan_mg(const int32_t *in, uint64_t n, int32_t *d_out2, 
                                 int grid, void *ws, size_t ws_bytes, void *const *d_peers,
                                 const void *d_mailbox, uint32_t cap, int rank, int world,
                                 uint32_t epoch, uint32_t *d_err, wf_stream_t stream) {
+  return wf_reduce_sum_i32_exscan_mg_ex(in, n, d_out2, block, grid, ws, ws_bytes, d_peers,
+                                        d_mailbox, cap, rank, world, epoch, d_err, 0u, stream);
+}
+
+int wf_reduce_sum_i32_exscan_mg_ex(const int32_t *in, uint64_t n, int32_t *d_out2, int block,
+                                   int grid, void *ws, size_t ws_bytes, void *const *d_peers,
+                                   const void *d_mailbox, uint32_t cap, int rank, int world,
+                                   uint32_t epoch, uint32_t *d_err, unsigned flags,
+                                   wf_stream_t stream) {
+  if (flags & ~unsigned(WF_FLAG_INPUT_STABLE)) return fail(WF_ERR_ARG, "unknown flags 0x%x", flags);
   int rc = reduce_common(WF_OP_REDUCE_SUM_I32, in, n, d_out2, block, grid, ws, ws_bytes);
   if (rc) return rc;
   rc = check_peer(d_peers, d_mailbox, cap, 1, rank, world, epoch, d_err);
@@ -363,7 +373,8 @@ int wf_reduce_sum_i32_exscan_mg(const int32_t *in, uint64_t n, int32_t *d_out2, 
   if (grid == 0) grid = auto_reduce_grid(false, block, n);
   return cuda_status(launch_reduce_i32_exscan_mg(in, n, d_out2, block, grid, ws, d_peers,
                                                  d_mailbox, cap, rank, world, epoch, d_err,
-                                                 static_cast<cudaStream_t>(stream)),
+                                                 static_cast<cudaStream_t>(stream),
+                                                 (flags & WF_FLAG_INPUT_STABLE) != 0),
                      "reduce_sum_i32_exscan_mg");
 }
 
@@ -371,6 +382,16 @@ int wf_compact_gt0_i32_mg(const int32_t *in, uint64_t n, int32_t *out, uint64_t 
                           void *ws, size_t ws_bytes, void *const *d_peers, const void *d_mailbox,
                           uint32_t cap, int rank, int world, uint32_t epoch, uint32_t *d_err,
                           wf_stream_t stream) {
+  return wf_compact_gt0_i32_mg_ex(in, n, out, d_counts3, ws, ws_bytes, d_peers, d_mailbox, cap,
+                                  rank, world, epoch, d_err, 0u, stream);
+}
+
+int wf_compact_gt0_i32_mg_ex(const int32_t *in, uint64_t n, int32_t *out, uint64_t *d_counts3,
+                             void *ws, size_t ws_bytes, void *const *d_peers,
+                             const void *d_mailbox, uint32_t cap, int rank, int world,
+                             uint32_t epoch, uint32_t *d_err, unsigned flags,
+                             wf_stream_t stream) {
+  if (flags & ~unsigned(WF_FLAG_INPUT_STABLE)) return fail(WF_ERR_ARG, "unknown flags 0x%x", flags);
   if (d_counts3 == nullptr) return fail(WF_ERR_ARG, "counts pointer is NULL");
   if (n > 0 && (in == nullptr || out == nullptr)) return fail(WF_ERR_ARG, "NULL buffer pointer");
   if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 3u)
@@ -383,7 +404,8 @@ int wf_compact_gt0_i32_mg(const int32_t *in, uint64_t n, int32_t *out, uint64_t 
   if (rc) return rc;
   return cuda_status(launch_compact_gt0_i32_mg(in, n, out, d_counts3, ws, d_peers, d_mailbox, cap,
                                                rank, world, epoch, d_err,
-                                               static_cast<cudaStream_t>(stream)),
+                                               static_cast<cudaStream_t>(stream),
+                                               (flags & WF_FLAG_INPUT_STABLE) != 0),
                      "compact_gt0_i32_mg");
 }
 
@@ -450,6 +472,13 @@ int wf_fold_u64(const uint64_t *vals, uint32_t count, uint64_t *out, wf_stream_t
 
 int wf_scan_inclusive_i32(const int32_t *in, int32_t *out, uint64_t n, const int32_t *d_carry_in,
                           void *ws, size_t ws_bytes, wf_stream_t stream) {
+  return wf_scan_inclusive_i32_ex(in, out, n, d_carry_in, ws, ws_bytes, 0u, stream);
+}
+
+int wf_scan_inclusive_i32_ex(const int32_t *in, int32_t *out, uint64_t n,
+                             const int32_t *d_carry_in, void *ws, size_t ws_bytes, unsigned flags,
+                             wf_stream_t stream) {
+  if (flags & ~unsigned(WF_FLAG_INPUT_STABLE)) return fail(WF_ERR_ARG, "unknown flags 0x%x", flags);
   if (n > 0 && (in == nullptr || out == nullptr)) return fail(WF_ERR_ARG, "NULL buffer pointer");
   if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 3u)
     return fail(WF_ERR_ARG, "buffers must be 4-byte aligned");
@@ -457,12 +486,19 @@ int wf_scan_inclusive_i32(const int32_t *in, int32_t *out, uint64_t n, const int
     return fail(WF_ERR_ARG, "n=%llu exceeds the tile-id range", (unsigned long long)n);
   int rc = check_ws(WF_OP_SCAN_INCLUSIVE_I32, n, ws, ws_bytes);
   if (rc) return rc;
-  return cuda_status(launch_scan_i32(in, out, n, d_carry_in, ws, static_cast<cudaStream_t>(stream)),
+  return cuda_status(launch_scan_i32(in, out, n, d_carry_in, ws, static_cast<cudaStream_t>(stream),
+                                     (flags & WF_FLAG_INPUT_STABLE) != 0),
                      "scan_inclusive_i32");
 }
 
 int wf_compact_gt0_i32(const int32_t *in, uint64_t n, int32_t *out, uint64_t *d_count, void *ws,
                        size_t ws_bytes, wf_stream_t stream) {
+  return wf_compact_gt0_i32_ex(in, n, out, d_count, ws, ws_bytes, 0u, stream);
+}
+
+int wf_compact_gt0_i32_ex(const int32_t *in, uint64_t n, int32_t *out, uint64_t *d_count,
+                          void *ws, size_t ws_bytes, unsigned flags, wf_stream_t stream) {
+  if (flags & ~unsigned(WF_FLAG_INPUT_STABLE)) return fail(WF_ERR_ARG, "unknown flags 0x%x", flags);
   if (d_count == nullptr) return fail(WF_ERR_ARG, "count pointer is NULL");
   if (n > 0 && (in == nullptr || out == nullptr)) return fail(WF_ERR_ARG, "NULL buffer pointer");
   if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 3u)
@@ -472,7 +508,8 @@ int wf_compact_gt0_i32(const int32_t *in, uint64_t n, int32_t *out, uint64_t *d_
   int rc = check_ws(WF_OP_COMPACT_GT0_I32, n, ws, ws_bytes);
   if (rc) return rc;
   return cuda_status(
-      launch_compact_gt0_i32(in, n, out, d_count, ws, static_cast<cudaStream_t>(stream)),
+      launch_compact_gt0_i32(in, n, out, d_count, ws, static_cast<cudaStream_t>(stream),
+                             (flags & WF_FLAG_INPUT_STABLE) != 0),
       "compact_gt0_i32");
 }
 

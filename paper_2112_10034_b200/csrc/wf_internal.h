@@ -84,7 +84,7 @@ cudaError_t launch_reduce_f32_mg(const float *in, uint64_t n, float *out, int bl
 cudaError_t launch_reduce_i32_exscan_mg(const int32_t *in, uint64_t n, int32_t *out2, int block,
                                         int grid, void *ws, void *const *peers, const void *mine,
                                         uint32_t cap, int rank, int world, uint32_t epoch,
-                                        uint32_t *err, cudaStream_t s);
+                                        uint32_t *err, cudaStream_t s, bool early = false);
 cudaError_t launch_hist256_mg(const uint8_t *in, uint64_t n, uint64_t *bins, int grid, void *ws,
                               void *const *peers, const void *mine, uint32_t cap, int rank,
                               int world, uint32_t epoch, uint32_t *err, cudaStream_t s,
@@ -101,26 +101,32 @@ cudaError_t launch_fold_u64(const uint64_t *v, uint32_t count, uint64_t *out,
                             cudaStream_t s);
 
 // scan / compaction (wf_scan.cu)
+// early: programmatic dependent launch on the caller's WF_FLAG_INPUT_STABLE
+// promise (the round-1 variant kernels ignore it)
 cudaError_t launch_scan_i32(const int32_t *in, int32_t *out, uint64_t n,
-                            const int32_t *carry, void *ws, cudaStream_t s);
+                            const int32_t *carry, void *ws, cudaStream_t s,
+                            bool early = false);
 cudaError_t launch_compact_gt0_i32(const int32_t *in, uint64_t n,
                                    int32_t *out, uint64_t *count, void *ws,
-                                   cudaStream_t s);
+                                   cudaStream_t s, bool early = false);
 
 // TMEM-parked single-pass scan / compaction (wf_scan_tmem.cu), any 4-byte
 // aligned buffers — the product kernels
 cudaError_t launch_scan_tmem_i32(const int32_t *in, int32_t *out, uint64_t n,
-                                 const int32_t *carry, void *ws, cudaStream_t s);
+                                 const int32_t *carry, void *ws, cudaStream_t s,
+                                 bool early = false);
 cudaError_t launch_compact_tmem_i32(const int32_t *in, uint64_t n, int32_t *out,
-                                    uint64_t *count, void *ws, cudaStream_t s);
+                                    uint64_t *count, void *ws, cudaStream_t s,
+                                    bool early = false);
 struct PeerArgs;  // wf_peer.cuh
 cudaError_t launch_compact_tmem_i32_mg(const int32_t *in, uint64_t n, int32_t *out,
                                        uint64_t *counts3, void *ws, const PeerArgs &pa,
-                                       cudaStream_t s);
+                                       cudaStream_t s, bool early = false);
 cudaError_t launch_compact_gt0_i32_mg(const int32_t *in, uint64_t n, int32_t *out,
                                       uint64_t *counts3, void *ws, void *const *peers,
                                       const void *mine, uint32_t cap, int rank, int world,
-                                      uint32_t epoch, uint32_t *err, cudaStream_t s);
+                                      uint32_t epoch, uint32_t *err, cudaStream_t s,
+                                      bool early = false);
 
 // Variant builds only (tools/variants/, -DWF_SCAN_IMPL != 0): the round-1
 // register-tile / smem-stage kernels and the L2-streamed two-pass kernels.

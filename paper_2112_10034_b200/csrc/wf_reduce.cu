@@ -432,9 +432,12 @@ cudaError_t launch_mg_block(const float *in, uint64_t n, float *out, int grid, v
 
 template <int BLOCK>
 cudaError_t launch_px_block(const int32_t *in, uint64_t n, int32_t *out2, int grid, void *ws,
-                            const PeerArgs &pa, cudaStream_t s) {
+                            const PeerArgs &pa, bool early, cudaStream_t s) {
   auto *ticket = reinterpret_cast<uint32_t *>(ws);
   auto *partials = reinterpret_cast<uint32_t *>(static_cast<char *>(ws) + kWsHeader);
+  if (early)
+    return launch_pdl(reduce_kernel<SumI32, BLOCK, kUnroll, false, true, true>, grid, BLOCK, s,
+                      in, n, out2, partials, ticket, MgArgs{}, pa);
   reduce_kernel<SumI32, BLOCK, kUnroll, false, true>
       <<<grid, BLOCK, 0, s>>>(in, n, out2, partials, ticket, MgArgs{}, pa);
   return cudaGetLastError();
@@ -455,14 +458,14 @@ extern "C" int wf_debug_set_trace_red(void *buf) {
 cudaError_t launch_reduce_i32_exscan_mg(const int32_t *in, uint64_t n, int32_t *out2, int block,
                                         int grid, void *ws, void *const *peers, const void *mine,
                                         uint32_t cap, int rank, int world, uint32_t epoch,
-                                        uint32_t *err, cudaStream_t s) {
+                                        uint32_t *err, cudaStream_t s, bool early) {
   PeerArgs pa{reinterpret_cast<uint64_t *const *>(peers), static_cast<const uint64_t *>(mine),
               cap, rank, world, epoch, err};
   switch (block) {
-    case 128: return launch_px_block<128>(in, n, out2, grid, ws, pa, s);
-    case 256: return launch_px_block<256>(in, n, out2, grid, ws, pa, s);
-    case 512: return launch_px_block<512>(in, n, out2, grid, ws, pa, s);
-    case 1024: return launch_px_block<1024>(in, n, out2, grid, ws, pa, s);
+    case 128: return launch_px_block<128>(in, n, out2, grid, ws, pa, early, s);
+    case 256: return launch_px_block<256>(in, n, out2, grid, ws, pa, early, s);
+    case 512: return launch_px_block<512>(in, n, out2, grid, ws, pa, early, s);
+    case 1024: return launch_px_block<1024>(in, n, out2, grid, ws, pa, early, s);
     default: return cudaErrorInvalidValue;
   }
 }

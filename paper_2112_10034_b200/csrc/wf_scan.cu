@@ -26,7 +26,7 @@
 namespace wf {
 
 cudaError_t launch_scan_i32(const int32_t *in, int32_t *out, uint64_t n,
-                            const int32_t *carry, void *ws, cudaStream_t s) {
+                            const int32_t *carry, void *ws, cudaStream_t s, bool early) {
   if (n == 0) return cudaSuccess;
 #if WF_SCAN_IMPL == 3
   if ((((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u) == 0) &&
@@ -35,11 +35,11 @@ cudaError_t launch_scan_i32(const int32_t *in, int32_t *out, uint64_t n,
 #elif WF_SCAN_IMPL != 0
   return launch_scan_legacy_i32(WF_SCAN_IMPL, in, out, n, carry, ws, s);
 #endif
-  return launch_scan_tmem_i32(in, out, n, carry, ws, s);
+  return launch_scan_tmem_i32(in, out, n, carry, ws, s, early);
 }
 
 cudaError_t launch_compact_gt0_i32(const int32_t *in, uint64_t n, int32_t *out,
-                                   uint64_t *count, void *ws, cudaStream_t s) {
+                                   uint64_t *count, void *ws, cudaStream_t s, bool early) {
   if (n == 0) return cudaMemsetAsync(count, 0, sizeof(uint64_t), s);
 #if WF_SCAN_IMPL == 3
   if ((reinterpret_cast<uintptr_t>(in) & 15u) == 0 && two_pass_usable(n))
@@ -47,7 +47,7 @@ cudaError_t launch_compact_gt0_i32(const int32_t *in, uint64_t n, int32_t *out,
 #elif WF_SCAN_IMPL != 0
   return launch_compact_legacy_i32(WF_SCAN_IMPL, in, n, out, count, ws, s);
 #endif
-  return launch_compact_tmem_i32(in, n, out, count, ws, s);
+  return launch_compact_tmem_i32(in, n, out, count, ws, s, early);
 }
 
 // Sharded compaction + offset exchange, fused into the TMEM kernel's last
@@ -56,11 +56,11 @@ cudaError_t launch_compact_gt0_i32(const int32_t *in, uint64_t n, int32_t *out,
 cudaError_t launch_compact_gt0_i32_mg(const int32_t *in, uint64_t n, int32_t *out,
                                       uint64_t *counts3, void *ws, void *const *peers,
                                       const void *mine, uint32_t cap, int rank, int world,
-                                      uint32_t epoch, uint32_t *err, cudaStream_t s) {
+                                      uint32_t epoch, uint32_t *err, cudaStream_t s, bool early) {
   PeerArgs pa{reinterpret_cast<uint64_t *const *>(peers), static_cast<const uint64_t *>(mine),
               cap, rank, world, epoch, err};
 #if WF_SCAN_IMPL == 0
-  if (n > 0) return launch_compact_tmem_i32_mg(in, n, out, counts3, ws, pa, s);
+  if (n > 0) return launch_compact_tmem_i32_mg(in, n, out, counts3, ws, pa, s, early);
 #endif
   cudaError_t e = launch_compact_gt0_i32(in, n, out, counts3, ws, s);
   if (e != cudaSuccess) return e;

@@ -87,6 +87,10 @@
 #define WF_LBK_COMPACT_TM 1  // compaction look-back width (1: 277.7 vs 2: 281.6 us, tools/lbk_sweep.sh)
 #endif
 
+#ifndef WF_TM_PREFETCH
+#define WF_TM_PREFETCH 1  // L2 prefetch of the first S tiles per CTA before griddepcontrol.wait
+#endif
+
 #ifndef WF_CMP_STCS
 #define WF_CMP_STCS 0  // 1: compaction stores with the streaming (.cs) hint
 #endif
@@ -308,11 +312,35 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
     sh.item_seq[threadIdx.x] = kNoItem;
     sh.item_posted[threadIdx.x] = kNoItem;
   }
-  if (warp == W_PROD && lane == 0)
-    sh.epoch = ld_volatile_u32(&hdr->epoch) & kEpochMask;  // before this CTA's first (release) draw
+  // a programmatic dependent launch behind this one may start its loads now
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+
+  // Early L2 prefetch of the first tiles: between them, the CTAs warm L2 with
+  // tiles [0, S * grid) — exactly the tiles the first claims will take —
+  // before anything touches the workspace.  For a programmatic dependent
+  // launch (the caller's WF_FLAG_INPUT_STABLE promise: the previous kernel on
+  // the stream does not write `in`) these reads overlap the previous grid's
+  // drain.  Only a hint: claims stay dynamic (ticket order), so no tile is
+  // ever owned by a CTA that is not running, and a grid that is only partly
+  // resident (other kernels on the GPU) still makes progress.
+  if (WF_TM_PREFETCH && warp == W_PROD && lane == 0)
+    for (uint32_t i = 0; i < uint32_t(S); ++i) {
+      const uint64_t t = uint64_t(blockIdx.x) + uint64_t(i) * gridDim.x;
+      if ((t + 1) * TM_TILE > n) break;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(in + t * TM_TILE),
+                   "r"(TM_TILE * 4u)
+                   : "memory");
+    }
+  // Nothing below touches the workspace, the carry or the outputs before the
+  // previous grid on the stream has completed and flushed (returns at once
+  // for an ordinary stream-ordered launch).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (warp == W_PROD && lane == 0)
+    sh.epoch = ld_volatile_u32(&hdr->epoch) & kEpochMask;  // before this CTA's first (release) draw
+  __syncthreads();
   const uint32_t epoch = sh.epoch;
 
   if (warp == W_PROD) {
@@ -924,44 +952,61 @@ extern "C" int wf_debug_set_trace_sweep(void *buf, uint32_t cap) {
 // `in` / `out` need only 4-byte alignment: the input is rounded down to 16 B
 // and its 0-3 leading elements masked; a scan output at another 16-byte
 // offset is written with scalar stores.
+// `early`: a programmatic dependent launch (the caller's WF_FLAG_INPUT_STABLE
+// promise); the kernel's static first loads then overlap the previous grid.
+template <bool COMPACT, bool PX>
+cudaError_t launch_tmem(uint32_t nt, bool early, cudaStream_t s, const int32_t *in, int32_t *out,
+                        uint64_t nv, const int32_t *carry, uint64_t *count, uint64_t *desc,
+                        TileHeader *hdr, uint32_t head, bool vec_out, const PeerArgs &pa) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tmem_grid<COMPACT, PX>(nt));
+  cfg.blockDim = dim3(TM_THREADS);
+  cfg.dynamicSmemBytes = tm_smem<COMPACT>();
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = early ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, tile_tmem_kernel<COMPACT, PX>, in, out, nv, nt, carry, count,
+                            desc, hdr, head, vec_out, pa);
+}
+
 cudaError_t launch_scan_tmem_i32(const int32_t *in, int32_t *out, uint64_t n,
-                                 const int32_t *carry, void *ws, cudaStream_t s) {
+                                 const int32_t *carry, void *ws, cudaStream_t s, bool early) {
   auto *hdr = reinterpret_cast<TileHeader *>(ws);
   auto *desc = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + kTileWsHeader);
   const uint32_t head = uint32_t((reinterpret_cast<uintptr_t>(in) & 15u) / 4u);
   const uint64_t nv = n + head;
   const uint32_t nt = uint32_t((nv + TM_TILE - 1) / TM_TILE);
-  tile_tmem_kernel<false><<<tmem_grid<false>(nt), TM_THREADS, tm_smem<false>(), s>>>(
-      in - head, out - head, nv, nt, carry, nullptr, desc, hdr, head,
+  return launch_tmem<false, false>(
+      nt, early, s, in - head, out - head, nv, carry, nullptr, desc, hdr, head,
       ((reinterpret_cast<uintptr_t>(in) ^ reinterpret_cast<uintptr_t>(out)) & 15u) == 0,
       PeerArgs{});
-  return cudaGetLastError();
 }
 
 cudaError_t launch_compact_tmem_i32(const int32_t *in, uint64_t n, int32_t *out, uint64_t *count,
-                                    void *ws, cudaStream_t s) {
+                                    void *ws, cudaStream_t s, bool early) {
   auto *hdr = reinterpret_cast<TileHeader *>(ws);
   auto *desc = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + kTileWsHeader);
   const uint32_t head = uint32_t((reinterpret_cast<uintptr_t>(in) & 15u) / 4u);
   const uint64_t nv = n + head;
   const uint32_t nt = uint32_t((nv + TM_TILE - 1) / TM_TILE);
-  tile_tmem_kernel<true><<<tmem_grid<true>(nt), TM_THREADS, tm_smem<true>(), s>>>(
-      in - head, out, nv, nt, nullptr, count, desc, hdr, head, false, PeerArgs{});
-  return cudaGetLastError();
+  return launch_tmem<true, false>(nt, early, s, in - head, out, nv, nullptr, count, desc, hdr,
+                                  head, false, PeerArgs{});
 }
 
 // n >= 1.  counts3 = {count, global offset, global total}.
 cudaError_t launch_compact_tmem_i32_mg(const int32_t *in, uint64_t n, int32_t *out,
                                        uint64_t *counts3, void *ws, const PeerArgs &pa,
-                                       cudaStream_t s) {
+                                       cudaStream_t s, bool early) {
   auto *hdr = reinterpret_cast<TileHeader *>(ws);
   auto *desc = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + kTileWsHeader);
   const uint32_t head = uint32_t((reinterpret_cast<uintptr_t>(in) & 15u) / 4u);
   const uint64_t nv = n + head;
   const uint32_t nt = uint32_t((nv + TM_TILE - 1) / TM_TILE);
-  tile_tmem_kernel<true, true><<<tmem_grid<true, true>(nt), TM_THREADS, tm_smem<true>(), s>>>(
-      in - head, out, nv, nt, nullptr, counts3, desc, hdr, head, false, pa);
-  return cudaGetLastError();
+  return launch_tmem<true, true>(nt, early, s, in - head, out, nv, nullptr, counts3, desc, hdr,
+                                 head, false, pa);
 }
 
 cudaError_t preload_tmem_mg_kernels() {

@@ -84,30 +84,34 @@ def reduce_sum_i32(x_local: torch.Tensor, group=None, block: int = 256) -> torch
 
 
 def scan_inclusive_i32(x_local: torch.Tensor, out: torch.Tensor | None = None,
-                       group=None, peer=None) -> torch.Tensor:
+                       group=None, peer=None, input_stable: bool = False) -> torch.Tensor:
     """`peer`: a p2p.PeerCollectives — the shard totals then travel over peer
-    memory in one kernel instead of NCCL all-gather + fold."""
+    memory in one kernel instead of NCCL all-gather + fold.  `input_stable`:
+    WF_FLAG_INPUT_STABLE for the first kernel of the call (the kernel issued
+    just before on the stream does not write `x_local`); the scan after the
+    fused pass 1 always takes it (pass 1 writes only the carry)."""
     rank, world = _world(group)
     if world == 1:
-        return ops.scan_inclusive_i32(x_local, out)
+        return ops.scan_inclusive_i32(x_local, out, input_stable=input_stable)
     if peer is not None:  # pass 1 + carry exchange in one kernel
-        carry = peer.reduce_exscan_i32(x_local)[:1]
-        return ops.scan_inclusive_i32(x_local, out, carry=carry)
+        carry = peer.reduce_exscan_i32(x_local, input_stable=input_stable)[:1]
+        return ops.scan_inclusive_i32(x_local, out, carry=carry, input_stable=True)
     totals = exchange(ops.reduce_sum_i32(x_local), group).reshape(-1)
     carry = ops.fold(totals, count=rank)  # exclusive prefix of earlier shards
     return ops.scan_inclusive_i32(x_local, out, carry=carry)
 
 
 def compact_gt0_i32(x_local: torch.Tensor, out: torch.Tensor | None = None, group=None,
-                    peer=None):
+                    peer=None, input_stable: bool = False):
     """Returns (out_local, count_local, offset, total) as device int64 scalars
     for count/offset/total; rank r's selected elements belong at
-    [offset, offset + count) of the global a[a > 0]."""
+    [offset, offset + count) of the global a[a > 0].  `input_stable`:
+    WF_FLAG_INPUT_STABLE."""
     rank, world = _world(group)
     if world > 1 and peer is not None:  # compaction + offset exchange in one kernel
-        out, c3 = peer.compact_gt0_i32(x_local, out)
+        out, c3 = peer.compact_gt0_i32(x_local, out, input_stable=input_stable)
         return out, c3[:1], c3[1:2], c3[2:]
-    out, count = ops.compact_gt0_i32(x_local, out)
+    out, count = ops.compact_gt0_i32(x_local, out, input_stable=input_stable)
     if world == 1:
         zero = torch.zeros(1, dtype=torch.int64, device=count.device)
         return out, count, zero, count

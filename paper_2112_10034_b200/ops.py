@@ -153,9 +153,12 @@ def fold(vals: torch.Tensor, count: int | None = None,
 # ---- K3 / K4 / K5 --------------------------------------------------------
 
 def scan_inclusive_i32(x: torch.Tensor, out: torch.Tensor | None = None,
-                       carry: torch.Tensor | None = None) -> torch.Tensor:
+                       carry: torch.Tensor | None = None,
+                       input_stable: bool = False) -> torch.Tensor:
     """Inclusive wrapping prefix sum (K3); ``carry`` (device int32[1]) is added
-    to every output (cross-GPU carry-in).  ``out`` may be ``x`` (in place)."""
+    to every output (cross-GPU carry-in).  ``out`` may be ``x`` (in place).
+    ``input_stable``: WF_FLAG_INPUT_STABLE (the kernel issued just before on
+    the stream does not write ``x``; ``carry`` may be its output)."""
     _require_cuda(x, torch.int32, "x")
     if out is None:
         out = torch.empty_like(x)
@@ -168,17 +171,20 @@ def scan_inclusive_i32(x: torch.Tensor, out: torch.Tensor | None = None,
         cptr = carry.data_ptr()
     with _on(x.device):
         ws = workspace(_lib.OP_SCAN_INCLUSIVE_I32, x.numel(), x.device)
-        check(_lib.load().wf_scan_inclusive_i32(x.data_ptr(), out.data_ptr(), x.numel(), cptr,
-                                                ws.data_ptr(), ws.numel(), _stream_handle()),
+        check(_lib.load().wf_scan_inclusive_i32_ex(x.data_ptr(), out.data_ptr(), x.numel(), cptr,
+                                                   ws.data_ptr(), ws.numel(),
+                                                   _lib.FLAG_INPUT_STABLE if input_stable else 0,
+                                                   _stream_handle()),
               "scan_inclusive_i32")
     return out
 
 
 def compact_gt0_i32(x: torch.Tensor, out: torch.Tensor | None = None,
-                    count: torch.Tensor | None = None):
+                    count: torch.Tensor | None = None, input_stable: bool = False):
     """Order-preserving ``x[x > 0]`` (K4).  Returns ``(out, count)`` where
     ``out`` has capacity ``x.numel()`` and ``count`` is a device int64[1]
-    (bit-identical to the C ABI's uint64)."""
+    (bit-identical to the C ABI's uint64).  ``input_stable``:
+    WF_FLAG_INPUT_STABLE."""
     _require_cuda(x, torch.int32, "x")
     if out is None:
         out = torch.empty_like(x)
@@ -190,9 +196,10 @@ def compact_gt0_i32(x: torch.Tensor, out: torch.Tensor | None = None,
     _require_cuda(count, torch.int64, "count")
     with _on(x.device):
         ws = workspace(_lib.OP_COMPACT_GT0_I32, x.numel(), x.device)
-        check(_lib.load().wf_compact_gt0_i32(x.data_ptr(), x.numel(), out.data_ptr(),
-                                             count.data_ptr(), ws.data_ptr(), ws.numel(),
-                                             _stream_handle()),
+        check(_lib.load().wf_compact_gt0_i32_ex(x.data_ptr(), x.numel(), out.data_ptr(),
+                                                count.data_ptr(), ws.data_ptr(), ws.numel(),
+                                                _lib.FLAG_INPUT_STABLE if input_stable else 0,
+                                                _stream_handle()),
               "compact_gt0_i32")
     return out, count
 

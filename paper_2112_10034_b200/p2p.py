@@ -194,7 +194,7 @@ class PeerCollectives:
         return self._run(self.ALLREDUCE, v, v.numel(), out, stream)
 
     def reduce_exscan_i32(self, x_local: torch.Tensor, out: torch.Tensor | None = None,
-                          block: int = 256, stream=None) -> torch.Tensor:
+                          block: int = 256, stream=None, input_stable: bool = False) -> torch.Tensor:
         """K1 over this rank's shard with the carry exchange fused into its
         last block (``wf_reduce_sum_i32_exscan_mg``): int32[2] = (wrapping sum
         of the shards of lower ranks, wrapping sum of all shards) — the
@@ -204,15 +204,16 @@ class PeerCollectives:
             out = torch.empty(2, dtype=torch.int32, device=x_local.device)
         self.epoch += 1
         ws = ops.workspace(_lib.OP_REDUCE_SUM_I32, x_local.numel(), x_local.device, stream)
-        _check(_lib.load().wf_reduce_sum_i32_exscan_mg(
+        _check(_lib.load().wf_reduce_sum_i32_exscan_mg_ex(
             x_local.data_ptr(), x_local.numel(), out.data_ptr(), block, 0, ws.data_ptr(),
             ws.numel(), self.boxes.peers.data_ptr(), self.boxes.own, self.cap, self.rank,
-            self.world, self.epoch, self.err.data_ptr(), ops._stream_handle(stream)),
+            self.world, self.epoch, self.err.data_ptr(),
+            _lib.FLAG_INPUT_STABLE if input_stable else 0, ops._stream_handle(stream)),
             "wf_reduce_sum_i32_exscan_mg")
         return out
 
     def compact_gt0_i32(self, x_local: torch.Tensor, out: torch.Tensor | None = None,
-                        stream=None):
+                        stream=None, input_stable: bool = False):
         """K4 over this rank's shard with the offset exchange fused into the
         compaction kernel (``wf_compact_gt0_i32_mg``): returns (out_local,
         int64[3] = (count, global offset, global total))."""
@@ -222,10 +223,11 @@ class PeerCollectives:
         counts = torch.empty(3, dtype=torch.int64, device=x_local.device)
         self.epoch += 1
         ws = ops.workspace(_lib.OP_COMPACT_GT0_I32, x_local.numel(), x_local.device, stream)
-        _check(_lib.load().wf_compact_gt0_i32_mg(
+        _check(_lib.load().wf_compact_gt0_i32_mg_ex(
             x_local.data_ptr(), x_local.numel(), out.data_ptr(), counts.data_ptr(), ws.data_ptr(),
             ws.numel(), self.boxes.peers.data_ptr(), self.boxes.own, self.cap, self.rank,
-            self.world, self.epoch, self.err.data_ptr(), ops._stream_handle(stream)),
+            self.world, self.epoch, self.err.data_ptr(),
+            _lib.FLAG_INPUT_STABLE if input_stable else 0, ops._stream_handle(stream)),
             "wf_compact_gt0_i32_mg")
         return out, counts
 

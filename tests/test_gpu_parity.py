@@ -283,6 +283,55 @@ def test_tmem_kernel_many_launches(ops):
         assert int(host(cnt)[0]) == len(want) and np.array_equal(host(out)[:len(want)], want)
 
 
+# tile counts around the early L2 prefetch of the first claims (4 stages x 148
+# CTAs = 592 tiles of 8192): fewer tiles than CTAs, exactly / one past, many
+TILE_EDGE_SIZES = [1, 8192 * 3 + 5, 8192 * 148, 8192 * 592, 8192 * 592 + 1, 8192 * 600 - 3,
+                   (1 << 23) + 77]
+
+
+def test_tmem_kernels_input_stable_chain(ops):
+    """K3/K4 with WF_FLAG_INPUT_STABLE: a back-to-back chain of dependent
+    launches over inputs of every tile-count regime, alternating scan and
+    compaction on one stream, every output in its own buffer; equal to the
+    oracle.  Only the L2 prefetch of the first tiles precedes
+    griddepcontrol.wait; the tickets, epochs, descriptors and outputs are
+    touched after it, so a launch that raced its predecessor would corrupt the
+    shared workspace."""
+    xs = [ops.fill_synthetic("i32_select", n, seed=i, param=600)
+          for i, n in enumerate(TILE_EDGE_SIZES)]
+    ys = [torch.empty_like(x) for x in xs]
+    outs = [torch.empty_like(x) for x in xs]
+    cnts = [torch.empty(1, dtype=torch.int64, device="cuda") for _ in xs]
+    torch.cuda.synchronize()
+    for _ in range(2):
+        for x, y, o, c in zip(xs, ys, outs, cnts):
+            ops.scan_inclusive_i32(x, y, input_stable=True)
+            ops.compact_gt0_i32(x, o, c, input_stable=True)
+    torch.cuda.synchronize()
+    for i, n in enumerate(TILE_EDGE_SIZES):
+        a = synthetic.generate("i32_select", n, seed=i, param=600)
+        assert np.array_equal(host(ys[i]), no.scan_inclusive_i32(a)), n
+        want = no.compact_gt0_i32(a)
+        assert int(host(cnts[i])[0]) == len(want), n
+        assert np.array_equal(host(outs[i])[:len(want)], want), n
+
+
+def test_scan_input_stable_carry_from_predecessor(ops):
+    """The flagged scan reads its device carry only after the previous kernel
+    (which wrote it) has completed: the sharded scan's pass 1 -> scan pair."""
+    n = (1 << 22) + 9
+    x = ops.fill_synthetic("i32_full", n, seed=4)
+    a = synthetic.generate("i32_full", n, seed=4)
+    torch.cuda.synchronize()
+    y = torch.empty_like(x)
+    for c in (0, 12345, -7, 2 ** 31 - 1):
+        carry = torch.full((1,), 0, dtype=torch.int32, device="cuda")
+        carry.fill_(c)  # a kernel that writes the carry right before the scan
+        ops.scan_inclusive_i32(x, y, carry=carry, input_stable=True)
+        want = (no.scan_inclusive_i32(a).astype(np.int64) + c).astype(np.int32)
+        assert np.array_equal(host(y), want), c
+
+
 # ---- K5 ----------------------------------------------------------------------
 
 @pytest.mark.parametrize("n", SIZES + [(1 << 22) + 13])

@@ -19,6 +19,7 @@ pc = p2p.PeerCollectives(boxes[0], 0, 1, 256, dev)
 
 
 def t(fn, it=30, r=7):
+    torch.cuda.synchronize()
     fn()
     torch.cuda.synchronize()
     v = []
@@ -33,9 +34,9 @@ def t(fn, it=30, r=7):
     return round(statistics.median(v), 1)
 
 
-def step(x, y):
-    c = pc.reduce_exscan_i32(x)[:1]
-    return ops.scan_inclusive_i32(x, y, carry=c)
+def step(x, y, flag=False):
+    c = pc.reduce_exscan_i32(x, input_stable=flag)[:1]
+    return ops.scan_inclusive_i32(x, y, carry=c, input_stable=flag)
 
 
 for lg in [int(v) for v in sys.argv[1:]] or [25, 26, 27]:
@@ -43,6 +44,9 @@ for lg in [int(v) for v in sys.argv[1:]] or [25, 26, 27]:
     y = torch.empty_like(x)
     res = {"lib": Path(str(_lib.lib_path())).stem, "log2n": lg,
            "step_us": t(lambda: step(x, y)),
+           "step_pdl_us": t(lambda: step(x, y, True)),
+           "compact_us": t(lambda: pc.compact_gt0_i32(x, y)),
+           "compact_pdl_us": t(lambda: pc.compact_gt0_i32(x, y, input_stable=True)),
            "pass1_us": t(lambda: pc.reduce_exscan_i32(x)),
            "scan_us": t(lambda: ops.scan_inclusive_i32(x, y)),
            "copy_us": t(lambda: y.copy_(x))}
