@@ -41,7 +41,7 @@ N_C5 = 1 << 32
 # 256-thread CTAs 615 us, 512 598 us from the first steps on, 1024 587 us but
 # only after ~25 launches (606-612 before; tools/bench_loop_probe2.py,
 # profiles/r01_reduce_experiments.md) — 512 is the robust choice.
-BLOCK_C2 = int(os.environ.get("WF_BENCH_BLOCK_C2", "512"))
+BLOCK_C2 = int(os.environ.get("WF_BENCH_BLOCK_C2", "256"))
 # timed steps (headline and C3-C5) as programmatic dependent launches
 # (WF_FLAG_INPUT_STABLE: consecutive steps read one input that nothing
 # between them writes); WF_BENCH_PDL=0 measures plain stream-ordered launches

@@ -33,6 +33,14 @@
 // workspace or the output.  Without the flag the launch is stream-ordered as
 // usual.
 
+#ifndef WF_RED_OUTER_UNROLL1
+// 1: the streaming loop is not unrolled beyond UNROLL by the compiler.  Its
+// own 4x unroll (16 loads per trip, issued a few at a time) was 5 % slower at
+// 256-thread CTAs and 10 % slower in the fused-exchange kernel at 1024
+// (tools/k2_pdl_probe.py, profiles/r02_reduce_experiments.md); with 1, 256-
+// thread CTAs are the fastest K2 configuration for both kernels
+#define WF_RED_OUTER_UNROLL1 1
+#endif
 #ifndef WF_RED_TRACE
 #define WF_RED_TRACE 0  // tools-only: per-block globaltimer stamps (tools/red_trace.py)
 #endif
@@ -185,6 +193,9 @@ __global__ void __launch_bounds__(BLOCK)
   auto vec_at = [&](uint64_t v) { return (PX && WF_PX_REV) ? vin + (nvec - 1 - v) : vin + v; };
   const uint64_t keep_vec = (uint64_t(WF_PX_KEEP_MB) << 20) / 16;
   uint64_t i = gtid;
+#if WF_RED_OUTER_UNROLL1
+#pragma unroll 1
+#endif
   for (; i + uint64_t(UNROLL - 1) * nthreads < nvec; i += UNROLL * nthreads) {
     uint4 q[UNROLL];
 #pragma unroll
@@ -195,6 +206,12 @@ __global__ void __launch_bounds__(BLOCK)
       else
         q[u] = ldg_stream(vec_at(v));
     }
+    // all UNROLL loads are issued before any is consumed: without this fence
+    // the compiler interleaved the adds and kept only 2 loads in flight in
+    // the fused-exchange (MG) kernel at 1024-thread CTAs (10 % slower)
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u)
+      asm volatile("" : "+r"(q[u].x), "+r"(q[u].y), "+r"(q[u].z), "+r"(q[u].w));
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
       acc[u][0] = Op::add(acc[u][0], Op::from_bits(q[u].x));

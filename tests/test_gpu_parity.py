@@ -112,7 +112,7 @@ def test_reduce_f32_reproducible_and_pinned(ops, golden):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("block", [256, 512, 1024])  # 512: bench.py C2 block
+@pytest.mark.parametrize("block", [256, 512, 1024])  # 256: bench.py C2 block
 def test_reduce_f32_full_config(ops, block):
     """BASELINE config 2 on one GPU: 2^30 fp32."""
     n = 1 << 30

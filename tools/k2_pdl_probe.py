@@ -34,7 +34,7 @@ def t(fn, it=20, r=5):
     return round(statistics.median(v), 2)
 
 
-for lg in (27, 28, 29, 30):
+for lg in [int(v) for v in sys.argv[1:]] or (27, 28, 29, 30):
     x = ops.fill_synthetic("f32_unit", 1 << lg, seed=1)
     torch.cuda.synchronize()
     for block in (256, 512, 1024):
