@@ -57,6 +57,29 @@ def ring(chunk_elems):
     return fn
 
 
+s3 = torch.cuda.Stream()
+
+
+def ring_kernel(chunk_elems):
+    """the same ring with a torch kernel (in-place +0 on the chunk, one HBM
+    read + write pass) between each chunk's H2D and its D2H, on a third
+    stream: does any kernel in the ring cost the copies time?"""
+    def fn():
+        for c in range(0, n, chunk_elems):
+            e1, e2 = torch.cuda.Event(), torch.cuda.Event()
+            with torch.cuda.stream(s1):
+                d[c:c + chunk_elems].copy_(hin[c:c + chunk_elems], non_blocking=True)
+                e1.record(s1)
+            s3.wait_event(e1)
+            with torch.cuda.stream(s3):
+                d[c:c + chunk_elems].add_(0)
+                e2.record(s3)
+            s2.wait_event(e2)
+            with torch.cuda.stream(s2):
+                hout[c:c + chunk_elems].copy_(d[c:c + chunk_elems], non_blocking=True)
+    return fn
+
+
 def h2d_only():
     d.copy_(hin, non_blocking=True)
 
@@ -68,6 +91,7 @@ def d2h_only():
 res = {"link_ms": med(link), "h2d_only_ms": med(h2d_only), "d2h_only_ms": med(d2h_only)}
 for mb in (1, 2, 4, 8, 16, 32, 64):
     res[f"ring_{mb}MiB_ms"] = med(ring((mb << 20) // 4))
+res["ring_16MiB_torch_kernel_ms"] = med(ring_kernel((16 << 20) // 4))
 res["scan_host_ms"] = med(lambda: ops.scan_inclusive_i32_host(hin, hout, device=dev))
 res["scan_host_ok"] = bool(torch.equal(hout, ops.scan_inclusive_i32(x).cpu()))
 res["frac_of_link"] = round(res["link_ms"] / res["scan_host_ms"], 4)
