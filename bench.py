@@ -364,12 +364,14 @@ def cpu_baseline_kernel(kind: str, budget_s: float) -> dict:
 
 
 # ---- GPU timing helpers -----------------------------------------------------
-def time_launches(fn, steps: int, warmup: int, flush=None):
+def time_launches(fn, steps: int, warmup: int, flush=None, clocks: dict | None = None):
     """Per-launch times (ms) on the current stream.  Without a flush the
     `steps` launches run back to back between two events (the steady state of
     a stream of calls; inputs larger than L2 need no flush) and the average
     is returned for each; with a flush (C1) every launch is bracketed by its
-    own events right after the L2 flush."""
+    own events right after the L2 flush.  `clocks`: filled with the SM clock
+    summary sampled during the back-to-back loop (K5 on random bytes can hit
+    the board's power cap)."""
     import torch
     torch.cuda.synchronize()  # whatever wrote the inputs has finished (WF_FLAG_INPUT_STABLE)
     for _ in range(warmup):
@@ -379,11 +381,14 @@ def time_launches(fn, steps: int, warmup: int, flush=None):
     torch.cuda.synchronize()
     if flush is None:
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        for _ in range(steps):
-            fn()
-        e.record()
-        torch.cuda.synchronize()
+        with ClockSampler(torch.cuda.current_device()) as clk:
+            s.record()
+            for _ in range(steps):
+                fn()
+            e.record()
+            torch.cuda.synchronize()
+        if clocks is not None:
+            clocks.update(clk.summary())
         return [s.elapsed_time(e) / steps] * steps
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(steps)]
@@ -792,15 +797,19 @@ def per_kernel(args, rank, world, local, dev, peak, checks: dict) -> dict:
     x = ops.fill_synthetic("i32_full", hi - lo, seed=0, base=lo, device=dev)
     y = torch.empty_like(x)
     scan = lambda: wd.scan_inclusive_i32(x, y, peer=pc, input_stable=PDL_STEPS)  # noqa: E731
-    t = time_launches(scan, steps, warm)
+    clk = {}
+    t = time_launches(scan, steps, warm, clocks=clk)
     res["c3_scan_i32"] = stats(t, hi - lo, 8 if world == 1 else 12, N_C3)
+    res["c3_scan_i32"]["clocks"] = clk
     checks["c3_scan_i32"] = check_c3(scan(), x, world, rank)
     log(f"rank {rank}: C4")
     # C4 compaction
     out = torch.empty_like(x)
     compact = lambda: wd.compact_gt0_i32(x, out, peer=pc, input_stable=PDL_STEPS)  # noqa: E731
-    t = time_launches(compact, steps, warm)
+    clk = {}
+    t = time_launches(compact, steps, warm, clocks=clk)
     res["c4_compact_i32"] = stats(t, hi - lo, 6, N_C4)
+    res["c4_compact_i32"]["clocks"] = clk
     checks["c4_compact_i32"] = check_c4(compact(), x, world, rank)
     res["c4_compact_i32"]["bytes_per_elem_note"] = "4 B read + 4 B x selectivity (~0.5) written"
     # also 0 %, 1 % and 100 % selectivity (same n, i32_select)
@@ -829,19 +838,23 @@ def per_kernel(args, rank, world, local, dev, peak, checks: dict) -> dict:
     lo, hi = wd.shard_range(N_C5, rank, world)
     u = ops.fill_synthetic("u8_uniform", hi - lo, seed=0, base=lo, device=dev)
     hist = lambda: wd.histogram256_u8(u, peer=pc, input_stable=PDL_STEPS)  # noqa: E731
-    t = time_launches(hist, steps, warm)
+    clk = {}
+    t = time_launches(hist, steps, warm, clocks=clk)
     res["c5_hist_u8"] = stats(t, hi - lo, 1, N_C5)
+    res["c5_hist_u8"]["clocks"] = clk
     checks["c5_hist_u8"] = check_c5(hist(), u, world)
     # also all-same-value and skewed (geometric) bytes
     variants = {}
     for gen in ("u8_const", "u8_geom"):
         ops.fill_synthetic(gen, hi - lo, seed=0, base=lo, out=u)
-        t = time_launches(hist, steps, warm)
+        clk = {}
+        t = time_launches(hist, steps, warm, clocks=clk)
         ms = statistics.mean(t)
         checks[f"c5_hist_u8/{gen}"] = check_c5(hist(), u, world)
         variants[gen] = {"kernel_us": round(ms * 1e3, 2),
                          "gbs": round((hi - lo) / (ms * 1e-3) / 1e9, 1),
-                         "gelem_s": round(N_C5 / (max_over_ranks(ms, world) * 1e-3) / 1e9, 3)}
+                         "gelem_s": round(N_C5 / (max_over_ranks(ms, world) * 1e-3) / 1e9, 3),
+                         "clocks": clk}
     res["c5_hist_u8"]["data_variants"] = variants
     if world == 1 and not args.headline_only:
         ops.fill_synthetic("u8_uniform", hi - lo, seed=0, base=lo, out=u)
