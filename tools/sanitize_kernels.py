@@ -46,6 +46,20 @@ r += [pc.reduce_exscan_i32(x), pc.compact_gt0_i32(x)[1], pc.histogram256_u8(u),
       pc.exscan_u64(torch.ones(1, dtype=torch.int64, device=dev))]
 kboxes = p2p.Mailboxes.local(1, dev)
 r.append(p2p.PeerReducer(kboxes[0], 0, 1).reduce_sum_f32(f))
+# WF_FLAG_INPUT_STABLE chains (programmatic dependent launches: each launch
+# starts while its predecessor drains, griddepcontrol.wait before the workspace)
+torch.cuda.synchronize()
+y = torch.empty_like(x)
+for _ in range(3):
+    r.append(ops.reduce_sum_f32(f, input_stable=True))
+    r.append(ops.histogram256_u8(u, input_stable=True))
+    ops.scan_inclusive_i32(x, y, input_stable=True)
+    r.append(ops.compact_gt0_i32(x, input_stable=True)[1])
+    r.append(pc.reduce_exscan_i32(x, input_stable=True))
+    ops.scan_inclusive_i32(x, y, carry=r[-1][:1], input_stable=True)
+    r.append(pc.compact_gt0_i32(x, input_stable=True)[1])
+    r.append(pc.histogram256_u8(u, input_stable=True))
+r.append(y)
 torch.cuda.synchronize()
 assert not pc.failed()
 boxes[0].close()
