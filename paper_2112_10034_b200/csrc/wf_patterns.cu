@@ -96,6 +96,55 @@ __global__ void __launch_bounds__(1024) warp_partials_kernel(const uint32_t *__r
         F32 ? __float_as_uint(fs) : is;
 }
 
+// grid * block >= n: every DSL thread sums at most ONE element, so the warp
+// partial of global warp w is the shfl_down tree over elements 32w .. 32w+31
+// (lane value 0 + a[i], 0 past n).  Here 8 lanes hold one 32-element segment
+// as 16-byte vectors (lane j: elements 4j .. 4j+3) and replay the same tree:
+//   off 16: lanes j < 4 add lane j+4 component-wise   (e + 16)
+//   off  8: lanes j < 2 add lane j+2                  (e + 8)
+//   off  4: lane 0 adds lane 1                        (e + 4)
+//   off  2: (c0 + c2), (c1 + c3);  off 1: their sum
+// — the same fp32 additions in the same association, so the bits are the
+// DSL kernel's; persistent grid instead of the DSL's grid * block threads.
+template <bool F32>
+__global__ void __launch_bounds__(256) warp_partials_1pt_kernel(const uint32_t *__restrict__ a,
+                                                                int64_t n, uint32_t nseg,
+                                                                uint32_t *__restrict__ out) {
+  const uint32_t j = threadIdx.x & 7u;  // lane within the segment
+  const uint64_t T = uint64_t(blockDim.x) * gridDim.x / 8;  // segments per grid step
+  for (uint64_t seg = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 8; seg < nseg;
+       seg += T) {
+    const int64_t e0 = int64_t(seg) * 32 + 4 * j;
+    uint4 q;
+    if (e0 + 3 < n) {
+      q = ldg_stream(reinterpret_cast<const uint4 *>(a + e0));
+    } else {
+      q.x = e0 < n ? a[e0] : 0u;
+      q.y = e0 + 1 < n ? a[e0 + 1] : 0u;
+      q.z = e0 + 2 < n ? a[e0 + 2] : 0u;
+      q.w = 0u;
+    }
+    if (F32) {
+      float v[4] = {__fadd_rn(0.0f, __uint_as_float(q.x)), __fadd_rn(0.0f, __uint_as_float(q.y)),
+                    __fadd_rn(0.0f, __uint_as_float(q.z)), __fadd_rn(0.0f, __uint_as_float(q.w))};
+#pragma unroll
+      for (int d = 4; d >= 1; d >>= 1) {  // element offsets 16, 8, 4
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float o = __shfl_down_sync(kFull, v[c], d, 8);
+          if (j < uint32_t(d)) v[c] = __fadd_rn(v[c], o);
+        }
+      }
+      if (j == 0) out[seg] = __float_as_uint(__fadd_rn(__fadd_rn(v[0], v[2]), __fadd_rn(v[1], v[3])));
+    } else {
+      uint32_t t = q.x + q.y + q.z + q.w;  // i32 wrap: any order is the same value
+#pragma unroll
+      for (int d = 4; d >= 1; d >>= 1) t += __shfl_down_sync(kFull, t, d, 8);
+      if (j == 0) out[seg] = t;
+    }
+  }
+}
+
 // 8 lanes per 32-element segment, 4 elements per lane (one 16-byte load),
 // kPrefixVec vectors per thread per iteration (all loads issued first),
 // grid-stride over the n/4 vectors; width-8 SHFL.UP scan of the lane totals.
@@ -176,6 +225,18 @@ cudaError_t launch_warp_partials(bool f32, const void *a, int64_t n, void *out, 
   if (grid == 0) return cudaSuccess;
   const auto *in = static_cast<const uint32_t *>(a);
   auto *o = static_cast<uint32_t *>(out);
+  const int64_t threads = int64_t(grid) * block;
+  if (threads >= n && (reinterpret_cast<uintptr_t>(a) & 15u) == 0) {  // one element per DSL thread
+    const uint32_t nseg = uint32_t(threads / 32);  // every warp of the DSL grid writes its partial
+    const uint64_t want = (uint64_t(nseg) * 8 + 255) / 256;
+    const uint64_t cap = uint64_t(sm_count(current_device())) * 8;
+    const unsigned g = unsigned(want < cap ? want : cap);
+    if (f32)
+      warp_partials_1pt_kernel<true><<<g, 256, 0, s>>>(in, n, nseg, o);
+    else
+      warp_partials_1pt_kernel<false><<<g, 256, 0, s>>>(in, n, nseg, o);
+    return cudaGetLastError();
+  }
   if (f32)
     warp_partials_kernel<true><<<grid, block, 0, s>>>(in, n, o);
   else

@@ -94,7 +94,24 @@ def test_warp_prefix_reference_pin(wf, calls):
 CASES = [  # (n, grid, block): ragged n, n < threads, n = 0, negative n, big blocks
     (1, 1, 32), (31, 1, 64), (1000, 3, 96), (4097, 7, 256), ((1 << 20) + 3, 64, 256),
     ((1 << 20), 4096, 256), (123457, 148, 1024), (0, 5, 128), (-7, 2, 64), (5000, 1, 32),
+    # one element per DSL thread (the vectorised native path): ragged last
+    # segment, whole warps past n, n a multiple of 4 but not of 32
+    (100, 2, 64), ((1 << 20) - 5, 4096, 256), (4100, 33, 128), (999, 40, 32),
 ]
+
+
+def test_partials_one_element_per_thread_special_values(wf, calls):
+    """The vectorised one-element-per-thread path replays the DSL's fp32
+    adds exactly: -0.0 (0 + -0.0 = +0.0), infinities and NaN included."""
+    vals = torch.tensor([-0.0, 1.5, float("inf"), -2.25, float("-inf"), 3.0e38, 3.0e38, -1e-45,
+                         float("nan"), 0.1, -0.0, 7.0], dtype=torch.float32)
+
+    def fill(t):
+        t.copy_(vals.repeat(t.numel() // vals.numel() + 1)[:t.numel()].to(t.device))
+    for n, grid, block in ((12, 1, 32), (1000, 40, 32), (4096 + 7, 20, 256)):
+        got = _partials(wf, SRC["C1_F32"], "f32", n, grid, block, fill)
+        want = _partials(wf, SRC["C1_F32"], "f32", n, grid, block, fill, generic=True)
+        assert torch.equal(got.view(torch.int32), want.view(torch.int32)), n
 
 
 @pytest.mark.parametrize("n,grid,block", CASES)
