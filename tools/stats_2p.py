@@ -1,3 +1,6 @@
+# ROUND-1 RECORD: drove the runtime switch WF_SCAN_2P, which round 2 removed from the
+# product library; the two-pass kernels now build only as variants
+# (python tools/build_variants.py tp="-DWF_SCAN_IMPL=3"), selected with WF_LIB.
 """Where does the two-pass kernel's time go?  Needs a -DWF_2P_STATS=1 build
 (WF_LIB=...).  Prints per-launch wait statistics at 2^28 for scan and compaction."""
 import ctypes

@@ -1,3 +1,6 @@
+# ROUND-1 RECORD: used runtime switches (WF_SCAN_2P / WF_SCAN_TMEM) that round 2
+# removed from the product library; the round-1 kernels build only as variants
+# (tools/build_variants.py with -DWF_SCAN_IMPL=1|2|3), selected with WF_LIB.
 mkdir -p gpurun_out
 for v in st_l1 st_l2; do for c in 256 512; do WF_2P_CHUNK_TILES=$c WF_LIB=build/variants/lib_$v.so timeout 100 python tools/stats_2p.py; done; done > gpurun_out/stats_2p.log 2>&1
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct

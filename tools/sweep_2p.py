@@ -1,3 +1,6 @@
+# ROUND-1 RECORD: drove the runtime switch WF_SCAN_2P, which round 2 removed from the
+# product library; the two-pass kernels now build only as variants
+# (python tools/build_variants.py tp="-DWF_SCAN_IMPL=3"), selected with WF_LIB.
 """Two-pass (L2-streamed) vs single-pass scan/compaction: correctness at ragged
 sizes and CUDA-event timing at 2^28, over chunk sizes (WF_2P_CHUNK_TILES) and
 library variants (WF_LIB).  Usage: python tools/sweep_2p.py [chunks...]"""

@@ -1,3 +1,6 @@
+# ROUND-1 RECORD: used runtime switches (WF_SCAN_2P / WF_SCAN_TMEM) that round 2
+# removed from the product library; the round-1 kernels build only as variants
+# (tools/build_variants.py with -DWF_SCAN_IMPL=1|2|3), selected with WF_LIB.
 mkdir -p gpurun_out
 timeout 300 python tools/sweep_2p.py 64 128 256 > gpurun_out/sweep_2p.log 2>&1
 for v in lead1k lead512 gap256 gap64; do WF_LIB=build/variants/lib_$v.so timeout 200 python tools/sweep_2p.py 128 >> gpurun_out/sweep_2p.log 2>&1; done

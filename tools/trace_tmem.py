@@ -85,6 +85,15 @@ for op, sel in jobs:
                       "parked_wait_lb": int(((t[:, 2] <= m) & (t[:, 5] > m)).sum()),
                       "in_lookback": int(((t[:, 5] <= m) & (t[:, 3] > m)).sum()),
                       "wait_finish": int(((t[:, 3] <= m) & (t[:, 4] > m)).sum())}}
+    # fill / drain: when the pipeline's fronts reach their ends, relative to
+    # the first claim (all in us)
+    res["fronts_us"] = {"first_land": round(float(t[:, 1].min()), 2),
+                        "first_finish": round(float(t[:, 4].min()), 2),
+                        "last_claim": round(float(t[:, 0].max()), 2),
+                        "last_land": round(float(t[:, 1].max()), 2),
+                        "last_park": round(float(t[:, 2].max()), 2),
+                        "last_prefix": round(float(t[:, 3].max()), 2),
+                        "end": round(float(t[:, 4].max()), 2)}
     # how far behind the claim front is the prefix front, in tiles, at mid-run
     res["at_mid"]["claimed"] = int((t[:, 0] <= m).sum())
     res["at_mid"]["prefix_known"] = int((t[:, 3] <= m).sum())
