@@ -37,8 +37,8 @@
 // 1: the streaming loop is not unrolled beyond UNROLL by the compiler.  Its
 // own 4x unroll (16 loads per trip, issued a few at a time) was 5 % slower at
 // 256-thread CTAs and 10 % slower in the fused-exchange kernel at 1024
-// (tools/k2_pdl_probe.py, profiles/r02_reduce_experiments.md); with 1, 256-
-// thread CTAs are the fastest K2 configuration for both kernels
+// (tools/k2_pdl_probe.py, profiles/r01_reduce_experiments.md "Round 2"); with
+// 1, 256-thread CTAs are the fastest K2 configuration for both kernels
 #define WF_RED_OUTER_UNROLL1 1
 #endif
 #ifndef WF_RED_TRACE
@@ -206,9 +206,8 @@ __global__ void __launch_bounds__(BLOCK)
       else
         q[u] = ldg_stream(vec_at(v));
     }
-    // all UNROLL loads are issued before any is consumed: without this fence
-    // the compiler interleaved the adds and kept only 2 loads in flight in
-    // the fused-exchange (MG) kernel at 1024-thread CTAs (10 % slower)
+    // keep the trip's UNROLL loads ahead of their adds (the compiler may not
+    // consume a load before the last one of the trip is issued)
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u)
       asm volatile("" : "+r"(q[u].x), "+r"(q[u].y), "+r"(q[u].z), "+r"(q[u].w));
