@@ -687,6 +687,7 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
           }
         }
       }
+#if !WF_TM_SWEEP  // (sweeper builds: the sweeper publishes the count, below)
       if constexpr (PX) {
         if (COMPACT && t == ntiles - 1 && q == 0 && h == 0) {
           const uint64_t total = uint64_t(prefix) + agg;
@@ -696,6 +697,7 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       } else {
         if (COMPACT && t == ntiles - 1 && q == 0 && h == 0 && lane == 0) *count = uint64_t(prefix) + agg;
       }
+#endif
       if (q == 0 && h == 0 && lane == 0) TM_STAMP(t, 4);
 #if WF_TM_PROF
       PROF_T(f5);
@@ -836,6 +838,20 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
           run += __shfl_sync(kFull, sc[k], 31);
         }
         f += ready;
+      }
+      // compaction: once the last tile is swept, `run` is the selected count
+      // (< 2^32: n < 2^32 per call).  Publish it — and run the sharded
+      // offset exchange — here, while the finishers still store the last
+      // parked tiles: the exchange's fence + flag round trip hides in that
+      // drain instead of following it (2^25 shard: the finishers' drain is
+      // ~5 us, tools/trace_tmem.py)
+      if constexpr (COMPACT) {
+        if constexpr (PX) {
+          if (lane == 0) *count = run;
+          peer_exscan_warp(uint64_t(run), count + 1, pa);
+        } else if (lane == 0) {
+          *count = run;
+        }
       }
     }
   }
