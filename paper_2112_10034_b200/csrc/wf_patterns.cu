@@ -152,10 +152,13 @@ __global__ void __launch_bounds__(256) warp_partials_1pt_kernel(const uint32_t *
 #define WF_PREFIX_VEC 4
 #endif
 #ifndef WF_PREFIX_CTAS
-#define WF_PREFIX_CTAS 16  // CTAs per SM the grid is sized for (8: 361 us, 16: 345 us at 2^28; tools/patterns_probe.py)
+#define WF_PREFIX_CTAS 32  // CTAs per SM the grid is sized for (8 / 16 / 32: 361 / 345-349 / 339 us at 2^28; tools/patterns_probe.py)
 #endif
 constexpr int kPrefixVec = WF_PREFIX_VEC;
-__global__ void __launch_bounds__(256) warp_prefix32_vec_kernel(const uint4 *__restrict__ a,
+#ifndef WF_PREFIX_MINB
+#define WF_PREFIX_MINB 1  // resident CTAs the register budget must allow
+#endif
+__global__ void __launch_bounds__(256, WF_PREFIX_MINB) warp_prefix32_vec_kernel(const uint4 *__restrict__ a,
                                                                 uint4 *__restrict__ out,
                                                                 uint64_t nvec) {
   const uint32_t sl = threadIdx.x & 7u;  // lane within the segment
