@@ -91,6 +91,10 @@
 #define WF_TM_PREFETCH 1  // L2 prefetch of the first S tiles per CTA before griddepcontrol.wait
 #endif
 
+#ifndef WF_CMP_PK
+#define WF_CMP_PK 1  // compaction: aggregators hand the packed per-chunk counts to the finishers
+#endif
+
 #ifndef WF_CMP_STCS
 #define WF_CMP_STCS 0  // 1: compaction stores with the streaming (.cs) hint
 #endif
@@ -263,6 +267,15 @@ struct TmShared {
   uint32_t item_seq[2 * P];
   uint32_t item_posted[2 * P];  // waiter: item whose prefix was posted at this ring entry
   uint32_t slot_wtot[P][4][2];  // per tile quarter and half
+#if WF_CMP_PK
+  // compaction: each lane's selected count per 128-element chunk (0-4), 4
+  // chunks per byte-packed word, written by the aggregators with the slot so
+  // the finisher does not recount: [slot][quarter][half * TMUL + m][word][lane]
+  // (0-4 % selectivity 172 -> 162 us, 1 % 200 -> 181 us, 50 % unchanged at
+  // 2^28; also moving the pair of warp scans into the aggregators made them
+  // the slower stage: 50 % 241 -> 250 us, tools/c4_sel_probe.py)
+  uint32_t slot_pk[P][4][2 * TMUL][2][32];
+#endif
   uint32_t tmem_base;
   uint32_t epoch;
 };
@@ -473,7 +486,7 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       for (int h = 0; h < 2; ++h) {
 #pragma unroll
         for (int m = 0; m < TMUL; ++m) {
-          uint32_t v[32], sum = 0;
+          uint32_t v[32], sum = 0, pk[2] = {0u, 0u};
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             uint4 x = *reinterpret_cast<const uint4 *>(stage + (8 * (TMUL * h + m) + j) * 128);
@@ -485,12 +498,22 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
               if (head > 2) x.z = 0;
             }
             v[4 * j] = x.x; v[4 * j + 1] = x.y; v[4 * j + 2] = x.z; v[4 * j + 3] = x.w;
-            if (COMPACT)
-              sum += (int32_t(x.x) > 0) + (int32_t(x.y) > 0) + (int32_t(x.z) > 0) + (int32_t(x.w) > 0);
-            else
+            if (COMPACT) {
+              const uint32_t c = (int32_t(x.x) > 0) + (int32_t(x.y) > 0) + (int32_t(x.z) > 0) +
+                                 (int32_t(x.w) > 0);
+              sum += c;
+              pk[j >> 2] |= c << (8 * (j & 3));
+            } else {
               sum += x.x + x.y + x.z + x.w;
+            }
           }
           tmem_st32(tcol + uint32_t(p) * SLOT_COLS + 32u * (TMUL * h + m), v);
+#if WF_CMP_PK
+          if (COMPACT) {
+            sh.slot_pk[p][q][TMUL * h + m][0][lane] = pk[0];
+            sh.slot_pk[p][q][TMUL * h + m][1][lane] = pk[1];
+          }
+#endif
           hsum[h] += sum;
         }
       }
@@ -579,6 +602,16 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       uint32_t v[TMUL][32];
 #pragma unroll
       for (int m = 0; m < TMUL; ++m) tmem_ld32(tcol + uint32_t(p) * SLOT_COLS + 32u * (TMUL * h + m), v[m]);
+#if WF_CMP_PK
+      uint32_t pkm[TMUL][2];
+      if (COMPACT) {  // read before the slot is freed (the next item rewrites it)
+#pragma unroll
+        for (int m = 0; m < TMUL; ++m) {
+          pkm[m][0] = sh.slot_pk[p][q][TMUL * h + m][0][lane];
+          pkm[m][1] = sh.slot_pk[p][q][TMUL * h + m][1][lane];
+        }
+      }
+#endif
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive1(&sh.freed[p]);
@@ -621,6 +654,9 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
           // 64 POPC per tile eighth took ~1150 cycles of the finisher's
           // ~2000 per tile (WF_TM_PROF), the finisher being the pipeline's
           // slowest stage.
+#if WF_CMP_PK
+          const uint32_t pk[2] = {pkm[m][0], pkm[m][1]};  // counted by the aggregator
+#else
           uint32_t pk[2] = {0u, 0u};
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -629,6 +665,7 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
                                (int32_t(x[3]) > 0);
             pk[j >> 2] |= c << (8 * (j & 3));
           }
+#endif
           uint32_t inc[2] = {pk[0], pk[1]};
 #pragma unroll
           for (int d = 1; d < 32; d <<= 1) {
