@@ -95,6 +95,10 @@
 #define WF_CMP_PK 1  // compaction: aggregators hand the packed per-chunk counts to the finishers
 #endif
 
+#ifndef WF_CMP_CHUNK_SKIP
+#define WF_CMP_CHUNK_SKIP 1  // compaction: skip the stores of chunks with nothing selected (uniform branch)
+#endif
+
 #ifndef WF_CMP_STCS
 #define WF_CMP_STCS 0  // 1: compaction stores with the streaming (.cs) hint
 #endif
@@ -619,6 +623,9 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       const bool full = vec_out && uint64_t(t + 1) * TM_TILE <= n && (t > 0 || head == 0);
       const uint64_t base0 = uint64_t(t) * TM_TILE + q * (QVEC * 128) + (8 * TMUL * h) * 128 + lane * 4;
       uint32_t loc[TMUL][8];  // scan: chunk add (local); compaction: chunk write position (local)
+      uint32_t nzc[TMUL];  // compaction: bit j = chunk j of the eighth has a selected element
+#pragma unroll
+      for (int m = 0; m < TMUL; ++m) nzc[m] = 0u;
       uint32_t run = 0;
 #pragma unroll
       for (int m = 0; m < TMUL; ++m) {
@@ -680,7 +687,10 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
           for (int j = 0; j < 8; ++j) {
             const uint32_t sh8 = 8 * (j & 3);
             loc[m][j] = run + (((inc[j >> 2] - pk[j >> 2]) >> sh8) & 0xffu);
-            run += (tot[j >> 2] >> sh8) & 0xffu;
+            const uint32_t cj = (tot[j >> 2] >> sh8) & 0xffu;
+            run += cj;
+            nzc[m] |= uint32_t(cj != 0u) << j;  // warp-uniform
+            if (!WF_CMP_CHUNK_SKIP && cj != 0u) nzc[m] = 0xffu;  // A/B: the whole eighth
           }
         }
       }
@@ -710,7 +720,8 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
               for (int k = 0; k < 4; ++k)
                 if (e + k < n && e + k >= head) out[e + k] = int32_t(x[k] + add);
             }
-          } else if (run != 0) {  // warp-uniform: nothing selected in this eighth, nothing to store
+          } else if ((nzc[m] >> j) & 1u) {
+            // warp-uniform: nothing selected in this eighth / chunk, nothing to store
             uint32_t pos = off + loc[m][j];
 #pragma unroll
             for (int k = 0; k < 4; ++k)
