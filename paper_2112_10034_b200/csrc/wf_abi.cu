@@ -232,7 +232,7 @@ int wf_reduce_sum_i32(const int32_t *in, uint64_t n, int32_t *out, int block, in
                       void *ws, size_t ws_bytes, wf_stream_t stream) {
   int rc = reduce_common(WF_OP_REDUCE_SUM_I32, in, n, out, block, grid, ws, ws_bytes);
   if (rc) return rc;
-  if (grid == 0) grid = auto_reduce_grid(false, block, n);
+  if (grid == 0) grid = auto_reduce_grid(kRedI32, block, n);
   return cuda_status(launch_reduce_i32(in, n, out, block, grid, ws, static_cast<cudaStream_t>(stream)),
                      "reduce_sum_i32");
 }
@@ -247,7 +247,7 @@ int wf_reduce_sum_f32_ex(const float *in, uint64_t n, float *out, int block, int
   if (flags & ~unsigned(WF_FLAG_INPUT_STABLE)) return fail(WF_ERR_ARG, "unknown flags 0x%x", flags);
   int rc = reduce_common(WF_OP_REDUCE_SUM_F32, in, n, out, block, grid, ws, ws_bytes);
   if (rc) return rc;
-  if (grid == 0) grid = auto_reduce_grid(true, block, n);
+  if (grid == 0) grid = auto_reduce_grid(kRedF32, block, n);
   return cuda_status(launch_reduce_f32(in, n, out, block, grid, ws, static_cast<cudaStream_t>(stream),
                                        (flags & WF_FLAG_INPUT_STABLE) != 0),
                      "reduce_sum_f32");
@@ -320,7 +320,7 @@ int wf_reduce_sum_f32_mg_ex(const float *in, uint64_t n, float *out, int block, 
   if (world < 1 || world > 32 || rank < 0 || rank >= world)
     return fail(WF_ERR_ARG, "rank %d / world %d out of range (world <= 32)", rank, world);
   if (epoch == 0) return fail(WF_ERR_ARG, "epoch must start at 1");
-  if (grid == 0) grid = auto_reduce_grid(true, block, n);
+  if (grid == 0) grid = auto_reduce_grid(kRedF32Mg, block, n);
   return cuda_status(launch_reduce_f32_mg(in, n, out, block, grid, ws, d_peers, d_mailbox, rank,
                                           world, epoch, (flags & WF_FLAG_INPUT_STABLE) != 0,
                                           static_cast<cudaStream_t>(stream)),
@@ -370,7 +370,7 @@ int wf_reduce_sum_i32_exscan_mg_ex(const int32_t *in, uint64_t n, int32_t *d_out
   if (rc) return rc;
   rc = check_peer(d_peers, d_mailbox, cap, 1, rank, world, epoch, d_err);
   if (rc) return rc;
-  if (grid == 0) grid = auto_reduce_grid(false, block, n);
+  if (grid == 0) grid = auto_reduce_grid(kRedI32Px, block, n);
   return cuda_status(launch_reduce_i32_exscan_mg(in, n, d_out2, block, grid, ws, d_peers,
                                                  d_mailbox, cap, rank, world, epoch, d_err,
                                                  static_cast<cudaStream_t>(stream),
@@ -643,7 +643,7 @@ int wf_reduce_sum_f32_host(const float *host_in, uint64_t n, float *host_out, vo
   return reduce_host<float>(
       WF_OP_REDUCE_SUM_F32, host_in, n, host_out, staging, staging_bytes, ws, ws_bytes, stream,
       [&](const float *d, uint64_t cnt, float *o, cudaStream_t s) {
-        return launch_reduce_f32(d, cnt, o, 512, auto_reduce_grid(true, 512, cnt), ws, s);
+        return launch_reduce_f32(d, cnt, o, 512, auto_reduce_grid(kRedF32, 512, cnt), ws, s);
       },
       [](const float *v, uint32_t c, float *o, cudaStream_t s) { return launch_fold_f32(v, c, o, s); });
 }
@@ -653,7 +653,7 @@ int wf_reduce_sum_i32_host(const int32_t *host_in, uint64_t n, int32_t *host_out
   return reduce_host<int32_t>(
       WF_OP_REDUCE_SUM_I32, host_in, n, host_out, staging, staging_bytes, ws, ws_bytes, stream,
       [&](const int32_t *d, uint64_t cnt, int32_t *o, cudaStream_t s) {
-        return launch_reduce_i32(d, cnt, o, 256, auto_reduce_grid(false, 256, cnt), ws, s);
+        return launch_reduce_i32(d, cnt, o, 256, auto_reduce_grid(kRedI32, 256, cnt), ws, s);
       },
       [](const int32_t *v, uint32_t c, int32_t *o, cudaStream_t s) { return launch_fold_i32(v, c, o, s); });
 }

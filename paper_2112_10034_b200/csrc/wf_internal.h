@@ -77,7 +77,9 @@ cudaError_t launch_reduce_i32(const int32_t *in, uint64_t n, int32_t *out,
 cudaError_t launch_reduce_f32(const float *in, uint64_t n, float *out,
                               int block, int grid, void *ws, cudaStream_t s,
                               bool early = false);
-int auto_reduce_grid(bool is_f32, int block, uint64_t n);
+// grid for the reduce kernel of `kind` (its own occupancy x SMs, capped by n)
+enum { kRedI32 = 0, kRedF32 = 1, kRedF32Mg = 2, kRedI32Px = 3 };
+int auto_reduce_grid(int kind, int block, uint64_t n);
 cudaError_t launch_reduce_f32_mg(const float *in, uint64_t n, float *out, int block, int grid,
                                  void *ws, void *const *peers, const void *mine, int rank,
                                  int world, uint32_t epoch, bool early, cudaStream_t s);

@@ -193,14 +193,11 @@ __global__ void __launch_bounds__(BLOCK)
   auto vec_at = [&](uint64_t v) { return (PX && WF_PX_REV) ? vin + (nvec - 1 - v) : vin + v; };
   const uint64_t keep_vec = (uint64_t(WF_PX_KEEP_MB) << 20) / 16;
   uint64_t i = gtid;
-#if WF_RED_OUTER_UNROLL1
-#pragma unroll 1
-#endif
-  for (; i + uint64_t(UNROLL - 1) * nthreads < nvec; i += UNROLL * nthreads) {
+  auto trip = [&](uint64_t i0) {  // UNROLL vectors per thread
     uint4 q[UNROLL];
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
-      const uint64_t v = i + u * nthreads;
+      const uint64_t v = i0 + u * nthreads;
       if (PX && WF_PX_KEEP_MB > 0)  // read last = the scan's first reads: keep; the rest: evict first
         q[u] = v + keep_vec >= nvec ? ldg_keep(vec_at(v)) : ldg_evict_first(vec_at(v));
       else
@@ -218,6 +215,15 @@ __global__ void __launch_bounds__(BLOCK)
       acc[u][2] = Op::add(acc[u][2], Op::from_bits(q[u].z));
       acc[u][3] = Op::add(acc[u][3], Op::from_bits(q[u].w));
     }
+  };
+  if constexpr (PX || !WF_RED_OUTER_UNROLL1) {
+    // (the sharded scan's pass 1 keeps the compiler's unroll: with its
+    // reversed, hinted loads it is 14 % faster that way, 23.3 vs 27.1 us
+    // per 2^25 shard, tools/c3_shard_probe.py)
+    for (; i + uint64_t(UNROLL - 1) * nthreads < nvec; i += UNROLL * nthreads) trip(i);
+  } else {
+#pragma unroll 1
+    for (; i + uint64_t(UNROLL - 1) * nthreads < nvec; i += UNROLL * nthreads) trip(i);
   }
 #pragma unroll
   for (int u = 0; u < UNROLL; ++u) {  // remainder: < UNROLL vectors left
@@ -415,21 +421,28 @@ cudaError_t launch_reduce(const typename Op::elem_t *in, uint64_t n,
   }
 }
 
-template <class Op, int BLOCK>
+// Resident blocks per SM of the instantiation a launch actually uses (plain,
+// dependent and fused forms differ in registers: sizing the sharded scan's
+// pass-1 kernel from the plain K1's occupancy gave it two waves, 27 vs 23 us
+// per 2^25 shard); the smaller of the stream-ordered and dependent forms.
+template <class Op, int BLOCK, bool MG, bool PX>
 int occupancy_blocks() {
-  int b = 0;
+  int b0 = 0, b1 = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &b, reduce_kernel<Op, BLOCK, kUnroll>, BLOCK, 0);
+      &b0, reduce_kernel<Op, BLOCK, kUnroll, MG, PX, false>, BLOCK, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &b1, reduce_kernel<Op, BLOCK, kUnroll, MG, PX, true>, BLOCK, 0);
+  const int b = b0 < b1 ? b0 : b1;
   return b > 0 ? b : 1;
 }
 
-template <class Op>
+template <class Op, bool MG, bool PX>
 int resident_blocks(int block) {
   switch (block) {
-    case 128: return occupancy_blocks<Op, 128>();
-    case 256: return occupancy_blocks<Op, 256>();
-    case 512: return occupancy_blocks<Op, 512>();
-    default: return occupancy_blocks<Op, 1024>();
+    case 128: return occupancy_blocks<Op, 128, MG, PX>();
+    case 256: return occupancy_blocks<Op, 256, MG, PX>();
+    case 512: return occupancy_blocks<Op, 512, MG, PX>();
+    default: return occupancy_blocks<Op, 1024, MG, PX>();
   }
 }
 
@@ -504,12 +517,26 @@ cudaError_t launch_reduce_f32_mg(const float *in, uint64_t n, float *out, int bl
   }
 }
 
-int auto_reduce_grid(bool is_f32, int block, uint64_t n) {
-  static int cache[2][11] = {};
+int auto_reduce_grid(int kind, int block, uint64_t n) {
+  static int cache[4][11] = {};
   const int lg = block == 128 ? 7 : block == 256 ? 8 : block == 512 ? 9 : 10;
-  int &per_sm = cache[is_f32][lg];
-  if (per_sm == 0) per_sm = is_f32 ? resident_blocks<SumF32>(block)
-                                   : resident_blocks<SumI32>(block);
+  int &per_sm = cache[kind & 3][lg];
+  if (per_sm == 0) {
+    switch (kind) {
+      case kRedI32: per_sm = resident_blocks<SumI32, false, false>(block); break;
+      case kRedF32:
+      case kRedF32Mg: {
+        // one grid for the plain and the fused-exchange K2: the fp32
+        // association depends on the grid, and the fused result must be
+        // bit-identical to the NCCL path's (plain K2 per rank + fold)
+        const int a = resident_blocks<SumF32, false, false>(block);
+        const int b = resident_blocks<SumF32, true, false>(block);
+        per_sm = a < b ? a : b;
+        break;
+      }
+      default: per_sm = resident_blocks<SumI32, false, true>(block); break;  // kRedI32Px
+    }
+  }
   uint64_t full = uint64_t(per_sm) * uint64_t(sm_count(current_device()));
   if (full > kMaxReduceGrid) full = kMaxReduceGrid;
   // enough blocks that each thread issues at least one UNROLL batch
