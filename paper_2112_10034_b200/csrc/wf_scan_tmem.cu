@@ -227,6 +227,7 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
 __device__ __forceinline__ void tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
+// issue only: the registers are valid after tmem_wait_ld()
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
@@ -240,7 +241,19 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         "=r"(v[31])
       : "r"(taddr)
       : "memory");
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// completes the loads issued by tmem_ld32; the registers are operands so no
+// use of them can be scheduled before the wait
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&v)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                 "+r"(v[6]), "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]),
+                 "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]), "+r"(v[16]), "+r"(v[17]),
+                 "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]),
+                 "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]),
+                 "+r"(v[30]), "+r"(v[31])
+               :
+               : "memory");
 }
 
 // named barrier over the 128 aggregator threads (id 1; id 0 is __syncthreads)
@@ -599,13 +612,14 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       // it: read the slot (metadata + TMEM), free it at once — the tile now
       // waits in this warp's registers, not in TMEM — and do the local scan /
       // ballot positions
+      uint32_t v[TMUL][32];
+#pragma unroll
+      for (int m = 0; m < TMUL; ++m) tmem_ld32(tcol + uint32_t(p) * SLOT_COLS + 32u * (TMUL * h + m), v[m]);
+      // the slot's shared metadata is read while the TMEM load is in flight
       uint32_t wexcl = h ? sh.slot_wtot[p][q][0] : 0u;
 #pragma unroll
       for (uint32_t w = 0; w < 4; ++w) wexcl += w < q ? sh.slot_wtot[p][w][0] + sh.slot_wtot[p][w][1] : 0u;
       const uint32_t agg = sh.slot_agg[p];
-      uint32_t v[TMUL][32];
-#pragma unroll
-      for (int m = 0; m < TMUL; ++m) tmem_ld32(tcol + uint32_t(p) * SLOT_COLS + 32u * (TMUL * h + m), v[m]);
 #if WF_CMP_PK
       uint32_t pkm[TMUL][2];
       if (COMPACT) {  // read before the slot is freed (the next item rewrites it)
@@ -616,6 +630,8 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
         }
       }
 #endif
+#pragma unroll
+      for (int m = 0; m < TMUL; ++m) tmem_wait_ld(v[m]);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive1(&sh.freed[p]);
