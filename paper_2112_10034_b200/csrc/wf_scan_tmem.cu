@@ -162,7 +162,7 @@ constexpr int W_SWEEP = W_PROD + 1;       // prefix sweeper (CTA 0 only; WF_TM_S
 #endif
 constexpr int NAG = WF_TM_NAG;
 constexpr int W_AGG2 = ((W_PROD + 1 + 3) / 4) * 4;  // 2nd group: warp % 4 = TMEM lane quarter
-constexpr int TM_THREADS = (NAG == 2 ? W_AGG2 + 4 : W_PROD + 1) * 32;
+constexpr int TM_THREADS = (NAG == 2 ? W_AGG2 + 4 : (WF_TM_SWEEP ? W_SWEEP + 1 : W_PROD + 1)) * 32;
 constexpr uint32_t kExitOnly = 0xfffffffdu;  // second stop item (NAG = 2): just leave
 #ifndef WF_TM_TMUL
 #define WF_TM_TMUL 1  // tile = 32 KiB x TMUL
@@ -177,7 +177,7 @@ constexpr uint32_t kBatch = WF_TM_BATCH;
 constexpr uint32_t kNoItem = 0xffffffffu;  // item_seq before the first publish
 static_assert((P & (P - 1)) == 0 && TM_COLS <= 512, "TMEM slots: power of two, <= 512 cols");
 static_assert(NLB >= 1 && NLB <= P, "look-back warps must not outnumber TMEM slots");
-static_assert(!WF_TM_SWEEP || (NLB == 1 && NAG == 2 && W_SWEEP < W_AGG2),
+static_assert(!WF_TM_SWEEP || (NLB == 1 && (NAG == 1 || W_SWEEP < W_AGG2)),
               "the sweeper warp sits in the gap before the second aggregator group");
 // stop items: one per look-back warp and one per finisher group
 constexpr int NSTOP = NLB > NFG ? NLB : NFG;
