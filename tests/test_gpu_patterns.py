@@ -125,7 +125,10 @@ def test_partials_native_equals_generic(wf, calls, n, grid, block, src, kind, ge
     assert torch.equal(got.view(torch.int32), want.view(torch.int32))
 
 
-@pytest.mark.parametrize("grid,block", [(1, 32), (3, 96), (148, 256), (4096, 256), (5, 1024)])
+@pytest.mark.parametrize("grid,block", [(1, 32), (3, 96), (148, 256), (4096, 256), (5, 1024),
+                                        # larger grids: multi-wave, odd grids, big blocks
+                                        (4096, 256 + 32), (4096 + 37, 256), (33000, 32),
+                                        (1200, 1024)])
 def test_warp_prefix_native_equals_generic(wf, calls, grid, block):
     n = grid * block
     res = []
