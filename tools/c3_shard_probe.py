@@ -34,8 +34,11 @@ def t(fn, it=30, r=7):
     return round(statistics.median(v), 1)
 
 
+P1_BLOCK = int(__import__("os").environ.get("WF_P1_BLOCK", "256"))
+
+
 def step(x, y, flag=False):
-    c = pc.reduce_exscan_i32(x, input_stable=flag)[:1]
+    c = pc.reduce_exscan_i32(x, block=P1_BLOCK, input_stable=flag)[:1]
     return ops.scan_inclusive_i32(x, y, carry=c, input_stable=flag)
 
 
@@ -47,7 +50,8 @@ for lg in [int(v) for v in sys.argv[1:]] or [25, 26, 27]:
            "step_pdl_us": t(lambda: step(x, y, True)),
            "compact_us": t(lambda: pc.compact_gt0_i32(x, y)),
            "compact_pdl_us": t(lambda: pc.compact_gt0_i32(x, y, input_stable=True)),
-           "pass1_us": t(lambda: pc.reduce_exscan_i32(x)),
+           "pass1_block": P1_BLOCK,
+           "pass1_us": t(lambda: pc.reduce_exscan_i32(x, block=P1_BLOCK)),
            "scan_us": t(lambda: ops.scan_inclusive_i32(x, y)),
            "copy_us": t(lambda: y.copy_(x))}
     want = torch.cumsum(x.to(torch.int64), 0).to(torch.int32)
