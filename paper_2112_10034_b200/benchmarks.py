@@ -20,6 +20,11 @@ three questions become
            every rank of the process group (launch under torchrun for
            1/2/4/8 GPUs): device time, max over ranks — the 1/2/4/8-GPU
            curve that replaces the reference's worker sweep.
+  shards   the same curve predicted on ONE GPU: the per-rank step of each
+           sharded op at the 1/2/4/8-GPU shard sizes, run with the fused
+           kernels on a world-1 mailbox (the exchange protocol executes; the
+           NVLink round trip, ~1-2 us, does not), steps as dependent
+           launches; speed-up = t(1 GPU) / t(N)  (bench_shards).
 
 All inputs are synthetic (``ops.fill_synthetic``) and generated in HBM.
 """
@@ -316,3 +321,91 @@ def bench_scaling(ops_=("reduce_sum_f32", "scan_inclusive_i32", "compact_gt0_i32
             r["exchange"] += " — FAILED (peer timeout)"
     torch.cuda.empty_cache()
     return rows
+
+
+def bench_shards(worlds=(1, 2, 4, 8), log2_total=None, iters: int = 20, repeats: int = 5,
+                 device=None) -> list[dict]:
+    """Predicted strong scaling on one GPU (module docstring, `shards`).  At
+    N = 1 the single-GPU ops run (what bench.py times at 1 GPU); at N > 1 the
+    fused per-rank kernels bench.py runs on each rank (p2p.PeerReducer /
+    PeerCollectives), here on a world-1 mailbox.  Every step is a
+    WF_FLAG_INPUT_STABLE launch, as in bench.py; each op's shard sizes are
+    interleaved round by round."""
+    from . import p2p
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    totals = log2_total or {"reduce_sum_f32": 30, "scan_inclusive_i32": 28,
+                            "compact_gt0_i32": 28, "histogram256_u8": 32}
+    boxes = p2p.Mailboxes.local(1, dev, cap=256)
+    kboxes = p2p.Mailboxes.local(1, dev)
+    pc = p2p.PeerCollectives(boxes[0], 0, 1, 256, dev)
+    pr = p2p.PeerReducer(kboxes[0], 0, 1)
+    step_us: dict = {}
+
+    def step_fn(op, world, x, y):
+        if op == "reduce_sum_f32":
+            red = ops.reduce_sum_f32 if world == 1 else pr.reduce_sum_f32
+            return lambda: red(x, block=256, input_stable=True)
+        if op == "scan_inclusive_i32":
+            if world == 1:
+                return lambda: ops.scan_inclusive_i32(x, y, input_stable=True)
+
+            def c3():
+                carry = pc.reduce_exscan_i32(x, input_stable=True)[:1]
+                ops.scan_inclusive_i32(x, y, carry=carry, input_stable=True)
+            return c3
+        if op == "compact_gt0_i32":
+            if world == 1:
+                return lambda: ops.compact_gt0_i32(x, y, input_stable=True)
+            return lambda: pc.compact_gt0_i32(x, y, input_stable=True)
+        if world == 1:
+            return lambda: ops.histogram256_u8(x, input_stable=True)
+        return lambda: pc.histogram256_u8(x, input_stable=True)
+
+    try:
+        # one op at a time, its shard sizes interleaved round by round: every
+        # timed loop follows the same op (no other op's dirty L2 lines), and
+        # clock / power drift hits every N alike
+        for op in totals:
+            fns = {}
+            for world in worlds:
+                x = ops.fill_synthetic(OPS[op][0], (1 << totals[op]) // world, seed=0, device=dev)
+                y = torch.empty(x.numel(), dtype=torch.int32, device=dev) \
+                    if op in ("scan_inclusive_i32", "compact_gt0_i32") else None
+                fns[world] = step_fn(op, world, x, y)
+            times = {world: [] for world in worlds}
+            torch.cuda.synchronize()  # the fills above wrote the inputs
+            for fn in fns.values():
+                fn()
+            for _ in range(repeats):
+                for world, fn in fns.items():
+                    torch.cuda.synchronize()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    for _ in range(iters):
+                        fn()
+                    e1.record()
+                    e1.synchronize()
+                    times[world].append(e0.elapsed_time(e1) * 1e3 / iters)
+            for world, v in times.items():
+                step_us[(op, world)] = statistics.median(v)
+            del fns
+            torch.cuda.empty_cache()
+        if pc.failed():
+            raise RuntimeError("bench_shards: the fused exchange timed out")
+    finally:
+        torch.cuda.synchronize()
+        boxes[0].close()
+        kboxes[0].close()
+    rows = []
+    for op in totals:
+        t1 = step_us.get((op, worlds[0]))
+        for world in worlds:
+            t = step_us[(op, world)]
+            rows.append({"op": op, "n": 1 << totals[op], "n_gpus": world, "scaling": "strong",
+                         "per_rank_us": t, "predicted_speedup": t1 / t * worlds[0],
+                         "predicted_efficiency": t1 / t * worlds[0] / world,
+                         "how": "one GPU: per-rank step at this shard size, world-1 fused "
+                                "protocol (NVLink round trip not included)"})
+    torch.cuda.empty_cache()
+    return rows
+

@@ -51,6 +51,25 @@ def test_bench_cli_all_suites():
     assert len(res["ops"]) == sum(len(v[2]) for v in bm.OPS.values())
     assert all(row["gelem_s"] > 0 for row in res["ops"])
     assert [row["n_gpus"] for row in res["scaling"]] == [1] * 4
+    assert [(row["op"], row["n_gpus"]) for row in res["shards"]][:4] == [
+        ("reduce_sum_f32", 1), ("reduce_sum_f32", 2), ("reduce_sum_f32", 4), ("reduce_sum_f32", 8)]
+    assert all(row["per_rank_us"] > 0 for row in res["shards"])
+
+
+@pytest.mark.gpu
+def test_bench_shards_small_totals():
+    """The one-GPU scaling prediction at small totals: every op at 1/2/4
+    shards, per-rank steps shrink with the shard, speed-ups are relative to
+    the 1-shard step."""
+    import torch
+    rows = bm.bench_shards(worlds=(1, 2, 4), iters=3, repeats=2,
+                           log2_total={"reduce_sum_f32": 24, "scan_inclusive_i32": 22,
+                                       "compact_gt0_i32": 22, "histogram256_u8": 26})
+    assert len(rows) == 12 and torch.cuda.is_available()
+    for r in rows:
+        assert r["per_rank_us"] > 0
+        if r["n_gpus"] == 1:
+            assert r["predicted_speedup"] == 1.0
 
 
 @pytest.mark.gpu
