@@ -525,6 +525,24 @@ def run_ours(args, rank, world, local) -> dict | None:
 
     if rank != 0:
         return None
+    predicted = None
+    if world == 1 and not args.headline_only and not args.no_shards:
+        log("rank 0: per-rank steps at the 1/2/4/8-GPU shard sizes (one-GPU scaling prediction)")
+        from paper_2112_10034_b200 import benchmarks as bm
+        rows = bm.bench_shards(iters=10, repeats=3)
+        predicted = {"how": "per-rank step of each sharded config at the 1/2/4/8-GPU shard "
+                            "sizes, measured on this one GPU with the fused per-rank kernels "
+                            "(world-1 mailbox: the exchange protocol runs, the NVLink round "
+                            "trip does not) as dependent launches; speedup = t(1) / t(N).  "
+                            "A prediction: the driver's multi-GPU run measures the real curve",
+                     "configs": {}}
+        names = {"reduce_sum_f32": "C2", "scan_inclusive_i32": "C3", "compact_gt0_i32": "C4",
+                 "histogram256_u8": "C5"}
+        for r in rows:
+            predicted["configs"].setdefault(names[r["op"]], {})[f"N{r['n_gpus']}"] = {
+                "per_rank_us": round(r["per_rank_us"], 1),
+                "speedup": round(r["predicted_speedup"], 3),
+                "efficiency": round(r["predicted_efficiency"], 3)}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_c2(args.cpu_budget)
@@ -577,6 +595,7 @@ def run_ours(args, rank, world, local) -> dict | None:
         "verified": checks,
         "clocks": clk.summary(),
         "per_kernel": per,
+        "predicted_scaling": predicted,
     }
 
 
@@ -981,6 +1000,8 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-shards", action="store_true",
+                    help="skip the one-GPU scaling prediction (predicted_scaling)")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     args = ap.parse_args()
     if args.warmup < 3:
