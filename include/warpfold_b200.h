@@ -200,6 +200,24 @@ int wf_compact_gt0_i32_mg(const int32_t *in, uint64_t n, int32_t *out,
                           void *const *d_peers, const void *d_mailbox,
                           uint32_t cap, int rank, int world, uint32_t epoch,
                           uint32_t *d_err, wf_stream_t stream);
+/* Single-pass sharded scan of a BLOCK-CYCLIC distributed array: global
+ * super-tile g (round_elems elements, a multiple of 8192) lives on rank
+ * g % world as its local super-tile g / world; this rank's `in` holds its
+ * super-tiles back to back (n elements, the last may be short) and `out`
+ * receives the GLOBAL inclusive scan at those positions.  Each round's
+ * super-tile totals are all-gathered over the peer mailbox inside the scan
+ * kernel (cap >= rounds words per rank), so every element is read once and
+ * written once (8 B/elem; the contiguous-shard reduce-then-scan needs 12).
+ * `rounds` must be the same on every rank (>= ceil(n / round_elems)); in /
+ * out 16-byte aligned.  max_grid > 0 caps the grid (ranks sharing one GPU
+ * must all be resident at once).  flags: WF_FLAG_INPUT_STABLE. */
+int wf_scan_inclusive_i32_cyclic_mg(const int32_t *in, int32_t *out, uint64_t n,
+                                    void *ws, size_t ws_bytes, void *const *d_peers,
+                                    const void *d_mailbox, uint32_t cap, int rank,
+                                    int world, uint32_t epoch, uint32_t *d_err,
+                                    uint64_t round_elems, uint32_t rounds,
+                                    int max_grid, unsigned flags,
+                                    wf_stream_t stream);
 /* ... with launch flags (WF_FLAG_INPUT_STABLE, as wf_reduce_sum_f32_ex) */
 int wf_reduce_sum_i32_exscan_mg_ex(const int32_t *in, uint64_t n, int32_t *d_out2,
                                    int block, int grid, void *ws, size_t ws_bytes,

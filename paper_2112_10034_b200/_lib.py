@@ -69,6 +69,9 @@ SIGNATURES = {
                                         C.c_int, _u32, _vp, _vp]),
     "wf_compact_gt0_i32_mg_ex": (C.c_int, [_vp, _u64, _vp, _vp, _vp, _sz, _vp, _vp, _u32,
                                            C.c_int, C.c_int, _u32, _vp, C.c_uint, _vp]),
+    "wf_scan_inclusive_i32_cyclic_mg": (C.c_int, [_vp, _vp, _u64, _vp, _sz, _vp, _vp, _u32, C.c_int,
+                                                  C.c_int, _u32, _vp, _u64, _u32, C.c_int,
+                                                  C.c_uint, _vp]),
     "wf_reduce_sum_i32_exscan_mg_ex": (C.c_int, [_vp, _u64, _vp, C.c_int, C.c_int, _vp, _sz, _vp,
                                                  _vp, _u32, C.c_int, C.c_int, _u32, _vp, C.c_uint,
                                                  _vp]),

@@ -378,6 +378,36 @@ int wf_reduce_sum_i32_exscan_mg_ex(const int32_t *in, uint64_t n, int32_t *d_out
                      "reduce_sum_i32_exscan_mg");
 }
 
+int wf_scan_inclusive_i32_cyclic_mg(const int32_t *in, int32_t *out, uint64_t n, void *ws,
+                                    size_t ws_bytes, void *const *d_peers,
+                                    const void *d_mailbox, uint32_t cap, int rank, int world,
+                                    uint32_t epoch, uint32_t *d_err, uint64_t round_elems,
+                                    uint32_t rounds, int max_grid, unsigned flags,
+                                    wf_stream_t stream) {
+  if (flags & ~unsigned(WF_FLAG_INPUT_STABLE)) return fail(WF_ERR_ARG, "unknown flags 0x%x", flags);
+  if (n > 0 && (in == nullptr || out == nullptr)) return fail(WF_ERR_ARG, "NULL buffer pointer");
+  if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u)
+    return fail(WF_ERR_ARG, "the block-cyclic scan takes 16-byte aligned buffers");
+  if (round_elems == 0 || round_elems % kTmemTile != 0 || round_elems > (uint64_t(1) << 31))
+    return fail(WF_ERR_ARG, "round_elems must be a positive multiple of %u (<= 2^31), got %llu",
+                unsigned(kTmemTile), (unsigned long long)round_elems);
+  if (uint64_t(rounds) * round_elems < n)
+    return fail(WF_ERR_ARG, "%u rounds of %llu elements cannot hold n=%llu", rounds,
+                (unsigned long long)round_elems, (unsigned long long)n);
+  if (world > 32) return fail(WF_ERR_ARG, "world %d > 32", world);
+  if (max_grid < 0) return fail(WF_ERR_CONFIG, "max_grid must be >= 0, got %d", max_grid);
+  int rc = check_ws(WF_OP_SCAN_INCLUSIVE_I32, n, ws, ws_bytes);
+  if (rc) return rc;
+  rc = check_peer(d_peers, d_mailbox, cap, rounds, rank, world, epoch, d_err);
+  if (rc) return rc;
+  return cuda_status(
+      launch_scan_tmem_i32_cyclic(in, out, n, ws, d_peers, d_mailbox, cap, rank, world, epoch,
+                                  d_err, uint32_t(round_elems / kTmemTile), rounds, max_grid,
+                                  static_cast<cudaStream_t>(stream),
+                                  (flags & WF_FLAG_INPUT_STABLE) != 0),
+      "scan_inclusive_i32_cyclic_mg");
+}
+
 int wf_compact_gt0_i32_mg(const int32_t *in, uint64_t n, int32_t *out, uint64_t *d_counts3,
                           void *ws, size_t ws_bytes, void *const *d_peers, const void *d_mailbox,
                           uint32_t cap, int rank, int world, uint32_t epoch, uint32_t *d_err,

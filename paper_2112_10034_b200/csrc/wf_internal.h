@@ -27,6 +27,7 @@ constexpr uint32_t kMaxReduceGrid = 8192;   // partial slots for reductions
 constexpr int kScanBlock = 256;             // threads per scan/compact tile
 constexpr int kScanVec = 4;                 // int4 loads per thread per tile
 constexpr uint64_t kScanTile = uint64_t(kScanBlock) * kScanVec * 4;  // 4096
+constexpr uint64_t kTmemTile = 8192;  // elements per TMEM-kernel tile (wf_scan_tmem.cu TM_TILE)
 #ifndef WF_HIST_BLOCK
 #define WF_HIST_BLOCK 1024
 #endif
@@ -124,6 +125,11 @@ struct PeerArgs;  // wf_peer.cuh
 cudaError_t launch_compact_tmem_i32_mg(const int32_t *in, uint64_t n, int32_t *out,
                                        uint64_t *counts3, void *ws, const PeerArgs &pa,
                                        cudaStream_t s, bool early = false);
+cudaError_t launch_scan_tmem_i32_cyclic(const int32_t *in, int32_t *out, uint64_t n, void *ws,
+                                        void *const *peers, const void *mine, uint32_t cap,
+                                        int rank, int world, uint32_t epoch, uint32_t *err,
+                                        uint32_t round_tiles, uint32_t rounds, int max_grid,
+                                        cudaStream_t s, bool early);
 cudaError_t launch_compact_gt0_i32_mg(const int32_t *in, uint64_t n, int32_t *out,
                                       uint64_t *counts3, void *ws, void *const *peers,
                                       const void *mine, uint32_t cap, int rank, int world,

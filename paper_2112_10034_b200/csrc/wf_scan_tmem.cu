@@ -176,6 +176,7 @@ constexpr uint32_t kNoTileTm = 0xffffffffu;
 constexpr uint32_t kBatch = WF_TM_BATCH;
 constexpr uint32_t kNoItem = 0xffffffffu;  // item_seq before the first publish
 static_assert((P & (P - 1)) == 0 && TM_COLS <= 512, "TMEM slots: power of two, <= 512 cols");
+static_assert(TM_TILE == kTmemTile, "wf_internal.h kTmemTile: the block-cyclic scan's tile unit");
 static_assert(NLB >= 1 && NLB <= P, "look-back warps must not outnumber TMEM slots");
 static_assert(!WF_TM_SWEEP || (NLB == 1 && (NAG == 1 || W_SWEEP < W_AGG2)),
               "the sweeper warp sits in the gap before the second aggregator group");
@@ -293,6 +294,7 @@ struct TmShared {
   // the slower stage: 50 % 241 -> 250 us, tools/c4_sel_probe.py)
   uint32_t slot_pk[P][4][2 * TMUL][2][32];
 #endif
+  uint32_t cx_wtot[2][2][4];  // CX aggregators: [group][item parity][warp] quarter sums
   uint32_t tmem_base;
   uint32_t epoch;
 };
@@ -302,17 +304,143 @@ struct TmShared {
 // 4096 elements, far more)
 __device__ __forceinline__ uint32_t pref_offset(uint32_t ntiles) { return (ntiles + 15u) & ~15u; }
 
+// CX sweeper (one warp, CTA 0; tile_tmem_kernel's CX note).  Mailbox word of
+// (bank, source rank, round): bank * world * cap + src * cap + round, holding
+// {(0x80000000 | epoch) << 32 | value} — one 64-bit store carries tag and
+// value together.
+static __device__ __noinline__ void cx_sweep(const uint64_t *desc_c, uint32_t ntiles,
+                                             uint32_t epoch, const PeerArgs pa,
+                                             uint32_t round_tiles, uint32_t rounds) {
+  uint64_t *desc = const_cast<uint64_t *>(desc_c);
+  uint64_t *pref = desc + pref_offset(ntiles);
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t tag_agg = uint32_t(pack_desc(epoch, kStAggregate, 0u) >> 32);
+  const uint32_t world = uint32_t(pa.world), rank = uint32_t(pa.rank);
+  const uint64_t bank = uint64_t(pa.epoch & 1u) * world * pa.cap;
+  constexpr int K = WF_SWEEP_K;
+  uint32_t before = 0;  // all ranks' totals of the rounds done (wrapping i32 sum)
+  bool failed = false;
+  for (uint32_t r = 0; r < rounds; ++r) {
+    const uint32_t t0 = r * round_tiles < ntiles ? r * round_tiles : ntiles;
+    const uint32_t t1 = t0 + round_tiles < ntiles ? t0 + round_tiles : ntiles;
+    // pass A: this rank's total of the round, as its aggregates arrive
+    uint32_t part = 0, backoff = 32;
+    for (uint32_t f = t0; f < t1;) {
+      uint64_t d[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t idx = f + lane + 32u * k;
+        d[k] = idx < t1 ? ld_relaxed_gpu(desc + idx) : 0ull;
+      }
+      uint32_t ready = 0;
+      bool gap = false;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const bool ok = uint32_t(d[k] >> 32) == tag_agg;
+        const uint32_t bal = __ballot_sync(kFull, ok);
+        if (!gap) {
+          const uint32_t take = bal == kFull ? 32u : uint32_t(__ffs(~bal)) - 1u;
+          if (lane < take) part += uint32_t(d[k]);
+          ready += take;
+          gap = take < 32u;
+        }
+      }
+      if (ready == 0) {
+        __nanosleep(backoff);
+        backoff = backoff < 256 ? backoff * 2 : 256;
+        continue;
+      }
+      backoff = 32;
+      f += ready;
+    }
+    const uint32_t mine = __reduce_add_sync(kFull, part);
+    // the round's all-gather: lane q stores to rank q and polls source q
+    // tag = epoch with the top bit set: no payload word of the other peer
+    // exchanges sharing the mailbox (counts, bins < 2^63) can look like it
+    const uint32_t tag = 0x80000000u | pa.epoch;
+    const uint64_t word = (uint64_t(tag) << 32) | mine;
+    for (uint32_t q = lane; q < world; q += 32)
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(pa.peers[q] + bank + rank * pa.cap + r),
+                   "l"(word)
+                   : "memory");
+    uint32_t lower = 0, all = 0;
+    for (uint32_t q = lane; q < world; q += 32) {
+      const uint64_t *slot = pa.mine + bank + q * pa.cap + r;
+      uint64_t w = peer_ld_acquire_sys(slot);
+      uint32_t spins = 0;
+      while (uint32_t(w >> 32) != tag) {
+        if (++spins > (1u << 25)) {  // ~4 s: a peer never arrived
+          failed = true;
+          w = 0;
+          break;
+        }
+        __nanosleep(128);
+        w = peer_ld_acquire_sys(slot);
+      }
+      all += uint32_t(w);
+      if (q < rank) lower += uint32_t(w);
+    }
+    lower = __reduce_add_sync(kFull, lower);
+    all = __reduce_add_sync(kFull, all);
+    // pass B: the round's prefixes, its aggregates all published by now
+    uint32_t run = before + lower;
+    for (uint32_t f = t0; f < t1; f += 32u * K) {
+      uint32_t v[K], sc[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t idx = f + lane + 32u * k;
+        v[k] = idx < t1 ? uint32_t(ld_relaxed_gpu(desc + idx)) : 0u;
+        sc[k] = v[k];
+      }
+#pragma unroll
+      for (int dd = 1; dd < 32; dd <<= 1) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const uint32_t y = __shfl_up_sync(kFull, sc[k], dd);
+          if (lane >= uint32_t(dd)) sc[k] += y;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t idx = f + lane + 32u * k;
+        if (idx < t1) st_relaxed_gpu(pref + idx, pack_desc(epoch, kStPrefix, run + sc[k] - v[k]));
+        run += __shfl_sync(kFull, sc[k], 31);
+      }
+    }
+    before += all;
+  }
+  if (__any_sync(kFull, failed) && lane == 0) *pa.err = 1u;
+}
+
 // PX (compaction only): the finisher warp of the last tile also runs the
 // offset exchange of wf_peer.cuh (peer_exscan_warp): count = {this rank's
 // count, its global offset, the global total} — the sharded compaction and
 // its exchange in ONE kernel (wf_compact_gt0_i32_mg).
-template <bool COMPACT, bool PX = false>
+//
+// CX (scan only): the cross-rank single-pass scan of a BLOCK-CYCLIC sharded
+// array.  Global super-tile g (round_tiles tiles) lives on rank g % world as
+// its local super-tile g / world, so this rank's local super-tile s is global
+// super-tile s * world + rank.  The sweeper sums the aggregates of each local
+// super-tile, all-gathers the round's totals over peer memory (one u64
+// {epoch, value} word per rank and round, wf_peer.cuh mailbox, bank by epoch
+// parity), and publishes every tile's prefix = (all ranks' totals of earlier
+// rounds) + (lower ranks' totals of this round) + its local prefix.  Every
+// element is read once and written once (8 B/elem, against the 12 B of
+// reduce-then-scan), and no rank waits for another rank's whole shard — only
+// for its same-round super-tile.  Deadlock freedom needs every claimed tile's
+// aggregate published without a free TMEM slot: CX aggregators sum a landed
+// stage and publish before they wait for the slot (a round's last tile can
+// otherwise be stuck in a stage whose CTA's slots all hold tiles of the same
+// round).  `rounds` is the same on every rank (ranks with fewer local
+// super-tiles contribute 0).
+template <bool COMPACT, bool PX = false, bool CX = false>
 __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
     tile_tmem_kernel(const int32_t *__restrict__ in, int32_t *__restrict__ out, uint64_t n,
                      uint32_t ntiles, const int32_t *__restrict__ carry_in,
                      uint64_t *__restrict__ count, uint64_t *__restrict__ desc,
                      TileHeader *__restrict__ hdr, uint32_t head, bool vec_out,
-                     PeerArgs pa) {
+                     PeerArgs pa, uint32_t round_tiles, uint32_t rounds) {
+  static_assert(!CX || (!COMPACT && !PX && WF_TM_SWEEP), "CX: the sweeper scan only");
   // `head` (0-3): the buffers were rounded down to 16 B, so virtual elements
   // [0, head) precede the caller's data; they read as 0 (neutral for the sum,
   // never selected) and are never stored.  Only tile 0 is affected.
@@ -476,6 +604,33 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       PROF_T(g1);
       const uint32_t t = sh.stage_tile[s];
       if (t == kExitOnly) break;
+      if constexpr (CX) {
+        if (t != kNoTileTm) {
+          // publish the tile's aggregate straight from the stage, before the
+          // TMEM slot wait (see CX above); the same sums as the parking pass
+          const int32_t *st = stages + s * TM_TILE + q * (QVEC * 128) + lane * 4;
+          uint32_t qs = 0;
+#pragma unroll 4
+          for (int j = 0; j < 16 * TMUL; ++j) {
+            uint4 x = *reinterpret_cast<const uint4 *>(st + j * 128);
+            if (head && t == 0 && q == 0 && j == 0 && lane == 0) {
+              if (head > 0) x.x = 0;
+              if (head > 1) x.y = 0;
+              if (head > 2) x.z = 0;
+            }
+            qs += x.x + x.y + x.z + x.w;
+          }
+          qs = __reduce_add_sync(kFull, qs);
+          const uint32_t b = (i / NAG) & 1u;
+          if (lane == 0) sh.cx_wtot[grp][b][q] = qs;
+          agg_sync(grp);
+          if (leader) {
+            const uint32_t a = sh.cx_wtot[grp][b][0] + sh.cx_wtot[grp][b][1] +
+                               sh.cx_wtot[grp][b][2] + sh.cx_wtot[grp][b][3];
+            st_relaxed_gpu(desc + t, pack_desc(epoch, kStAggregate, a));
+          }
+        }
+      }
       if (kp > 0) mbar_wait(&sh.freed[p], (kp - 1) & 1u);
       PROF_T(g2);
       tc_fence_after();
@@ -557,7 +712,8 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
         // publish the aggregate right here, not in the look-back warp: a
         // look-back warp busy with an older tile must never delay it
 #if WF_TM_SWEEP
-        st_relaxed_gpu(desc + t, pack_desc(epoch, kStAggregate, a));  // dense: the sweeper reads 32 K per trip
+        if constexpr (!CX)  // (CX: published before the slot wait)
+          st_relaxed_gpu(desc + t, pack_desc(epoch, kStAggregate, a));  // dense: the sweeper reads 32 K per trip
 #else
         if (t == 0) {
           const uint32_t c0 = (!COMPACT && carry_in != nullptr) ? uint32_t(*carry_in) : 0u;
@@ -827,7 +983,9 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
     // per-tile look-back that must walk back to an older resolved prefix and
     // occupies a look-back warp for its whole duration (per-tile traces:
     // ~5 us waiting for a free look-back warp + ~2.8 us of look-back).
-    if (blockIdx.x == 0) {
+    if (CX && blockIdx.x == 0) {
+      cx_sweep(desc, ntiles, epoch, pa, round_tiles, rounds);
+    } else if (blockIdx.x == 0) {
       uint64_t *pref = desc + pref_offset(ntiles);
       const uint32_t tag_agg = uint32_t(pack_desc(epoch, kStAggregate, 0u) >> 32);
       uint32_t run = (!COMPACT && carry_in != nullptr) ? uint32_t(*carry_in) : 0u;
@@ -986,18 +1144,18 @@ constexpr size_t tm_smem() {
 
 // Sets the dynamic-smem opt-in of the instantiation on the current device
 // (per device, before every launch) and returns the persistent grid.
-template <bool COMPACT, bool PX = false>
+template <bool COMPACT, bool PX = false, bool CX = false>
 int tmem_grid(uint32_t ntiles) {
   static int per_sm[2] = {0, 0};
   static DeviceMask configured;
   configured.ensure([] {
-    cudaFuncSetAttribute(tile_tmem_kernel<COMPACT, PX>,
+    cudaFuncSetAttribute(tile_tmem_kernel<COMPACT, PX, CX>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(tm_smem<COMPACT>()));
   });
   int &b = per_sm[COMPACT];
   if (b == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tile_tmem_kernel<COMPACT, PX>, TM_THREADS,
-                                                  tm_smem<COMPACT>());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tile_tmem_kernel<COMPACT, PX, CX>,
+                                                  TM_THREADS, tm_smem<COMPACT>());
     if (b > int(512 / TM_COLS)) b = int(512 / TM_COLS);  // TMEM: 512 columns per SM
     if (b < 1) b = 1;
   }
@@ -1034,12 +1192,15 @@ extern "C" int wf_debug_set_trace_sweep(void *buf, uint32_t cap) {
 // offset is written with scalar stores.
 // `early`: a programmatic dependent launch (the caller's WF_FLAG_INPUT_STABLE
 // promise); the kernel's static first loads then overlap the previous grid.
-template <bool COMPACT, bool PX>
+template <bool COMPACT, bool PX, bool CX = false>
 cudaError_t launch_tmem(uint32_t nt, bool early, cudaStream_t s, const int32_t *in, int32_t *out,
                         uint64_t nv, const int32_t *carry, uint64_t *count, uint64_t *desc,
-                        TileHeader *hdr, uint32_t head, bool vec_out, const PeerArgs &pa) {
+                        TileHeader *hdr, uint32_t head, bool vec_out, const PeerArgs &pa,
+                        uint32_t round_tiles = 0, uint32_t rounds = 0, int max_grid = 0) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(tmem_grid<COMPACT, PX>(nt));
+  int grid = tmem_grid<COMPACT, PX, CX>(nt);
+  if (max_grid > 0 && grid > max_grid) grid = max_grid;
+  cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(TM_THREADS);
   cfg.dynamicSmemBytes = tm_smem<COMPACT>();
   cfg.stream = s;
@@ -1048,8 +1209,8 @@ cudaError_t launch_tmem(uint32_t nt, bool early, cudaStream_t s, const int32_t *
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = early ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, tile_tmem_kernel<COMPACT, PX>, in, out, nv, nt, carry, count,
-                            desc, hdr, head, vec_out, pa);
+  return cudaLaunchKernelEx(&cfg, tile_tmem_kernel<COMPACT, PX, CX>, in, out, nv, nt, carry,
+                            count, desc, hdr, head, vec_out, pa, round_tiles, rounds);
 }
 
 cudaError_t launch_scan_tmem_i32(const int32_t *in, int32_t *out, uint64_t n,
@@ -1089,10 +1250,33 @@ cudaError_t launch_compact_tmem_i32_mg(const int32_t *in, uint64_t n, int32_t *o
                                  head, false, pa);
 }
 
+// Cross-rank single-pass scan of a block-cyclic sharded array (CX above):
+// `in` / `out` 16-byte aligned, this rank's local super-tiles of
+// round_tiles * 8192 elements back to back (the last may be short), the same
+// `rounds` on every rank.  `max_grid` > 0 caps the grid (ranks sharing one
+// GPU in tests: their grids must be co-resident, as the rounds wait on each
+// other mid-kernel).
+cudaError_t launch_scan_tmem_i32_cyclic(const int32_t *in, int32_t *out, uint64_t n, void *ws,
+                                        void *const *peers, const void *mine, uint32_t cap,
+                                        int rank, int world, uint32_t epoch, uint32_t *err,
+                                        uint32_t round_tiles, uint32_t rounds, int max_grid,
+                                        cudaStream_t s, bool early) {
+  const PeerArgs pa{reinterpret_cast<uint64_t *const *>(peers), static_cast<const uint64_t *>(mine),
+                    cap, rank, world, epoch, err};
+  auto *hdr = reinterpret_cast<TileHeader *>(ws);
+  auto *desc = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + kTileWsHeader);
+  const uint32_t nt = uint32_t((n + TM_TILE - 1) / TM_TILE);
+  return launch_tmem<false, false, true>(nt, early, s, in, out, n, nullptr, nullptr, desc, hdr,
+                                         0u, true, pa, round_tiles, rounds, max_grid);
+}
+
 cudaError_t preload_tmem_mg_kernels() {
   tmem_grid<true, true>(1);  // dynamic-smem opt-in on this device
+  tmem_grid<false, false, true>(1);
   cudaFuncAttributes a;
-  return cudaFuncGetAttributes(&a, tile_tmem_kernel<true, true>);
+  cudaError_t e = cudaFuncGetAttributes(&a, tile_tmem_kernel<true, true>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tile_tmem_kernel<false, false, true>);
+  return e;
 }
 
 }  // namespace wf

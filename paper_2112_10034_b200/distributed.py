@@ -83,6 +83,23 @@ def reduce_sum_i32(x_local: torch.Tensor, group=None, block: int = 256) -> torch
     return ops.fold(exchange(part, group).reshape(-1))
 
 
+def cyclic_rounds(n: int, rank: int, world: int, round_elems: int = 1 << 22):
+    """Block-cyclic layout of a global array of `n` elements: global
+    super-tile g (`round_elems` elements, the last one short) lives on rank
+    g % world.  Returns (rounds, [(global_start, length), ...] of this
+    rank's super-tiles in local order); `rounds` is the same on every rank
+    (ranks with fewer super-tiles contribute empty rounds)."""
+    supers = -(-n // round_elems)
+    rounds = -(-supers // world)
+    mine = []
+    for r in range(rounds):
+        g = r * world + rank
+        if g < supers:
+            start = g * round_elems
+            mine.append((start, min(round_elems, n - start)))
+    return rounds, mine
+
+
 def scan_inclusive_i32(x_local: torch.Tensor, out: torch.Tensor | None = None,
                        group=None, peer=None, input_stable: bool = False) -> torch.Tensor:
     """`peer`: a p2p.PeerCollectives — the shard totals then travel over peer

@@ -212,6 +212,33 @@ class PeerCollectives:
             "wf_reduce_sum_i32_exscan_mg")
         return out
 
+    def scan_inclusive_i32_cyclic(self, x_local: torch.Tensor, out: torch.Tensor | None = None,
+                                  round_elems: int = 1 << 22, rounds: int | None = None,
+                                  max_grid: int = 0, stream=None,
+                                  input_stable: bool = False) -> torch.Tensor:
+        """Single-pass scan of a BLOCK-CYCLIC sharded array
+        (``wf_scan_inclusive_i32_cyclic_mg``): global super-tile g of
+        `round_elems` elements lives on rank g % world; `x_local` holds this
+        rank's super-tiles back to back (``distributed.cyclic_rounds``) and
+        `out` receives the global inclusive scan at those positions.  The
+        round totals are all-gathered inside the scan kernel, so each element
+        is read once (8 B/elem).  `rounds`: the same on every rank (default:
+        this rank's own count — pass the global count when shards differ)."""
+        ops._require_cuda(x_local, torch.int32, "x")
+        if out is None:
+            out = torch.empty_like(x_local)
+        if rounds is None:
+            rounds = -(-x_local.numel() // round_elems)
+        self.epoch += 1
+        ws = ops.workspace(_lib.OP_SCAN_INCLUSIVE_I32, x_local.numel(), x_local.device, stream)
+        _check(_lib.load().wf_scan_inclusive_i32_cyclic_mg(
+            x_local.data_ptr(), out.data_ptr(), x_local.numel(), ws.data_ptr(), ws.numel(),
+            self.boxes.peers.data_ptr(), self.boxes.own, self.cap, self.rank, self.world,
+            self.epoch, self.err.data_ptr(), round_elems, rounds, max_grid,
+            _lib.FLAG_INPUT_STABLE if input_stable else 0, ops._stream_handle(stream)),
+            "wf_scan_inclusive_i32_cyclic_mg")
+        return out
+
     def compact_gt0_i32(self, x_local: torch.Tensor, out: torch.Tensor | None = None,
                         stream=None, input_stable: bool = False):
         """K4 over this rank's shard with the offset exchange fused into the

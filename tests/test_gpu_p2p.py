@@ -106,6 +106,49 @@ def test_fused_histogram_input_stable_chain(mods):
         boxes[0].close()
 
 
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+def test_cyclic_scan_in_process(mods, world):
+    """Single-pass scan of a block-cyclic sharded array, every rank a
+    concurrent kernel on its own stream of the one GPU (grids capped so all
+    ranks are resident at once: the rounds wait on each other mid-kernel).
+    Each rank's output equals the global inclusive scan at its positions;
+    three calls in a row (epoch banks alternate), plain and dependent
+    launches."""
+    ops, p2p, wd = mods
+    dev = torch.device("cuda", 0)
+    round_elems = 8192 * 24
+    n = round_elems * (3 * world + 1) + 8192 * 5 + 4  # ragged global tail
+    full = ops.fill_synthetic("i32_full", n, seed=21)
+    want = torch.cumsum(full.to(torch.int64), 0).to(torch.int32)
+    boxes = p2p.Mailboxes.local(world, dev, cap=256)
+    pcs = [p2p.PeerCollectives(boxes[r], r, world, 256, dev) for r in range(world)]
+    layout = [wd.cyclic_rounds(n, r, world, round_elems) for r in range(world)]
+    rounds = layout[0][0]
+    xs, wants = [], []
+    for r in range(world):
+        parts = layout[r][1]
+        xs.append(torch.cat([full[s:s + m] for s, m in parts]))
+        wants.append(torch.cat([want[s:s + m] for s, m in parts]))
+    streams = [torch.cuda.Stream(dev) for _ in range(world)]
+    cap = 148 // world
+    torch.cuda.synchronize()
+    try:
+        for call in range(3):
+            outs = [torch.full_like(x, -1) for x in xs]
+            for r in (range(world) if call % 2 == 0 else reversed(range(world))):
+                with torch.cuda.stream(streams[r]):
+                    pcs[r].scan_inclusive_i32_cyclic(xs[r], outs[r], round_elems, rounds,
+                                                     max_grid=cap, stream=streams[r],
+                                                     input_stable=call == 2)
+            torch.cuda.synchronize()
+            for r in range(world):
+                assert torch.equal(outs[r], wants[r]), (call, r)
+        assert not any(pc.failed() for pc in pcs)
+    finally:
+        torch.cuda.synchronize()
+        boxes[0].close()
+
+
 def _child_read_mailbox(handle: bytes, world: int, q) -> None:
     import ctypes as C
     import torch as T
