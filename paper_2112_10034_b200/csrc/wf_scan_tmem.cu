@@ -162,6 +162,7 @@ constexpr int W_SWEEP = W_PROD + 1;       // prefix sweeper (CTA 0 only; WF_TM_S
 #endif
 constexpr int NAG = WF_TM_NAG;
 constexpr int W_AGG2 = ((W_PROD + 1 + 3) / 4) * 4;  // 2nd group: warp % 4 = TMEM lane quarter
+constexpr int W_TOTAL = W_SWEEP + 1;  // CX round totaler (CTA 0): the idle warp before W_AGG2
 constexpr int TM_THREADS = (NAG == 2 ? W_AGG2 + 4 : (WF_TM_SWEEP ? W_SWEEP + 1 : W_PROD + 1)) * 32;
 constexpr uint32_t kExitOnly = 0xfffffffdu;  // second stop item (NAG = 2): just leave
 #ifndef WF_TM_TMUL
@@ -307,23 +308,40 @@ __device__ __forceinline__ uint32_t pref_offset(uint32_t ntiles) { return (ntile
 // CX sweeper (one warp, CTA 0; tile_tmem_kernel's CX note).  Mailbox word of
 // (bank, source rank, round): bank * world * cap + src * cap + round, holding
 // {(0x80000000 | epoch) << 32 | value} — one 64-bit store carries tag and
-// value together.
-static __device__ __noinline__ void cx_sweep(const uint64_t *desc_c, uint32_t ntiles,
-                                             uint32_t epoch, const PeerArgs pa,
-                                             uint32_t round_tiles, uint32_t rounds) {
-  uint64_t *desc = const_cast<uint64_t *>(desc_c);
-  uint64_t *pref = desc + pref_offset(ntiles);
+// value together.  This rank's round-r prefixes need only the totals of the
+// LOWER ranks' round r (and every rank's earlier rounds), not its own: the
+// round is swept as its aggregates arrive, exactly like the plain sweeper, and
+// its total is published when the round ends.
+static __device__ __forceinline__ uint32_t cx_poll(const PeerArgs &pa, uint64_t bank,
+                                                   uint32_t src, uint32_t round, uint32_t tag,
+                                                   bool &failed) {
+  const uint64_t *slot = pa.mine + bank + src * pa.cap + round;
+  uint64_t w = peer_ld_relaxed_sys(slot);
+  uint32_t spins = 0;
+  while (uint32_t(w >> 32) != tag) {
+    if (++spins > (1u << 25)) {  // ~4 s: a peer never arrived
+      failed = true;
+      return 0u;
+    }
+    __nanosleep(64);
+    w = peer_ld_relaxed_sys(slot);
+  }
+  return uint32_t(w);
+}
+
+// Round totaler: sum the round's aggregates as they arrive, publish.
+static __device__ __noinline__ void cx_totals(const uint64_t *desc, uint32_t ntiles,
+                                              uint32_t epoch, const PeerArgs pa,
+                                              uint32_t round_tiles, uint32_t rounds) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t tag_agg = uint32_t(pack_desc(epoch, kStAggregate, 0u) >> 32);
   const uint32_t world = uint32_t(pa.world), rank = uint32_t(pa.rank);
   const uint64_t bank = uint64_t(pa.epoch & 1u) * world * pa.cap;
+  const uint32_t tag = 0x80000000u | pa.epoch;  // cx_sweep
   constexpr int K = WF_SWEEP_K;
-  uint32_t before = 0;  // all ranks' totals of the rounds done (wrapping i32 sum)
-  bool failed = false;
   for (uint32_t r = 0; r < rounds; ++r) {
     const uint32_t t0 = r * round_tiles < ntiles ? r * round_tiles : ntiles;
     const uint32_t t1 = t0 + round_tiles < ntiles ? t0 + round_tiles : ntiles;
-    // pass A: this rank's total of the round, as its aggregates arrive
     uint32_t part = 0, backoff = 32;
     for (uint32_t f = t0; f < t1;) {
       uint64_t d[K];
@@ -336,8 +354,7 @@ static __device__ __noinline__ void cx_sweep(const uint64_t *desc_c, uint32_t nt
       bool gap = false;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        const bool ok = uint32_t(d[k] >> 32) == tag_agg;
-        const uint32_t bal = __ballot_sync(kFull, ok);
+        const uint32_t bal = __ballot_sync(kFull, uint32_t(d[k] >> 32) == tag_agg);
         if (!gap) {
           const uint32_t take = bal == kFull ? 32u : uint32_t(__ffs(~bal)) - 1u;
           if (lane < take) part += uint32_t(d[k]);
@@ -353,45 +370,72 @@ static __device__ __noinline__ void cx_sweep(const uint64_t *desc_c, uint32_t nt
       backoff = 32;
       f += ready;
     }
-    const uint32_t mine = __reduce_add_sync(kFull, part);
-    // the round's all-gather: lane q stores to rank q and polls source q
-    // tag = epoch with the top bit set: no payload word of the other peer
-    // exchanges sharing the mailbox (counts, bins < 2^63) can look like it
-    const uint32_t tag = 0x80000000u | pa.epoch;
-    const uint64_t word = (uint64_t(tag) << 32) | mine;
+    // the 64-bit word is self-contained (tag and value) and nothing else is
+    // read through it: a relaxed system-scope store, no release fence
+    const uint64_t word = (uint64_t(tag) << 32) | __reduce_add_sync(kFull, part);
     for (uint32_t q = lane; q < world; q += 32)
-      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(pa.peers[q] + bank + rank * pa.cap + r),
-                   "l"(word)
-                   : "memory");
-    uint32_t lower = 0, all = 0;
-    for (uint32_t q = lane; q < world; q += 32) {
-      const uint64_t *slot = pa.mine + bank + q * pa.cap + r;
-      uint64_t w = peer_ld_acquire_sys(slot);
-      uint32_t spins = 0;
-      while (uint32_t(w >> 32) != tag) {
-        if (++spins > (1u << 25)) {  // ~4 s: a peer never arrived
-          failed = true;
-          w = 0;
-          break;
-        }
-        __nanosleep(128);
-        w = peer_ld_acquire_sys(slot);
-      }
-      all += uint32_t(w);
-      if (q < rank) lower += uint32_t(w);
-    }
+      peer_st_relaxed_sys(pa.peers[q] + bank + rank * pa.cap + r, word);
+  }
+}
+
+static __device__ __noinline__ void cx_sweep(const uint64_t *desc_c, uint32_t ntiles,
+                                             uint32_t epoch, const PeerArgs pa,
+                                             uint32_t round_tiles, uint32_t rounds) {
+  uint64_t *desc = const_cast<uint64_t *>(desc_c);
+  uint64_t *pref = desc + pref_offset(ntiles);
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t tag_agg = uint32_t(pack_desc(epoch, kStAggregate, 0u) >> 32);
+  const uint32_t world = uint32_t(pa.world), rank = uint32_t(pa.rank);
+  const uint64_t bank = uint64_t(pa.epoch & 1u) * world * pa.cap;
+  const uint32_t tag = 0x80000000u | pa.epoch;
+  constexpr int K = WF_SWEEP_K;
+  uint32_t before = 0;  // every rank's totals of the rounds done (wrapping i32 sum)
+  bool failed = false;
+  for (uint32_t r = 0; r < rounds; ++r) {
+    const uint32_t t0 = r * round_tiles < ntiles ? r * round_tiles : ntiles;
+    const uint32_t t1 = t0 + round_tiles < ntiles ? t0 + round_tiles : ntiles;
+    // the lower ranks' totals of this round (lane q polls rank q)
+    uint32_t lower = 0;
+    for (uint32_t q = lane; q < rank; q += 32) lower += cx_poll(pa, bank, q, r, tag, failed);
     lower = __reduce_add_sync(kFull, lower);
-    all = __reduce_add_sync(kFull, all);
-    // pass B: the round's prefixes, its aggregates all published by now
-    uint32_t run = before + lower;
-    for (uint32_t f = t0; f < t1; f += 32u * K) {
-      uint32_t v[K], sc[K];
+    // sweep this rank's tiles of the round as their aggregates arrive
+    const uint32_t start = before + lower;
+    uint32_t run = start, backoff = 32;
+    for (uint32_t f = t0; f < t1;) {
+      uint64_t d[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const uint32_t idx = f + lane + 32u * k;
-        v[k] = idx < t1 ? uint32_t(ld_relaxed_gpu(desc + idx)) : 0u;
-        sc[k] = v[k];
+        d[k] = idx < t1 ? ld_relaxed_gpu(desc + idx) : 0ull;
       }
+      uint32_t v[K], ready = 0;
+      bool ok[K], gap = false;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        ok[k] = uint32_t(d[k] >> 32) == tag_agg;
+        v[k] = uint32_t(d[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t b = __ballot_sync(kFull, ok[k]);
+        if (!gap) {
+          if (b == kFull) {
+            ready += 32;
+          } else {
+            ready += uint32_t(__ffs(~b)) - 1u;
+            gap = true;
+          }
+        }
+      }
+      if (ready == 0) {
+        __nanosleep(backoff);
+        backoff = backoff < 256 ? backoff * 2 : 256;
+        continue;
+      }
+      backoff = 32;
+      uint32_t sc[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) sc[k] = 32u * k + lane < ready ? v[k] : 0u;
 #pragma unroll
       for (int dd = 1; dd < 32; dd <<= 1) {
 #pragma unroll
@@ -402,12 +446,19 @@ static __device__ __noinline__ void cx_sweep(const uint64_t *desc_c, uint32_t nt
       }
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        const uint32_t idx = f + lane + 32u * k;
-        if (idx < t1) st_relaxed_gpu(pref + idx, pack_desc(epoch, kStPrefix, run + sc[k] - v[k]));
+        const uint32_t j = 32u * k + lane;
+        if (j < ready) st_relaxed_gpu(pref + f + j, pack_desc(epoch, kStPrefix, run + sc[k] - v[k]));
         run += __shfl_sync(kFull, sc[k], 31);
       }
+      f += ready;
     }
-    before += all;
+    // the next round starts after every other rank's total of this one (this
+    // rank's own is `run - start`; the totaler publishes it for the others)
+    uint32_t others = 0;
+    for (uint32_t q = lane; q < world; q += 32)
+      if (q != rank) others += cx_poll(pa, bank, q, r, tag, failed);
+    others = __reduce_add_sync(kFull, others);
+    before = run + others - lower;
   }
   if (__any_sync(kFull, failed) && lane == 0) *pa.err = 1u;
 }
@@ -440,7 +491,8 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
                      uint64_t *__restrict__ count, uint64_t *__restrict__ desc,
                      TileHeader *__restrict__ hdr, uint32_t head, bool vec_out,
                      PeerArgs pa, uint32_t round_tiles, uint32_t rounds) {
-  static_assert(!CX || (!COMPACT && !PX && WF_TM_SWEEP), "CX: the sweeper scan only");
+  static_assert(!CX || (!COMPACT && !PX && WF_TM_SWEEP && NAG == 2 && W_TOTAL < W_AGG2),
+                "CX: the sweeper scan only, with a spare warp for the round totals");
   // `head` (0-3): the buffers were rounded down to 16 B, so virtual elements
   // [0, head) precede the caller's data; they read as 0 (neutral for the sum,
   // never selected) and are never stored.  Only tile 0 is affected.
@@ -974,6 +1026,12 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
       if (!__any_sync(kFull, polled)) __nanosleep(64);  // nothing parked: do not hammer smem
       __syncwarp();
     }
+  } else if (CX && warp == W_TOTAL) {
+    // ---------------------------- round totaler ---------------------------
+    // (CX, CTA 0) this rank's total of every round, published to all ranks as
+    // soon as the round's aggregates are in — independent of any other rank,
+    // so the ranks' rounds never chain
+    if (blockIdx.x == 0) cx_totals(desc, ntiles, epoch, pa, round_tiles, rounds);
   } else if (warp == W_SWEEP) {
     // ------------------------------- sweeper ------------------------------
     // One warp of CTA 0 turns the aggregates into exclusive prefixes in tile
