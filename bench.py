@@ -46,6 +46,10 @@ BLOCK_C2 = int(os.environ.get("WF_BENCH_BLOCK_C2", "256"))
 # (WF_FLAG_INPUT_STABLE: consecutive steps read one input that nothing
 # between them writes); WF_BENCH_PDL=0 measures plain stream-ordered launches
 PDL_STEPS = os.environ.get("WF_BENCH_PDL", "1") != "0"
+# C3 at N > 1: super-tile (round) size of the block-cyclic layout — 512 tiles,
+# a third of one GPU's on-chip pipeline (1776 tiles), so a rank keeps reading
+# while the lower ranks' round totals arrive
+C3_ROUND = 1 << 22
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 NOMINAL_HBM_GBS = 8000.0   # north_star / BASELINE.md §4: % of peak also vs 8.0 TB/s
 
@@ -238,6 +242,23 @@ def check_c3(y, x, world: int, rank: int) -> bool:
              - x[lo:hi].to(torch.int64)) % (1 << 32)
         ok &= int(d.count_nonzero()) == 0
     return bool(all_sum(torch.tensor([0 if ok else 1], device=x.device), world).item() == 0)
+
+
+def check_c3_cyclic(y, parts, world: int) -> bool:
+    """Block-cyclic scan: this rank's output == the global inclusive scan
+    (the whole synthetic array regenerated here, int64 cumsum wrapped to
+    int32) at its super-tiles' positions."""
+    import torch
+    from paper_2112_10034_b200 import ops
+    full = ops.fill_synthetic("i32_full", N_C3, seed=0, device=y.device)
+    want = torch.cumsum(full.to(torch.int64), 0).to(torch.int32)
+    del full
+    ok, off = True, 0
+    for start, m in parts:
+        ok &= torch.equal(y[off:off + m], want[start:start + m])
+        off += m
+    del want
+    return bool(all_sum(torch.tensor([0 if ok else 1], device=y.device), world).item() == 0)
 
 
 def check_c4(res, x, world: int, rank: int) -> bool:
@@ -811,16 +832,41 @@ def per_kernel(args, rank, world, local, dev, peak, checks: dict) -> dict:
         del graph
         del x1, flush_buf, tiny
     log(f"rank {rank}: C3")
-    # C3 scan
+    # C3 scan.  N > 1 with peer memory and a GPU per rank: block-cyclic
+    # super-tiles and the single-pass cross-rank scan (8 B/elem); otherwise
+    # contiguous shards and reduce-then-scan (12 B/elem at N > 1)
     lo, hi = wd.shard_range(N_C3, rank, world)
-    x = ops.fill_synthetic("i32_full", hi - lo, seed=0, base=lo, device=dev)
-    y = torch.empty_like(x)
-    scan = lambda: wd.scan_inclusive_i32(x, y, peer=pc, input_stable=PDL_STEPS)  # noqa: E731
+    cyclic = world > 1 and pc is not None and (
+        os.environ.get("WF_BENCH_SAME_GPU") != "1" or os.environ.get("WF_BENCH_CYCLIC") == "1")
+    if cyclic:
+        rounds, parts = wd.cyclic_rounds(N_C3, rank, world, C3_ROUND)
+        x = torch.empty(sum(m for _, m in parts), dtype=torch.int32, device=dev)
+        off = 0
+        for start, m in parts:  # this rank's super-tiles of the global synthetic array
+            ops.fill_synthetic("i32_full", m, seed=0, base=start, out=x[off:off + m])
+            off += m
+        y = torch.empty_like(x)
+        scan = lambda: pc.scan_inclusive_i32_cyclic(  # noqa: E731
+            x, y, C3_ROUND, rounds, input_stable=PDL_STEPS)
+    else:
+        x = ops.fill_synthetic("i32_full", hi - lo, seed=0, base=lo, device=dev)
+        y = torch.empty_like(x)
+        scan = lambda: wd.scan_inclusive_i32(x, y, peer=pc, input_stable=PDL_STEPS)  # noqa: E731
     clk = {}
     t = time_launches(scan, steps, warm, clocks=clk)
-    res["c3_scan_i32"] = stats(t, hi - lo, 8 if world == 1 else 12, N_C3)
+    res["c3_scan_i32"] = stats(t, x.numel(), 8 if world == 1 or cyclic else 12, N_C3)
     res["c3_scan_i32"]["clocks"] = clk
-    checks["c3_scan_i32"] = check_c3(scan(), x, world, rank)
+    res["c3_scan_i32"]["layout"] = (
+        f"block-cyclic super-tiles of {C3_ROUND} elements, single-pass scan with the round "
+        f"totals all-gathered inside the kernel (8 B/elem)" if cyclic else
+        "contiguous shards" + (", reduce-then-scan with a fused carry exchange (12 B/elem)"
+                               if world > 1 else ""))
+    if cyclic:
+        checks["c3_scan_i32"] = check_c3_cyclic(scan(), parts, world)
+        # C4 / C5 use contiguous shards
+        x = ops.fill_synthetic("i32_full", hi - lo, seed=0, base=lo, device=dev)
+    else:
+        checks["c3_scan_i32"] = check_c3(scan(), x, world, rank)
     log(f"rank {rank}: C4")
     # C4 compaction
     out = torch.empty_like(x)

@@ -127,6 +127,36 @@ def test_bench_n2_path_simulated(wd, monkeypatch):
 
 
 @pytest.mark.slow
+def test_bench_n2_cyclic_scan_two_processes_one_gpu():
+    """bench.py's C3 leg at N=2 on the block-cyclic single-pass scan, as two
+    real processes (torchrun, gloo, IPC mailboxes) time-slicing GPU 0: the
+    kernels wait on each other's round totals mid-kernel across contexts;
+    the check regenerates the global array and compares every super-tile."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, WF_BENCH_SAME_GPU="1", WF_BENCH_BACKEND="gloo", WF_BENCH_CYCLIC="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                        "--master-port", str(port), "bench.py", "--gpus", "2", "--steps", "3",
+                        "--warmup", "3", "--no-cpu-baseline"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    c3 = line["per_kernel"]["c3_scan_i32"]
+    assert c3["layout"].startswith("block-cyclic") and c3["bytes_per_elem"] == 8
+    assert line["verified"]["c3_scan_i32"] is True
+    assert all(line["verified"].values()), line["verified"]
+
+
+@pytest.mark.slow
 def test_bench_n2_two_processes_one_gpu():
     """bench.py at N=2 as the driver launches it (torchrun, one process per
     rank), with both ranks on GPU 0 over gloo (WF_BENCH_SAME_GPU): real
