@@ -41,6 +41,7 @@ from .config import LaunchConfig
 from .memory import DeviceMemory
 
 NOMINAL_HBM_GBS = 8000.0  # north_star's 8 TB/s
+C3_ROUND = 1 << 22        # block-cyclic super-tile of the sharded scan (bench.py C3_ROUND)
 L2_BYTES = 126 << 20      # B200 L2: inputs at or below this stay resident across repeats
 
 # Barrier-free kernels for the modes suite (the reference uses the same four
@@ -348,11 +349,10 @@ def bench_shards(worlds=(1, 2, 4, 8), log2_total=None, iters: int = 20, repeats:
         if op == "scan_inclusive_i32":
             if world == 1:
                 return lambda: ops.scan_inclusive_i32(x, y, input_stable=True)
-
-            def c3():
-                carry = pc.reduce_exscan_i32(x, input_stable=True)[:1]
-                ops.scan_inclusive_i32(x, y, carry=carry, input_stable=True)
-            return c3
+            # bench.py's N > 1 path: block-cyclic super-tiles, single pass
+            rounds = -(-x.numel() // C3_ROUND)
+            return lambda: pc.scan_inclusive_i32_cyclic(x, y, C3_ROUND, rounds,
+                                                        input_stable=True)
         if op == "compact_gt0_i32":
             if world == 1:
                 return lambda: ops.compact_gt0_i32(x, y, input_stable=True)
