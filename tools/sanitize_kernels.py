@@ -60,7 +60,15 @@ for _ in range(3):
     r.append(pc.compact_gt0_i32(x, input_stable=True)[1])
     r.append(pc.histogram256_u8(u, input_stable=True))
 r.append(y)
+# the block-cyclic single-pass scan (world 1: its totaler, sweeper and mailbox
+# rounds execute), plain and dependent, rounds of 16 tiles
+xc = ops.fill_synthetic("i32_full", 8192 * 16 * 5 + 8192 * 3, seed=9)
+yc = torch.empty_like(xc)
+for flag in (False, True):
+    pc.scan_inclusive_i32_cyclic(xc, yc, 8192 * 16, 6, input_stable=flag)
+r.append(yc)
 torch.cuda.synchronize()
+assert torch.equal(yc, torch.cumsum(xc.to(torch.int64), 0).to(torch.int32))
 assert not pc.failed()
 boxes[0].close()
 kboxes[0].close()
