@@ -143,3 +143,56 @@ def test_peer_mailbox_setup_failure_is_collective():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert out == {0: "raised LaunchError", 1: "raised LaunchError"}
+
+
+def _cyclic_worker(rank, world, port, n, round_elems, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rounds, parts = wd.cyclic_rounds(n, rank, world, round_elems)
+        full = synthetic.generate("i32_full", n, seed=8)
+        local = [full[s:s + m] for s, m in parts]
+        # every rank's total of every round (0 for rounds it has no data in):
+        # what the kernel's totaler publishes into the peer mailboxes
+        mine = np.zeros(rounds, dtype=np.int64)
+        for r, a in enumerate(local):
+            mine[r] = no.reduce_sum_i32(a) & 0xFFFFFFFF
+        totals = wd.exchange(torch.from_numpy(mine)).reshape(world, rounds).numpy()
+        # the sweeper's rule: round r starts at (all ranks' earlier rounds)
+        # + (lower ranks' round r)
+        out, before = [], 0
+        for r, a in enumerate(local):
+            start = (before + int(totals[:rank, r].sum())) & 0xFFFFFFFF
+            out.append((parts[r][0], no.scan_inclusive_i32(a, carry=np.int32(np.uint32(start)))))
+            before = (before + int(totals[:, r].sum())) & 0xFFFFFFFF
+        q.put((rank, rounds, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 5 * 4096 + 77), (3, 11 * 4096), (2, 4096)])
+def test_cyclic_scan_combine_rule_two_ranks(world, n):
+    """The block-cyclic sharded scan's host layout (distributed.cyclic_rounds)
+    and the per-round combine rule its kernel implements, over a real gloo
+    process group: stitched back in global order the ranks' super-tiles equal
+    the global inclusive scan.  Every rank sees the same round count."""
+    round_elems = 4096
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_cyclic_worker, args=(r, world, port, n, round_elems, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert len({rounds for _, rounds, _ in got}) == 1
+    pieces = sorted((start, arr) for _, _, out in got for start, arr in out)
+    stitched = np.concatenate([arr for _, arr in pieces])
+    assert [s for s, _ in pieces] == list(range(0, n, round_elems))
+    full = synthetic.generate("i32_full", n, seed=8)
+    assert np.array_equal(stitched, no.scan_inclusive_i32(full))
+
