@@ -292,11 +292,25 @@ def bench_scaling(ops_=("reduce_sum_f32", "scan_inclusive_i32", "compact_gt0_i32
         gen = OPS[op][0]
         n = 1 << totals[op]
         lo, hi = wd.shard_range(n, rank, world)
-        x = ops.fill_synthetic(gen, hi - lo, seed=0, base=lo, device=dev)
-        outs = _outs(op, hi - lo, dev)
+        layout = "contiguous"
+        if op == "scan_inclusive_i32" and pc is not None:
+            # block-cyclic super-tiles, single-pass scan (as bench.py at N > 1)
+            rounds, parts = wd.cyclic_rounds(n, rank, world, C3_ROUND)
+            x = torch.empty(sum(m for _, m in parts), dtype=torch.int32, device=dev)
+            off = 0
+            for start, m in parts:
+                ops.fill_synthetic(gen, m, seed=0, base=start, out=x[off:off + m])
+                off += m
+            layout = f"block-cyclic ({C3_ROUND}-element super-tiles)"
+        else:
+            x = ops.fill_synthetic(gen, hi - lo, seed=0, base=lo, device=dev)
+        outs = _outs(op, x.numel(), dev)
         if op == "reduce_sum_f32":
             fn = (lambda: pr.reduce_sum_f32(x, block=512)) if pr is not None else \
                 (lambda: wd.reduce_sum_f32(x, group=group, block=512))
+        elif op == "scan_inclusive_i32" and pc is not None:
+            fn = lambda: pc.scan_inclusive_i32_cyclic(x, outs["out"], C3_ROUND,  # noqa: E731
+                                                      rounds)
         elif op == "scan_inclusive_i32":
             fn = lambda: wd.scan_inclusive_i32(x, outs["out"], group=group, peer=pc)  # noqa: E731
         elif op == "compact_gt0_i32":
@@ -310,7 +324,8 @@ def bench_scaling(ops_=("reduce_sum_f32", "scan_inclusive_i32", "compact_gt0_i32
             dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
         t = float(t.item())
         rows.append({"op": op, "n": n, "n_gpus": world, "scaling": "strong",
-                     "us": t * 1e6, "gelem_s": n / t / 1e9, "exchange": exchange})
+                     "us": t * 1e6, "gelem_s": n / t / 1e9, "exchange": exchange,
+                     "layout": layout})
         del x, outs
     failed = pc is not None and pc.failed()
     for closer in (pr, pc):
