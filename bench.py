@@ -810,6 +810,25 @@ def per_kernel(args, rank, world, local, dev, peak, checks: dict) -> dict:
         res["c1_reduce_i32"]["latency_context_us"] = {
             "k1_on_4_elements": round(statistics.mean(t0) * 1e3, 2),
             "torch_sum_same_input": round(statistics.mean(tl) * 1e3, 2)}
+        # end to end through the C-ABI host entry point (pinned host buffer ->
+        # H2D -> K1 -> D2H of the sum), the call a reference user makes
+        host1 = torch.empty(N_C1, dtype=torch.int32, pin_memory=True)
+        host1.copy_(x1)
+        want1 = int(ops.reduce_sum_i32(x1, block=256).item())
+        got1 = ops.reduce_sum_i32_host(host1, device=dev)  # warm (staging, streams)
+        e2e_t = []
+        for _ in range(max(20, steps)):
+            t1 = time.perf_counter()
+            got1 = ops.reduce_sum_i32_host(host1, device=dev)
+            e2e_t.append(time.perf_counter() - t1)
+        checks["e2e/c1"] = got1 == want1
+        e2e_s = statistics.median(e2e_t)
+        res["c1_reduce_i32"]["e2e"] = {
+            "value": round(N_C1 / e2e_s / 1e9, 4), "unit": "Gelem/s",
+            "path": "wf_reduce_sum_i32_host", "h2d_bytes_per_step": 4 * N_C1,
+            "d2h_bytes_per_step": 4, "ms_per_step": round(e2e_s * 1e3, 4),
+            "steps": len(e2e_t), "how": "median of synchronous calls, host clock"}
+        del host1
         # warm L2 (SURVEY §8d asks for cold and warm): the 4 MiB input stays
         # L2-resident and 20 launches are replayed from one CUDA graph, so
         # neither host launch cost nor HBM is in the number
