@@ -315,6 +315,7 @@ __device__ __forceinline__ uint32_t pref_offset(uint32_t ntiles) { return (ntile
 static __device__ __forceinline__ uint32_t cx_poll(const PeerArgs &pa, uint64_t bank,
                                                    uint32_t src, uint32_t round, uint32_t tag,
                                                    bool &failed) {
+  if (failed) return 0u;  // one missing peer costs one timeout, not one per round
   const uint64_t *slot = pa.mine + bank + src * pa.cap + round;
   uint64_t w = peer_ld_relaxed_sys(slot);
   uint32_t spins = 0;
@@ -398,6 +399,7 @@ static __device__ __noinline__ void cx_sweep(const uint64_t *desc_c, uint32_t nt
     uint32_t lower = 0;
     for (uint32_t q = lane; q < rank; q += 32) lower += cx_poll(pa, bank, q, r, tag, failed);
     lower = __reduce_add_sync(kFull, lower);
+    failed = __any_sync(kFull, failed);
     // sweep this rank's tiles of the round as their aggregates arrive
     const uint32_t start = before + lower;
     uint32_t run = start, backoff = 32;
@@ -458,9 +460,10 @@ static __device__ __noinline__ void cx_sweep(const uint64_t *desc_c, uint32_t nt
     for (uint32_t q = lane; q < world; q += 32)
       if (q != rank) others += cx_poll(pa, bank, q, r, tag, failed);
     others = __reduce_add_sync(kFull, others);
+    failed = __any_sync(kFull, failed);
     before = run + others - lower;
   }
-  if (__any_sync(kFull, failed) && lane == 0) *pa.err = 1u;
+  if (failed && lane == 0) *pa.err = 1u;
 }
 
 // PX (compaction only): the finisher warp of the last tile also runs the

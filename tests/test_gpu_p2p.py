@@ -149,6 +149,36 @@ def test_cyclic_scan_in_process(mods, world):
         boxes[0].close()
 
 
+def test_cyclic_scan_missing_peer_fails_loudly(mods):
+    """A rank whose peer never launches its half of the cyclic scan: the
+    sweeper's polls time out ONCE (not once per round), the kernel completes,
+    the rank's error word is set, and the device stays usable."""
+    import time
+    ops, p2p, wd = mods
+    dev = torch.device("cuda", 0)
+    round_elems = 8192 * 4
+    n = round_elems * 2 * 6
+    full = ops.fill_synthetic("i32_full", n, seed=5)
+    boxes = p2p.Mailboxes.local(2, dev, cap=64)
+    pcs = [p2p.PeerCollectives(boxes[r], r, 2, 64, dev) for r in range(2)]
+    rounds, parts = wd.cyclic_rounds(n, 1, 2, round_elems)
+    x = torch.cat([full[s:s + m] for s, m in parts])
+    torch.cuda.synchronize()
+    try:
+        t0 = time.perf_counter()
+        pcs[1].scan_inclusive_i32_cyclic(x, round_elems=round_elems, rounds=rounds)
+        torch.cuda.synchronize()
+        elapsed = time.perf_counter() - t0
+        assert pcs[1].failed()
+        assert elapsed < 30.0, elapsed  # one ~4 s timeout, not one per round
+        # the GPU is still fine
+        y = ops.scan_inclusive_i32(x)
+        assert torch.equal(y, torch.cumsum(x.to(torch.int64), 0).to(torch.int32))
+    finally:
+        torch.cuda.synchronize()
+        boxes[0].close()
+
+
 def _child_read_mailbox(handle: bytes, world: int, q) -> None:
     import ctypes as C
     import torch as T
