@@ -385,21 +385,25 @@ def cpu_baseline_kernel(kind: str, budget_s: float) -> dict:
 
 
 # ---- GPU timing helpers -----------------------------------------------------
-def time_launches(fn, steps: int, warmup: int, flush=None, clocks: dict | None = None):
+def time_launches(fn, steps: int, warmup: int, flush=None, clocks: dict | None = None,
+                  world: int = 1):
     """Per-launch times (ms) on the current stream.  Without a flush the
     `steps` launches run back to back between two events (the steady state of
     a stream of calls; inputs larger than L2 need no flush) and the average
     is returned for each; with a flush (C1) every launch is bracketed by its
     own events right after the L2 flush.  `clocks`: filled with the SM clock
     summary sampled during the back-to-back loop (K5 on random bytes can hit
-    the board's power cap)."""
+    the board's power cap).  `world` > 1 (a sharded leg every rank runs): a
+    barrier before the warm-up and before the timed loop, so no rank's fused
+    exchange waits inside the kernel for a rank still busy elsewhere (e.g.
+    the rank-0-only C1 leg) and the timed loops start together."""
     import torch
-    torch.cuda.synchronize()  # whatever wrote the inputs has finished (WF_FLAG_INPUT_STABLE)
+    barrier_sync(world)  # whatever wrote the inputs has finished (WF_FLAG_INPUT_STABLE)
     for _ in range(warmup):
         if flush is not None:
             flush()
         fn()
-    torch.cuda.synchronize()
+    barrier_sync(world)
     if flush is None:
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with ClockSampler(torch.cuda.current_device()) as clk:
@@ -872,7 +876,7 @@ def per_kernel(args, rank, world, local, dev, peak, checks: dict) -> dict:
         y = torch.empty_like(x)
         scan = lambda: wd.scan_inclusive_i32(x, y, peer=pc, input_stable=PDL_STEPS)  # noqa: E731
     clk = {}
-    t = time_launches(scan, steps, warm, clocks=clk)
+    t = time_launches(scan, steps, warm, clocks=clk, world=world)
     res["c3_scan_i32"] = stats(t, x.numel(), 8 if world == 1 or cyclic else 12, N_C3)
     res["c3_scan_i32"]["clocks"] = clk
     res["c3_scan_i32"]["layout"] = (
@@ -891,7 +895,7 @@ def per_kernel(args, rank, world, local, dev, peak, checks: dict) -> dict:
     out = torch.empty_like(x)
     compact = lambda: wd.compact_gt0_i32(x, out, peer=pc, input_stable=PDL_STEPS)  # noqa: E731
     clk = {}
-    t = time_launches(compact, steps, warm, clocks=clk)
+    t = time_launches(compact, steps, warm, clocks=clk, world=world)
     res["c4_compact_i32"] = stats(t, hi - lo, 6, N_C4)
     res["c4_compact_i32"]["clocks"] = clk
     checks["c4_compact_i32"] = check_c4(compact(), x, world, rank)
@@ -900,7 +904,7 @@ def per_kernel(args, rank, world, local, dev, peak, checks: dict) -> dict:
     variants = {}
     for permille in (0, 10, 1000):
         ops.fill_synthetic("i32_select", hi - lo, seed=0, base=lo, param=permille, out=x)
-        t = time_launches(compact, steps, warm)
+        t = time_launches(compact, steps, warm, world=world)
         ms = statistics.mean(t)
         bpe = 4 + 4 * permille / 1000
         checks[f"c4_compact_i32/{permille / 10:g}%"] = check_c4(compact(), x, world, rank)
@@ -923,7 +927,7 @@ def per_kernel(args, rank, world, local, dev, peak, checks: dict) -> dict:
     u = ops.fill_synthetic("u8_uniform", hi - lo, seed=0, base=lo, device=dev)
     hist = lambda: wd.histogram256_u8(u, peer=pc, input_stable=PDL_STEPS)  # noqa: E731
     clk = {}
-    t = time_launches(hist, steps, warm, clocks=clk)
+    t = time_launches(hist, steps, warm, clocks=clk, world=world)
     res["c5_hist_u8"] = stats(t, hi - lo, 1, N_C5)
     res["c5_hist_u8"]["clocks"] = clk
     checks["c5_hist_u8"] = check_c5(hist(), u, world)
@@ -932,7 +936,7 @@ def per_kernel(args, rank, world, local, dev, peak, checks: dict) -> dict:
     for gen in ("u8_const", "u8_geom"):
         ops.fill_synthetic(gen, hi - lo, seed=0, base=lo, out=u)
         clk = {}
-        t = time_launches(hist, steps, warm, clocks=clk)
+        t = time_launches(hist, steps, warm, clocks=clk, world=world)
         ms = statistics.mean(t)
         checks[f"c5_hist_u8/{gen}"] = check_c5(hist(), u, world)
         variants[gen] = {"kernel_us": round(ms * 1e3, 2),
