@@ -52,6 +52,26 @@ __device__ __forceinline__ void count_word(uint32_t *sh, uint32_t lane4, uint32_
 __device__ __forceinline__ void count_byte(uint32_t *sh, uint32_t lane4, uint32_t b) {
   atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(sh) + ((b << 8) | lane4)), 1u);
 }
+#elif WF_HIST_LOP3
+// (default) 32 KiB layout, byte offset (bin << 7) | (lane << 2) formed by ONE
+// 3-input LOP3 ((shifted word & 0x7f80) | lane*4: disjoint bits) after one
+// shift, the smem base in the ATOMS's uniform-register operand: SHF + LOP3 +
+// ATOMS per byte instead of SHF + LOP3 + IADD + ATOMS (the #else form).  The
+// loop is bound by shared-atomic wavefronts, but under the board power cap
+// fewer issued instructions per byte are measurably faster (2^32 bytes:
+// uniform 645.6 -> 634.7 us, all-equal 692-751 -> 642-676 us, geometric
+// 648-654 -> 628-647 us; alternating runs, tools/hist_probe.py)
+constexpr uint32_t kBinWords = 32;
+__device__ __forceinline__ void count_word(uint32_t *sh, uint32_t lane4, uint32_t w) {
+  char *base = reinterpret_cast<char *>(sh);
+  atomicAdd(reinterpret_cast<uint32_t *>(base + (((w << 7) & 0x7f80u) | lane4)), 1u);
+  atomicAdd(reinterpret_cast<uint32_t *>(base + (((w >> 1) & 0x7f80u) | lane4)), 1u);
+  atomicAdd(reinterpret_cast<uint32_t *>(base + (((w >> 9) & 0x7f80u) | lane4)), 1u);
+  atomicAdd(reinterpret_cast<uint32_t *>(base + (((w >> 17) & 0x7f80u) | lane4)), 1u);
+}
+__device__ __forceinline__ void count_byte(uint32_t *sh, uint32_t lane4, uint32_t b) {
+  atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(sh) + ((b << 7) | lane4)), 1u);
+}
 #else
 constexpr uint32_t kBinWords = WF_HIST_BINW;
 constexpr uint32_t kBinShift = WF_HIST_BINW == 64 ? 6 : 5;
@@ -82,7 +102,7 @@ __global__ void __launch_bounds__(BLOCK, 2048 / BLOCK)
   for (uint32_t i = threadIdx.x; i < 256 * kBinWords; i += BLOCK) sh[i] = 0u;
   __syncthreads();
 
-#if WF_HIST_PRMT
+#if WF_HIST_PRMT || WF_HIST_LOP3
   const uint32_t lane4 = (threadIdx.x & 31) << 2;
 #define WF_CNT4(w) count_word(sh, lane4, (w))
 #define WF_CNT1(b) count_byte(sh, lane4, (b))

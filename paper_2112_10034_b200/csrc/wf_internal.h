@@ -35,6 +35,9 @@ constexpr int kHistBlock = WF_HIST_BLOCK;
 #ifndef WF_HIST_PRMT
 #define WF_HIST_PRMT 0  // 1: 256 B bin stride, one PRMT per address (slower, wf_hist.cu)
 #endif
+#ifndef WF_HIST_LOP3
+#define WF_HIST_LOP3 1  // 32 KiB layout, address by one 3-input LOP3 (wf_hist.cu; 0: + IADD, 646 vs 635 us)
+#endif
 #ifndef WF_HIST_BINW
 #define WF_HIST_BINW 32  // words per bin row in the non-PRMT layout (32 or 64)
 #endif
