@@ -11,10 +11,10 @@ namespace wf {
 
 // Workspace layout: a 256-byte header followed by op-specific arrays.
 constexpr size_t kWsHeader = 256;
-// Scan / compaction workspaces have a larger header: bytes [256, 8192) hold
-// the two-pass kernel's per-chunk arrival counters (16 B apart), which no
-// other kernel writes, so they stay zero between launches whatever the
-// single-pass kernel left in the descriptor array behind the header.
+// Scan / compaction workspaces have a larger header: bytes [256, 8192) are
+// reserved for the two-pass variant build's per-chunk arrival counters (16 B
+// apart; tools/variants/wf_scan2p.cu) — no product kernel writes them, so a
+// workspace stays valid for either build.
 constexpr size_t kTileWsHeader = 8192;
 constexpr size_t kChunkCnt2P = 1024;  // [256, 1024): two-pass tickets
 constexpr uint32_t kMaxChunks2P = uint32_t((kTileWsHeader - kChunkCnt2P) / 16);
