@@ -953,6 +953,9 @@ def per_kernel(args, rank, world, local, dev, peak, checks: dict) -> dict:
             exchange += " — FAILED (peer timeout)"
         for k in ("c3_scan_i32", "c4_compact_i32", "c5_hist_u8"):
             res[k]["exchange"] = exchange
+        if cyclic:
+            res["c3_scan_i32"]["exchange"] = exchange.replace(
+                "C3: scan pass 1", "C3: round totals all-gathered by the scan kernel")
     # DRAM bytes per launch measured by ncu --set full at the 1-GPU BASELINE
     # size (profiles/ncu_traffic.json) next to the algorithmic bytes
     if world == 1:

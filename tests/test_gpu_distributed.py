@@ -127,11 +127,14 @@ def test_bench_n2_path_simulated(wd, monkeypatch):
 
 
 @pytest.mark.slow
-def test_bench_n2_cyclic_scan_two_processes_one_gpu():
-    """bench.py's C3 leg at N=2 on the block-cyclic single-pass scan, as two
-    real processes (torchrun, gloo, IPC mailboxes) time-slicing GPU 0: the
-    kernels wait on each other's round totals mid-kernel across contexts;
-    the check regenerates the global array and compares every super-tile."""
+@pytest.mark.parametrize("nproc", [2, 4, 8])
+def test_bench_cyclic_scan_processes_one_gpu(nproc):
+    """bench.py at N = 2 / 4 / 8 with C3 on the block-cyclic single-pass
+    scan, as real processes (torchrun, gloo, IPC mailboxes) time-slicing GPU
+    0: the kernels wait on each other's round totals mid-kernel across
+    contexts; every leg's result is checked (the C3 check regenerates the
+    global array and compares every super-tile).  The driver's 8-GPU
+    scaling run takes this code path with one GPU per rank."""
     import json
     import os
     import socket
@@ -144,16 +147,19 @@ def test_bench_n2_cyclic_scan_two_processes_one_gpu():
         port = s.getsockname()[1]
     env = dict(os.environ, WF_BENCH_SAME_GPU="1", WF_BENCH_BACKEND="gloo", WF_BENCH_CYCLIC="1")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
-                        "--master-port", str(port), "bench.py", "--gpus", "2", "--steps", "3",
-                        "--warmup", "3", "--no-cpu-baseline"],
+                        "--nproc-per-node", str(nproc), "--master-addr", "127.0.0.1",
+                        "--master-port", str(port), "bench.py", "--gpus", str(nproc),
+                        "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-shards"],
                        cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == nproc and line["config"]["parallelism"] == f"shard{nproc}"
     c3 = line["per_kernel"]["c3_scan_i32"]
     assert c3["layout"].startswith("block-cyclic") and c3["bytes_per_elem"] == 8
     assert line["verified"]["c3_scan_i32"] is True
     assert all(line["verified"].values()), line["verified"]
+    for k in ("c3_scan_i32", "c4_compact_i32", "c5_hist_u8"):
+        assert "FAILED" not in line["per_kernel"][k]["exchange"], line["per_kernel"][k]
 
 
 @pytest.mark.slow
