@@ -103,6 +103,15 @@ __device__ __forceinline__ uint32_t atom_add_relaxed_gpu(uint32_t *p, uint32_t v
   return old;
 }
 
+// 64-bit relaxed draw on a TileHeader read as one word {epoch:32 | ticket:32}
+// (little-endian: ticket in the low half): returns the launch's epoch with
+// the ticket in ONE L2 round trip (wf_scan_tmem.cu).
+__device__ __forceinline__ uint64_t atom_add_relaxed_gpu_u64(uint64_t *p, uint64_t v) {
+  uint64_t old;
+  asm volatile("atom.relaxed.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ void fence_acq_rel_gpu() {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
@@ -159,10 +168,11 @@ __device__ __forceinline__ uint64_t pack_desc(uint32_t epoch, uint32_t st,
 }
 
 // Workspace header of the look-back kernels (first 256 bytes of the ws).
-struct TileHeader {
+struct alignas(8) TileHeader {
   uint32_t ticket;  // dynamic tile-id counter, reset by the last CTA
   uint32_t epoch;   // launch epoch, bumped by the last CTA
 };
+static_assert(sizeof(TileHeader) == 8, "TileHeader is one 64-bit word {epoch, ticket}");
 
 // Thread 0 of every CTA: read the epoch, then take a ticket.  The CTA that
 // draws the last ticket knows every CTA has already read the epoch, so it can

@@ -551,8 +551,18 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
   // previous grid on the stream has completed and flushed (returns at once
   // for an ordinary stream-ordered launch).
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (warp == W_PROD && lane == 0)
-    sh.epoch = ld_volatile_u32(&hdr->epoch) & kEpochMask;  // before this CTA's first (release) draw
+  // The CTA's first ticket draw returns the launch epoch with it: the header
+  // is one 64-bit word {epoch | ticket}, so one L2 round trip instead of an
+  // epoch read ordered before the draw (a draw can only see this launch's
+  // epoch: the reset for the next launch needs every CTA's last draw, and
+  // this one precedes that CTA's last)
+  uint64_t *const hdr64 = reinterpret_cast<uint64_t *>(hdr);
+  uint32_t first = 0;
+  if (warp == W_PROD && lane == 0) {
+    const uint64_t w = atom_add_relaxed_gpu_u64(hdr64, kBatch);
+    first = uint32_t(w);
+    sh.epoch = uint32_t(w >> 32) & kEpochMask;
+  }
   __syncthreads();
   const uint32_t epoch = sh.epoch;
 
@@ -568,11 +578,11 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
     auto failing = [&](uint32_t base) {  // each CTA examines exactly one failing draw
       if (base == (nbatches + gridDim.x - 1) * kBatch) {  // last of all draws: reset for the next launch
         fence_acq_rel_gpu();
-        atomicExch(&hdr->ticket, 0u);
-        atomicExch(&hdr->epoch, (epoch + 1) & kEpochMask);
+        atomicExch(reinterpret_cast<unsigned long long *>(hdr64),
+                   (unsigned long long)((epoch + 1) & kEpochMask) << 32);
       }
     };
-    uint32_t cur = lane == 0 ? atom_add_acq_rel_gpu(&hdr->ticket, kBatch) : 0u;  // after the epoch read
+    uint32_t cur = first;
     uint32_t nxt = 0, j = 0;
 #if WF_TM_PROF
     unsigned long long acc[3] = {0, 0, 0};
@@ -589,7 +599,7 @@ __global__ void __launch_bounds__(TM_THREADS, WF_TM_MINB)
           if (cur >= ntiles) {
             failing(cur);
           } else {
-            nxt = atom_add_relaxed_gpu(&hdr->ticket, kBatch);  // examined at the end of this batch
+            nxt = uint32_t(atom_add_relaxed_gpu_u64(hdr64, kBatch));  // examined at the end of this batch
             t = cur;
           }
         } else {
