@@ -174,6 +174,8 @@ struct alignas(8) TileHeader {
 };
 static_assert(sizeof(TileHeader) == 8, "TileHeader is one 64-bit word {epoch, ticket}");
 
+// (Round-1 variant kernels, tools/variants/; the product TMEM kernel draws
+// ticket and epoch in one 64-bit atomic instead.)
 // Thread 0 of every CTA: read the epoch, then take a ticket.  The CTA that
 // draws the last ticket knows every CTA has already read the epoch, so it can
 // reset the counter and bump the epoch for the next stream-ordered launch.
