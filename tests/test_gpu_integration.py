@@ -69,3 +69,17 @@ def test_integration_stub_matches_reference_oracle(warpfold):
     run_oracle(kernel, cfg, bind_args(kernel.params, mem, [a, out, n]))
     ref = int(mem.view(out, "i32").astype(np.int64).sum()) & 0xFFFFFFFF
     assert ns["reduce_sum_i32"](mem, a, n) & 0xFFFFFFFF == ref
+
+
+def test_c_consumer_host_paths_end_to_end(tmp_path):
+    """A plain C program (tests/c_consumer/abi_consumer.c) drives the
+    host-buffer entry points of C2-C5 through the header and the .so alone —
+    no Python or torch in that process — and checks every result against
+    serial C loops (fp32 sum exact by construction, wrapping int32 sum,
+    carried scan, ordered compaction, 256 bins)."""
+    import subprocess
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from test_host import build_c_consumer
+    r = subprocess.run([str(build_c_consumer(tmp_path)), "gpu"], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and r.stdout.strip() == "OK gpu", r.stdout + r.stderr

@@ -226,3 +226,27 @@ def test_refcheck_is_checker_only():
     imports = re.compile(r"^\s*(from\s+warpfold[\s.]|import\s+warpfold\b)", re.M)
     assert [p.name for p in pkg.rglob("*.py")
             if imports.search(p.read_text()) and p.name != "refcheck.py"] == []
+
+
+def build_c_consumer(tmp_path):
+    """tests/c_consumer/abi_consumer.c as a plain C99 program linked against
+    the library and the CUDA runtime (-Wall -Wextra -Werror: the header is
+    valid C)."""
+    import subprocess
+    exe = tmp_path / "abi_consumer"
+    lib_dir = _lib.lib_path().parent
+    cmd = ["gcc", "-std=c99", "-Wall", "-Wextra", "-Werror", "-O2", f"-I{ROOT / 'include'}",
+           str(ROOT / "tests" / "c_consumer" / "abi_consumer.c"), f"-L{lib_dir}",
+           f"-l:{_lib.lib_path().name}", f"-Wl,-rpath,{lib_dir}", "-L/usr/local/cuda/lib64",
+           "-lcudart", "-Wl,-rpath,/usr/local/cuda/lib64", "-o", str(exe)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_c_consumer_links_and_maps_errors(tmp_path):
+    """The boundary from C: no Python, no torch in the process."""
+    import subprocess
+    r = subprocess.run([str(build_c_consumer(tmp_path)), "cpu"], capture_output=True, text=True,
+                       timeout=120)
+    assert r.returncode == 0 and r.stdout.strip() == "OK cpu", r.stderr
