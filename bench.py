@@ -975,11 +975,14 @@ def per_kernel(args, rank, world, local, dev, peak, checks: dict) -> dict:
 def warpfold_python_sample(n: int = 1 << 20) -> dict | None:
     """The reference's OWN CPU path, unmodified: warpfold's
     launch(hybrid_transform(kernel)) (runtime/launch.py:90,
-    passes/pipeline.py:103) on the per-warp-partials fp32 kernel of SURVEY
-    §8c (tests/golden/C1_F32.spk), all host cores as fork workers, from the
-    copy installed in baseline/_ref.  Supplementary: the arm's `value` stays
-    the compiled restatement (orders of magnitude faster, so the conservative
-    denominator)."""
+    passes/pipeline.py:103) with all host cores as fork workers, from the
+    copy installed in baseline/_ref, on the formulations SURVEY §8(d) names:
+    the per-warp-partials reduction of §8c in fp32 (C2, the top-level
+    fields) and int32 (C1), and the lane-reversed warp prefix (C3, warp
+    level) — 2^20 elements each, results checked.  C4 / C5 have no reference
+    path (not expressible in its DSL).  Supplementary: the arm's `value`
+    stays the compiled restatement (orders of magnitude faster, so the
+    conservative denominator)."""
     ref = ROOT / "baseline" / "_ref"
     if not (ref / "warpfold").is_dir():
         return {"unavailable": "baseline/_ref/warpfold not installed"}
@@ -991,24 +994,47 @@ def warpfold_python_sample(n: int = 1 << 20) -> dict | None:
         from warpfold.runtime.launch import launch
         from oracle import synthetic
         workers = os.cpu_count() or 1
-        kernel = parse_module((ROOT / "tests" / "golden" / "C1_F32.spk").read_text()).kernel()
-        grid, block = 8 * workers, 256
-        cfg = LaunchConfig(grid_size=grid, block_size=block, warp_size=32, workers=workers)
-        mem = DeviceMemory()
-        a, out = mem.alloc(4 * n), mem.alloc(4 * grid * block // 32)
-        mem.view(a, "f32")[:] = synthetic.generate("f32_unit", n, seed=1)
-        prog = hybrid_transform(kernel, cfg)
-        t = time.perf_counter()
-        launch(prog, cfg, mem, [a, out, n])
-        el = time.perf_counter() - t
+        block = 256
+
+        def timed(spk, gen, dtype, grid, out_len, with_n):
+            kernel = parse_module((ROOT / "tests" / "golden" / spk).read_text()).kernel()
+            cfg = LaunchConfig(grid_size=grid, block_size=block, warp_size=32, workers=workers)
+            mem = DeviceMemory()
+            a, out = mem.alloc(4 * n), mem.alloc(4 * out_len)
+            x = synthetic.generate(gen, n, seed=1)
+            mem.view(a, dtype)[:] = x
+            prog = hybrid_transform(kernel, cfg)
+            t = time.perf_counter()
+            launch(prog, cfg, mem, [a, out, n] if with_n else [a, out])
+            el = time.perf_counter() - t
+            row = {"value": round(n / el / 1e9, 9), "unit": "Gelem/s", "cores": workers,
+                   "kind": "reference", "sample": f"one launch over 2^{n.bit_length() - 1} {dtype} "
+                   f"elements ({spk}), grid {grid} x block {block}, {workers} fork workers, "
+                   f"{el:.2f} s"}
+            return row, x, np.array(mem.view(out, dtype))
+
+        grid = 8 * workers
+        res, x, parts = timed("C1_F32.spk", "f32_unit", "f32", grid, grid * block // 32, True)
         total = np.float32(0)
-        for v in mem.view(out, "f32"):
+        for v in parts:
             total = np.float32(total + v)
-        return {"value": round(n / el / 1e9, 9), "unit": "Gelem/s", "cores": workers,
-                "kind": "reference",
-                "sample": f"one launch over 2^{n.bit_length() - 1} fp32 elements, grid {grid} x "
-                          f"block {block}, {workers} fork workers, {el:.2f} s",
-                "result": float(total)}
+        res["result"] = float(total)
+        rows = {"c2_reduce_f32": dict(res)}
+        row, x, parts = timed("C1_I32.spk", "i32_full", "i32", grid, grid * block // 32, True)
+        want = int(x.astype(np.int64).sum()) & 0xFFFFFFFF
+        row["checked"] = (int(parts.astype(np.int64).sum()) & 0xFFFFFFFF) == want
+        rows["c1_reduce_i32"] = row
+        row, x, y = timed("C3_WARP_PREFIX.spk", "i32_full", "i32", n // block, n, False)
+        w = x.astype(np.int64).reshape(-1, 32)
+        want_p = np.cumsum(w, axis=1)  # per-warp inclusive prefix (lane-reversed suffix scan)
+        row["checked"] = bool(np.array_equal(y.astype(np.int64).reshape(-1, 32) & 0xFFFFFFFF,
+                                             want_p & 0xFFFFFFFF))
+        rows["c3_warp_prefix_i32"] = row
+        rows["c4_compact_i32"] = rows["c5_hist_u8"] = {
+            "unavailable": "no reference path: not expressible in the reference DSL "
+                           "(no ballot / atomics / u8, dsl/lexer.py:18-25, dsl/parser.py:83-88)"}
+        res["per_kernel"] = rows
+        return res
     except Exception as e:  # the supplementary leg never fails the arm
         return {"unavailable": f"{type(e).__name__}: {e}"}
 
